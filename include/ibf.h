@@ -1,0 +1,218 @@
+/*
+ * ibf.h — C ABI of libibf.so, the B200 (sm_100a) hot path of the barrier-free
+ * augmented-Lagrangian elastodynamics solver (arXiv 2512.12151).
+ *
+ * The reference (`intact`, pure Python + numpy) has no FFI; its hot path sits
+ * behind plain Python function seams.  Each entry point below replaces one of
+ * those seams (paths relative to /root/reference/pkg/src) and keeps its
+ * argument meaning and error behaviour; INTEGRATION.md shows the ctypes
+ * binding a maintainer of `intact` would add.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  "dev" pointers are CUDA device memory,
+ *    "host" pointers are host memory.  Vectors of points are (n,3) float64
+ *    row-major, exactly the reference's state layout (intact/mesh.py:52-60).
+ *  - Every call is asynchronous on the given stream unless it returns a host
+ *    scalar, in which case it synchronises that stream before returning.
+ *  - Every call returns an ibf_status; on failure ibf_last_error() holds a
+ *    message.  No exception crosses the ABI.  IBF_ERR_NONFINITE maps to the
+ *    reference's NonFiniteEnergyError (intact/solver.py:35-37).
+ *  - Handles are not re-entrant; one stream per handle.
+ */
+#ifndef IBF_H
+#define IBF_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* ibf_stream;   /* == cudaStream_t */
+
+typedef enum {
+    IBF_OK = 0,
+    IBF_ERR_BAD_ARG = 1,
+    IBF_ERR_CUDA = 2,
+    IBF_ERR_OOM = 3,
+    IBF_ERR_NONFINITE = 4,   /* NonFiniteEnergyError, intact/solver.py:35 */
+    IBF_ERR_NO_DEVICE = 5
+} ibf_status;
+
+/* material models — MaterialModel, intact/elasticity.py:31-35 */
+enum { IBF_SNH = 0, IBF_NH = 1, IBF_COR = 2, IBF_LIN = 3 };
+/* pair kinds — PairKind, intact/distance.py:28-30 */
+enum { IBF_VF = 0, IBF_EE = 1 };
+
+const char* ibf_version(void);
+const char* ibf_last_error(void);
+
+/* ------------------------------------------------------------------ geometry */
+
+/* Batched pair distance: d (n), grad (n,12), weights (n,4), degenerate (n).
+ * Replaces vf_eval / ee_eval + _finish (intact/distance.py:153-189).
+ * pts: (n,4,3) dev. Bit-identical to the reference on the build host. */
+int ibf_pair_eval(int kind, int64_t n, const double* pts, double* d, double* grad,
+                  double* weights, uint8_t* degenerate, ibf_stream s);
+
+/* Additive-CCD TOI per pair in [0,1]. Replaces accd_batch (intact/ccd.py:37-91).
+ * x0, x1: (n,4,3) dev; toi: (n) dev. Bit-identical to the reference. */
+int ibf_accd(int kind, int64_t n, const double* x0, const double* x1, double min_gap,
+             double* toi, ibf_stream s);
+
+/* --------------------------------------------------------------- CCD handle */
+typedef struct ibf_ccd ibf_ccd;
+
+/* Surface primitives (host int64 arrays as System stores them,
+ * intact/stepper.py:103-113): tris (nt,3), edges (ne,2), verts (nv). */
+int ibf_ccd_create(int64_t n_tris, const int64_t* tris, int64_t n_edges, const int64_t* edges,
+                   int64_t n_verts, const int64_t* verts, ibf_ccd** out);
+void ibf_ccd_destroy(ibf_ccd* c);
+
+/* Broad phase only: replaces candidate_pairs (intact/ccd.py:113-145).
+ * Returns counts; fetch the pairs with ibf_ccd_get_candidates. Pairs are
+ * ordered (vertex, triangle) / (edge a, edge b) ascending — the set equals the
+ * reference's bit-exactly; the reference's order is its BVH frontier order. */
+int ibf_ccd_candidates(ibf_ccd* c, const double* x0, const double* x1, double min_gap,
+                       int64_t* n_vf, int64_t* n_ee, ibf_stream s);
+int ibf_ccd_get_candidates(ibf_ccd* c, int64_t* vf_host, int64_t* ee_host, ibf_stream s);
+
+/* Global step limit: replaces max_step_size (intact/ccd.py:168-193).
+ * alpha = min(cap, min TOI); the blocking pairs (TOI < 1, VF first then EE)
+ * stay on the device in the handle (ibf_ccd_blocking). */
+int ibf_max_step_size(ibf_ccd* c, const double* x, const double* x_hat, double min_gap,
+                      double cap, double* alpha_host, int64_t* n_blocking_host, ibf_stream s);
+/* Device views of the last blocking set: kinds (n) int32, quads (n,4) int32, tois (n). */
+int ibf_ccd_blocking(ibf_ccd* c, const int32_t** kinds, const int32_t** quads,
+                     const double** tois, int64_t* n);
+/* Host copy of the last blocking set (BlockingPairs, intact/ccd.py:148-165). */
+int ibf_ccd_get_blocking(ibf_ccd* c, int64_t* kinds, int64_t* quads, double* tois, ibf_stream s);
+
+/* ------------------------------------------------------------ active set */
+typedef struct ibf_contacts ibf_contacts;
+
+/* ActiveSet (intact/contact.py:154-261) as device SoA with insertion order. */
+int ibf_contacts_create(int64_t n_verts, int admit_all, ibf_contacts** out);
+void ibf_contacts_destroy(ibf_contacts* c);
+int64_t ibf_contacts_size(const ibf_contacts* c);
+/* ActiveSet.update(blocking) with the blocking set of a ccd handle
+ * (intact/contact.py:179-205). Returns (admitted, pruned) as the reference counts. */
+int ibf_contacts_update(ibf_contacts* c, const ibf_ccd* blocking, int64_t* admitted,
+                        int64_t* pruned, ibf_stream s);
+/* Same from explicit host arrays: kinds (n), quads (n,4), tois (n). */
+int ibf_contacts_update_host(ibf_contacts* c, int64_t n, const int64_t* kinds,
+                             const int64_t* quads, const double* tois, int64_t* admitted,
+                             int64_t* pruned, ibf_stream s);
+/* refresh_anchors (intact/contact.py:207-235); returns the degenerate count. */
+int ibf_contacts_refresh_anchors(ibf_contacts* c, const double* x, int64_t* n_degenerate,
+                                 ibf_stream s);
+/* dual_update_sweep (intact/contact.py:251-261); returns max |c| on the s == 0 branch. */
+int ibf_contacts_dual_sweep(ibf_contacts* c, const double* x_hat, double offset, double mu,
+                            double decay, double* worst_host, ibf_stream s);
+/* Host export/import of the SoA state (kind, quad(4), lam, gamma, s, anchor_d,
+ * anchor_grad(12), anchor_x(12)); import replaces the whole set (ActiveSet.add). */
+int ibf_contacts_export(const ibf_contacts* c, int64_t* kind, int64_t* quad, double* lam,
+                        double* gamma, double* s, double* anchor_d, double* anchor_grad,
+                        double* anchor_x, ibf_stream st);
+int ibf_contacts_import(ibf_contacts* c, int64_t n, const int64_t* kind, const int64_t* quad,
+                        const double* lam, const double* gamma, const double* s,
+                        const double* anchor_d, const double* anchor_grad,
+                        const double* anchor_x, ibf_stream st);
+
+/* --------------------------------------------------------- elastic system */
+typedef struct ibf_system ibf_system;
+
+/* System (intact/stepper.py:103-128) + ElasticRegion list (intact/solver.py:40-47):
+ * masses (n) host, dbc_mask (n) host (uint8), regions given as per-region
+ * (model, mu, lam, n_tets) with their tets (int64, global ids), shape_rows
+ * (m,4,3) and volumes (m) concatenated in region order.  Builds the static
+ * symmetric BSR pattern (diagonal + upper), the gather maps and workspaces. */
+int ibf_system_create(int64_t n_verts, const double* masses, const uint8_t* dbc_mask,
+                      int n_regions, const int* models, const double* mus,
+                      const double* lams, const int64_t* region_tets,
+                      const int64_t* tets, const double* shape_rows,
+                      const double* volumes, ibf_system** out);
+void ibf_system_destroy(ibf_system* s);
+/* pattern sizes: n_blocks = diagonal + strict-upper blocks */
+int ibf_system_pattern(const ibf_system* s, int64_t* n_blocks, int64_t* n_lower);
+
+/* assemble (intact/solver.py:109-156): gradient into grad (n,3) dev and the
+ * system matrix (mass + h^2 PSD elasticity + mu*gamma rank-one contact terms,
+ * DBC-masked) kept in the handle; contacts may be NULL. */
+int ibf_assemble(ibf_system* s, ibf_contacts* c, const double* x_hat, const double* x_tilde,
+                 double mu, double offset, double h, int apply_dbc, double* grad,
+                 ibf_stream st);
+/* y = H x with the last assembled matrix (BlockSparseMatrix.matvec,
+ * intact/sparse.py:64-73, contact part applied matrix-free). */
+int ibf_system_matvec(ibf_system* s, const double* x, double* y, ibf_stream st);
+/* Host copy of the elastic BSR (rows, cols, blocks) of the last assembly. */
+int ibf_system_export_bsr(ibf_system* s, int64_t* rows, int64_t* cols, double* blocks,
+                          ibf_stream st);
+
+/* pcg_solve on the last assembled matrix (intact/sparse.py:99-150).
+ * info_host = (iterations, converged, rel_residual). max_iters <= 0 -> 10 n. */
+int ibf_system_pcg(ibf_system* s, const double* rhs, double* x_out, double rel_tol,
+                   int64_t max_iters, double* info_host, ibf_stream st);
+
+/* incremental_energy (intact/solver.py:88-106) at x_hat + r_k p for k < n_r
+ * (p may be NULL -> x_hat itself); contacts frozen at their anchors. */
+int ibf_incremental_energy(ibf_system* s, ibf_contacts* c, const double* x_hat,
+                           const double* p, int n_r, const double* r_host,
+                           const double* x_tilde, double mu, double offset, double h,
+                           double* energies_host, ibf_stream st);
+
+/* min over regions of inversion_safe_step (intact/elasticity.py:337-356). */
+int ibf_inversion_safe_step(ibf_system* s, const double* x, const double* p, double* out_host,
+                            ibf_stream st);
+
+/* stiffness_diagonal_max (intact/stepper.py:191-200). */
+int ibf_stiffness_diagonal_max(ibf_system* s, const double* x, double h, double* out_host,
+                               ibf_stream st);
+
+/* solve_subproblem (intact/solver.py:178-233): Newton loop (cap 64, exit on a
+ * full step or zero gradient), PCG, descent safeguard, NH cap, strict-decrease
+ * backtracking, then one dual sweep.  x_hat: warm start in, result out.
+ * result_host = (newton_iters, cg_iters, stalled, worst_violation). */
+int ibf_solve_subproblem(ibf_system* s, ibf_contacts* c, const double* x_tilde,
+                         const double* x, double* x_hat, double mu, double offset, double h,
+                         double cg_tol, double decay, double* result_host, ibf_stream st);
+
+/* ------------------------------------------------------- step glue kernels */
+/* x_tilde = x + h v + h^2 g (intact/stepper.py:263) */
+int ibf_inertia_target(int64_t n, const double* x, const double* v, double h,
+                       const double* gravity3_host, double* x_tilde, ibf_stream st);
+/* clamp_state (intact/stepper.py:229-239), in place into x */
+int ibf_clamp_state(int64_t n, double* x, const double* x_hat, double alpha, ibf_stream st);
+/* out = a - b elementwise over n doubles (x_hat - x for the outer-pass cap,
+ * intact/stepper.py:308) */
+int ibf_vec_sub(int64_t n, const double* a, const double* b, double* out, ibf_stream st);
+/* v = (x - x_t) / h (intact/stepper.py:225-226) */
+int ibf_velocity_update(int64_t n, const double* x, const double* x_t, double h, double* v,
+                        ibf_stream st);
+
+/* ---------------------------------------------- standalone sparse matrices */
+typedef struct ibf_bsr ibf_bsr;
+/* BlockSparseMatrix(n, rows, cols, blocks) (intact/sparse.py:49-62): coalesces
+ * duplicate COO triplets; host inputs, blocks (nnz,3,3). */
+int ibf_bsr_create(int64_t n, int64_t nnz, const int64_t* rows, const int64_t* cols,
+                   const double* blocks, ibf_bsr** out);
+void ibf_bsr_destroy(ibf_bsr* m);
+int ibf_bsr_matvec(ibf_bsr* m, const double* x, double* y, ibf_stream st);
+/* mask_dirichlet (intact/sparse.py:81-87): vertex_mask (n) host, diag (n,3,3) host */
+int ibf_bsr_mask_dirichlet(ibf_bsr* m, const uint8_t* vertex_mask, const double* diag,
+                           ibf_stream st);
+/* coalesced block count and host copy (rows, cols, blocks (nb,3,3)) */
+int64_t ibf_bsr_size(const ibf_bsr* m);
+int ibf_bsr_export(const ibf_bsr* m, int64_t* rows, int64_t* cols, double* blocks, ibf_stream st);
+int ibf_bsr_pcg(ibf_bsr* m, const double* rhs, double* x_out, double rel_tol,
+                int64_t max_iters, double* info_host, ibf_stream st);
+
+/* Timing of the last PCG solve's SpMV launches (device ms and count), for the
+ * bench's roofline line. */
+int ibf_system_spmv_stats(const ibf_system* s, double* bytes_per_spmv);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* IBF_H */

@@ -1,0 +1,666 @@
+// Continuous collision detection on the device: swept-box LBVH broad phase,
+// bit-exact additive-CCD narrow phase, global step limit, blocking pairs.
+//
+// Replaces (paths relative to /root/reference/pkg/src):
+//   swept_boxes / AABBTree       intact/bvh.py:172-174, :54-154
+//   candidate_pairs              intact/ccd.py:113-145
+//   accd_batch                   intact/ccd.py:37-91
+//   max_step_size, BlockingPairs intact/ccd.py:148-193
+//   vf_eval / ee_eval            intact/distance.py:153-189
+//
+// Broad phase.  Boxes are the reference's swept (start U end) boxes with its
+// asymmetric pads (triangles +min_gap, vertices 0, edges 0.5*min_gap), in
+// FP64 — min/max/+-pad are exact, so the overlap set is bit-identical to the
+// reference's whatever tree is used.  Tree: Karras LBVH over 30-bit Morton
+// codes with the primitive index in the low 32 bits (unique keys), CUB radix
+// sort, bottom-up refit with arrival flags.  One thread per query traverses
+// with a private stack.
+//
+// Fused narrow-phase prefilter.  For max_step_size only pairs that can block
+// matter: a candidate whose starting gap is <= 0 has TOI 0, and one whose
+// motion bound l_p is below its gap keeps TOI 1 without advancement
+// (intact/ccd.py:64-68).  The traversal evaluates that test in place and
+// appends only the survivors (usually a tiny fraction), which are then sorted
+// (deterministic order) and advanced by one thread each.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <vector>
+
+#include "geometry.cuh"
+#include "internal.cuh"
+
+namespace ibf {
+
+using geo::V3;
+
+// ---------------------------------------------------------------- batched API kernels
+
+__global__ void k_pair_eval(int kind, int64_t n, const double* __restrict__ pts, double* __restrict__ d,
+                            double* __restrict__ grad, double* __restrict__ wts, uint8_t* __restrict__ degen) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    V3 P[4];
+    for (int k = 0; k < 4; ++k) P[k] = geo::ld3(pts + 12 * i + 3 * k);
+    double g[12], w[4];
+    bool dg;
+    const double dd = geo::pair_eval(kind, P, g, w, dg);
+    if (d) d[i] = dd;
+    if (grad)
+      for (int k = 0; k < 12; ++k) grad[12 * i + k] = g[k];
+    if (wts)
+      for (int k = 0; k < 4; ++k) wts[4 * i + k] = w[k];
+    if (degen) degen[i] = dg ? 1 : 0;
+  }
+}
+
+__global__ void k_accd_batch(int kind, int64_t n, const double* __restrict__ x0, const double* __restrict__ x1,
+                             double min_gap, double* __restrict__ toi) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    V3 A[4], B[4];
+    for (int k = 0; k < 4; ++k) {
+      A[k] = geo::ld3(x0 + 12 * i + 3 * k);
+      B[k] = geo::ld3(x1 + 12 * i + 3 * k);
+    }
+    toi[i] = geo::accd_toi(kind, A, B, min_gap);
+  }
+}
+
+// ---------------------------------------------------------------- boxes
+
+// swept boxes of primitives of arity K (1 point, 2 edge, 3 triangle)
+template <int K>
+__global__ void k_swept_boxes(int64_t n, const int* __restrict__ prims, const double* __restrict__ x0,
+                              const double* __restrict__ x1, double pad, double* __restrict__ lo,
+                              double* __restrict__ hi) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    for (int c = 0; c < 3; ++c) {
+      double l0 = INFINITY, h0 = -INFINITY, l1 = INFINITY, h1 = -INFINITY;
+      for (int k = 0; k < K; ++k) {
+        const int64_t v = prims[K * i + k];
+        const double a = x0[3 * v + c], b = x1[3 * v + c];
+        l0 = geo::np_min(l0, a);
+        h0 = geo::np_max(h0, a);
+        l1 = geo::np_min(l1, b);
+        h1 = geo::np_max(h1, b);
+      }
+      lo[3 * i + c] = geo::sub(geo::np_min(l0, l1), pad);
+      hi[3 * i + c] = geo::add(geo::np_max(h0, h1), pad);
+    }
+  }
+}
+
+// centre bounds for Morton normalisation: per-block partials
+__global__ void k_bounds(int64_t n, const double* __restrict__ lo, const double* __restrict__ hi,
+                         double* __restrict__ part) {
+  __shared__ double red[8];
+  double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    for (int c = 0; c < 3; ++c) {
+      const double ctr = 0.5 * (lo[3 * i + c] + hi[3 * i + c]);
+      if (ctr == ctr) {
+        mn[c] = fmin(mn[c], ctr);
+        mx[c] = fmax(mx[c], ctr);
+      }
+    }
+  for (int c = 0; c < 3; ++c) {
+    const double a = -block_max(-mn[c], red);
+    const double b = block_max(mx[c], red);
+    if (threadIdx.x == 0) {
+      part[6 * blockIdx.x + c] = a;
+      part[6 * blockIdx.x + 3 + c] = b;
+    }
+  }
+}
+
+__device__ __forceinline__ unsigned int spread10(unsigned int v) {
+  v &= 0x3ffu;
+  v = (v | (v << 16)) & 0x030000FFu;
+  v = (v | (v << 8)) & 0x0300F00Fu;
+  v = (v | (v << 4)) & 0x030C30C3u;
+  v = (v | (v << 2)) & 0x09249249u;
+  return v;
+}
+
+__global__ void k_morton(int64_t n, const double* __restrict__ lo, const double* __restrict__ hi,
+                         const double* __restrict__ part, int nparts, unsigned long long* __restrict__ keys) {
+  double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int b = 0; b < nparts; ++b)
+    for (int c = 0; c < 3; ++c) {
+      mn[c] = fmin(mn[c], part[6 * b + c]);
+      mx[c] = fmax(mx[c], part[6 * b + 3 + c]);
+    }
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    unsigned int q[3];
+    for (int c = 0; c < 3; ++c) {
+      const double span = mx[c] - mn[c];
+      const double ctr = 0.5 * (lo[3 * i + c] + hi[3 * i + c]);
+      double u = (span > 0.0 && ctr == ctr) ? (ctr - mn[c]) / span : 0.0;
+      u = fmin(fmax(u, 0.0), 1.0);
+      q[c] = (unsigned int)(u * 1023.0);
+    }
+    const unsigned long long code = (spread10(q[0]) << 2) | (spread10(q[1]) << 1) | spread10(q[2]);
+    keys[i] = (code << 32) | (unsigned long long)i;
+  }
+}
+
+// ---------------------------------------------------------------- LBVH (Karras 2012)
+
+__device__ __forceinline__ int delta(const unsigned long long* k, int n, int i, int j) {
+  if (j < 0 || j >= n) return -1;
+  return __clzll(k[i] ^ k[j]);
+}
+
+// internal nodes 0..n-2, leaves n-1..2n-2 (leaf n-1+i holds sorted slot i)
+__global__ void k_build(int n, const unsigned long long* __restrict__ k, int* __restrict__ left,
+                        int* __restrict__ right, int* __restrict__ parent) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n - 1; i += gridDim.x * blockDim.x) {
+    const int d = (delta(k, n, i, i + 1) - delta(k, n, i, i - 1)) >= 0 ? 1 : -1;
+    const int dmin = delta(k, n, i, i - d);
+    int lmax = 2;
+    while (delta(k, n, i, i + lmax * d) > dmin) lmax *= 2;
+    int l = 0;
+    for (int t = lmax / 2; t >= 1; t /= 2)
+      if (delta(k, n, i, i + (l + t) * d) > dmin) l += t;
+    const int j = i + l * d;
+    const int dnode = delta(k, n, i, j);
+    int s = 0;
+    int div = 2;
+    int t;
+    do {
+      t = (l + div - 1) / div;
+      if (delta(k, n, i, i + (s + t) * d) > dnode) s += t;
+      div *= 2;
+    } while (t > 1);
+    const int g = i + s * d + min(d, 0);
+    const int lc = (min(i, j) == g) ? (n - 1 + g) : g;
+    const int rc = (max(i, j) == g + 1) ? (n - 1 + g + 1) : g + 1;
+    left[i] = lc;
+    right[i] = rc;
+    parent[lc] = i;
+    parent[rc] = i;
+  }
+}
+
+__global__ void k_refit(int n, const unsigned long long* __restrict__ k, const double* __restrict__ plo,
+                        const double* __restrict__ phi, const int* __restrict__ left, const int* __restrict__ right,
+                        const int* __restrict__ parent, int* __restrict__ flag, double* __restrict__ nlo,
+                        double* __restrict__ nhi) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int prim = (int)(k[i] & 0xffffffffull);
+    int node = n - 1 + i;
+    for (int c = 0; c < 3; ++c) {
+      nlo[3 * node + c] = plo[3 * prim + c];
+      nhi[3 * node + c] = phi[3 * prim + c];
+    }
+    if (n == 1) continue;
+    __threadfence();
+    node = parent[node];
+    while (true) {
+      const int old = atomicAdd(flag + node, 1);
+      if (old == 0) break;  // first arrival: the sibling finishes this node
+      const int a = left[node], b = right[node];
+      for (int c = 0; c < 3; ++c) {
+        nlo[3 * node + c] = fmin(__ldcg(nlo + 3 * a + c), __ldcg(nlo + 3 * b + c));
+        nhi[3 * node + c] = fmax(__ldcg(nhi + 3 * a + c), __ldcg(nhi + 3 * b + c));
+      }
+      __threadfence();
+      if (node == 0) break;
+      node = parent[node];
+    }
+  }
+}
+
+struct Tree {
+  int n;
+  const unsigned long long* keys;  // sorted
+  const int* left;
+  const int* right;
+  const double* lo;
+  const double* hi;
+};
+
+__device__ __forceinline__ bool overlap(const double ql[3], const double qh[3], const double* lo, const double* hi) {
+  return ql[0] <= hi[0] && ql[1] <= hi[1] && ql[2] <= hi[2] && qh[0] >= lo[0] && qh[1] >= lo[1] && qh[2] >= lo[2];
+}
+
+struct TraverseArgs {
+  Tree tree;
+  int64_t nq;
+  const double* qlo;
+  const double* qhi;
+  int kind;            // 0: vertex-vs-triangle, 1: edge-vs-edge (a < b)
+  const int* qprim;    // verts (VF) or edges (EE)
+  const int* tprim;    // tris (VF) or edges (EE)
+  const double* x0;
+  const double* x1;
+  double min_gap;
+  int filter;          // 1: keep only pairs that can block (TOI 0 or needs advancement)
+  unsigned long long* out;
+  unsigned long long cap;
+  unsigned long long* counters;  // [0] emitted, [1] all candidates
+};
+
+__device__ __forceinline__ bool make_quad(const TraverseArgs& a, int qi, int pi, int q[4]) {
+  if (a.kind == 0) {
+    const int v = a.qprim[qi];
+    const int t0 = a.tprim[3 * pi], t1 = a.tprim[3 * pi + 1], t2 = a.tprim[3 * pi + 2];
+    if (v == t0 || v == t1 || v == t2) return false;
+    q[0] = v; q[1] = t0; q[2] = t1; q[3] = t2;
+    return true;
+  }
+  if (!(qi < pi)) return false;
+  const int a0 = a.qprim[2 * qi], a1 = a.qprim[2 * qi + 1];
+  const int b0 = a.tprim[2 * pi], b1 = a.tprim[2 * pi + 1];
+  if (a0 == b0 || a0 == b1 || a1 == b0 || a1 == b1) return false;
+  q[0] = a0; q[1] = a1; q[2] = b0; q[3] = b1;
+  return true;
+}
+
+__global__ void __launch_bounds__(128) k_traverse(TraverseArgs a) {
+  unsigned long long n_cand = 0;
+  for (int64_t qi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; qi < a.nq; qi += (int64_t)gridDim.x * blockDim.x) {
+    const double ql[3] = {a.qlo[3 * qi], a.qlo[3 * qi + 1], a.qlo[3 * qi + 2]};
+    const double qh[3] = {a.qhi[3 * qi], a.qhi[3 * qi + 1], a.qhi[3 * qi + 2]};
+    // LBVH depth is bounded by the 64 key bits, so depth+1 entries suffice
+    int stack[80];
+    int sp = 0;
+    stack[sp++] = 0;  // root: internal node 0, or the single leaf when n == 1
+    while (sp) {
+      const int node = stack[--sp];
+      if (!overlap(ql, qh, a.tree.lo + 3 * node, a.tree.hi + 3 * node)) continue;
+      if (node >= a.tree.n - 1) {
+        const int pi = (int)(a.tree.keys[node - (a.tree.n - 1)] & 0xffffffffull);
+        int q[4];
+        if (!make_quad(a, (int)qi, pi, q)) continue;
+        ++n_cand;
+        bool emit = true;
+        if (a.filter) {
+          V3 X0[4], X1[4];
+          for (int k = 0; k < 4; ++k) {
+            X0[k] = geo::ld3(a.x0 + 3 * (int64_t)q[k]);
+            X1[k] = geo::ld3(a.x1 + 3 * (int64_t)q[k]);
+          }
+          emit = geo::accd_class(a.kind, X0, X1, a.min_gap) != 1;
+        }
+        if (emit) {
+          const unsigned long long slot = atomicAdd(a.counters, 1ull);
+          if (slot < a.cap) a.out[slot] = ((unsigned long long)qi << 32) | (unsigned long long)pi;
+        }
+      } else {
+        stack[sp++] = a.tree.right[node];
+        stack[sp++] = a.tree.left[node];
+      }
+    }
+  }
+  if (n_cand) atomicAdd(a.counters + 1, n_cand);
+}
+
+__global__ void k_pair_toi(int64_t n, int kind, const unsigned long long* __restrict__ pairs,
+                           const int* __restrict__ qprim, const int* __restrict__ tprim,
+                           const double* __restrict__ x0, const double* __restrict__ x1, double min_gap,
+                           double* __restrict__ toi, int* __restrict__ quad_out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int qi = (int)(pairs[i] >> 32), pi = (int)(pairs[i] & 0xffffffffull);
+    int q[4];
+    if (kind == 0) {
+      q[0] = qprim[qi]; q[1] = tprim[3 * pi]; q[2] = tprim[3 * pi + 1]; q[3] = tprim[3 * pi + 2];
+    } else {
+      q[0] = qprim[2 * qi]; q[1] = qprim[2 * qi + 1]; q[2] = tprim[2 * pi]; q[3] = tprim[2 * pi + 1];
+    }
+    for (int k = 0; k < 4; ++k) quad_out[4 * i + k] = q[k];
+    if (toi) {
+      V3 A[4], B[4];
+      for (int k = 0; k < 4; ++k) {
+        A[k] = geo::ld3(x0 + 3 * (int64_t)q[k]);
+        B[k] = geo::ld3(x1 + 3 * (int64_t)q[k]);
+      }
+      toi[i] = geo::accd_toi(kind, A, B, min_gap);
+    }
+  }
+}
+
+__global__ void k_min_toi(int64_t n, const double* __restrict__ toi, double* __restrict__ out) {
+  __shared__ double red[8];
+  double v = INFINITY;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    v = fmin(v, toi[i]);
+  v = -block_max(-v, red);
+  if (threadIdx.x == 0 && v < INFINITY) atomic_min_nonneg(out, v);
+}
+
+__global__ void k_block_flag(int64_t n, const double* __restrict__ toi, int* __restrict__ flag) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    flag[i] = toi[i] < 1.0 ? 1 : 0;
+}
+
+__global__ void k_block_write(int64_t n, int64_t base, int kind, const int* __restrict__ flag,
+                              const int* __restrict__ pos, const int* __restrict__ quad, const double* __restrict__ toi,
+                              int* __restrict__ bkind, int* __restrict__ bquad, double* __restrict__ btoi) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    if (!flag[i]) continue;
+    const int64_t d = base + pos[i];
+    bkind[d] = kind;
+    for (int k = 0; k < 4; ++k) bquad[4 * d + k] = quad[4 * i + k];
+    btoi[d] = toi[i];
+  }
+}
+
+__global__ void k_set(double* p, double v) { *p = v; }
+
+static int grid_for(int64_t n, int threads = 256) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>(div_up(n, threads), 148LL * 16));
+}
+
+// Build the LBVH over n primitive boxes (c->box_lo/hi) into c's node arrays.
+static int build_tree(ibf_ccd* c, int64_t n, cudaStream_t s, Tree& t) {
+  const int nparts = (int)std::min<int64_t>(grid_for(n), 148 * 2);
+  IBF_TRY(c->dscratch.reserve(6 * (size_t)nparts + 8));
+  IBF_TRY(c->keys.reserve(n));
+  IBF_TRY(c->keys_sorted.reserve(n));
+  const int64_t nn = std::max<int64_t>(2 * n - 1, 1);
+  IBF_TRY(c->node_left.reserve(nn));
+  IBF_TRY(c->node_right.reserve(nn));
+  IBF_TRY(c->node_parent.reserve(nn));
+  IBF_TRY(c->node_flag.reserve(nn));
+  IBF_TRY(c->node_lo.reserve(3 * nn));
+  IBF_TRY(c->node_hi.reserve(3 * nn));
+  k_bounds<<<nparts, 256, 0, s>>>(n, c->box_lo.p, c->box_hi.p, c->dscratch.p);
+  IBF_LAUNCH_CHECK();
+  k_morton<<<grid_for(n), 256, 0, s>>>(n, c->box_lo.p, c->box_hi.p, c->dscratch.p, nparts, c->keys.p);
+  IBF_LAUNCH_CHECK();
+  size_t need = 0;
+  cub::DeviceRadixSort::SortKeys(nullptr, need, c->keys.p, c->keys_sorted.p, (int)n, 0, 64, s);
+  IBF_TRY(c->cub_tmp.reserve(need + 16));
+  size_t have = c->cub_tmp.cap;
+  IBF_CUDA(cub::DeviceRadixSort::SortKeys(c->cub_tmp.p, have, c->keys.p, c->keys_sorted.p, (int)n, 0, 64, s));
+  if (n > 1) {
+    k_build<<<grid_for(n - 1), 256, 0, s>>>((int)n, c->keys_sorted.p, c->node_left.p, c->node_right.p,
+                                             c->node_parent.p);
+    IBF_LAUNCH_CHECK();
+  }
+  IBF_CUDA(cudaMemsetAsync(c->node_flag.p, 0, nn * sizeof(int), s));
+  k_refit<<<grid_for(n), 256, 0, s>>>((int)n, c->keys_sorted.p, c->box_lo.p, c->box_hi.p, c->node_left.p,
+                                       c->node_right.p, c->node_parent.p, c->node_flag.p, c->node_lo.p, c->node_hi.p);
+  IBF_LAUNCH_CHECK();
+  t.n = (int)n;
+  t.keys = c->keys_sorted.p;
+  t.left = c->node_left.p;
+  t.right = c->node_right.p;
+  t.lo = c->node_lo.p;
+  t.hi = c->node_hi.p;
+  return IBF_OK;
+}
+
+// One broad-phase pass (VF or EE): boxes, tree, traversal with optional
+// prefilter, sort.  Result pairs in c->pairs_sorted[0..count).
+static int broad_pass(ibf_ccd* c, int kind, const double* x0, const double* x1, double min_gap, bool filter,
+                      int64_t* count, int64_t* n_candidates, cudaStream_t s) {
+  const int64_t nt = (kind == 0) ? c->nt : c->ne;
+  const int64_t nq = (kind == 0) ? c->nv : c->ne;
+  *count = 0;
+  *n_candidates = 0;
+  if (nt == 0 || nq == 0) return IBF_OK;
+  IBF_TRY(c->box_lo.reserve(3 * nt));
+  IBF_TRY(c->box_hi.reserve(3 * nt));
+  IBF_TRY(c->qlo.reserve(3 * nq));
+  IBF_TRY(c->qhi.reserve(3 * nq));
+  if (kind == 0) {
+    k_swept_boxes<3><<<grid_for(nt), 256, 0, s>>>(nt, c->tris.p, x0, x1, min_gap, c->box_lo.p, c->box_hi.p);
+    IBF_LAUNCH_CHECK();
+    k_swept_boxes<1><<<grid_for(nq), 256, 0, s>>>(nq, c->verts.p, x0, x1, 0.0, c->qlo.p, c->qhi.p);
+    IBF_LAUNCH_CHECK();
+  } else {
+    k_swept_boxes<2><<<grid_for(nt), 256, 0, s>>>(nt, c->edges.p, x0, x1, 0.5 * min_gap, c->box_lo.p, c->box_hi.p);
+    IBF_LAUNCH_CHECK();
+    IBF_CUDA(cudaMemcpyAsync(c->qlo.p, c->box_lo.p, 3 * nt * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    IBF_CUDA(cudaMemcpyAsync(c->qhi.p, c->box_hi.p, 3 * nt * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  }
+  Tree tree;
+  IBF_TRY(build_tree(c, nt, s, tree));
+  IBF_TRY(c->counters.reserve(4));
+  IBF_TRY(c->host.reserve(64));
+  if (c->pairs.cap < 4096) IBF_TRY(c->pairs.reserve(1 << 16));
+  for (int attempt = 0; attempt < 3; ++attempt) {
+    IBF_CUDA(cudaMemsetAsync(c->counters.p, 0, 2 * sizeof(unsigned long long), s));
+    TraverseArgs a;
+    a.tree = tree;
+    a.nq = nq;
+    a.qlo = c->qlo.p;
+    a.qhi = c->qhi.p;
+    a.kind = kind;
+    a.qprim = (kind == 0) ? c->verts.p : c->edges.p;
+    a.tprim = (kind == 0) ? c->tris.p : c->edges.p;
+    a.x0 = x0;
+    a.x1 = x1;
+    a.min_gap = min_gap;
+    a.filter = filter ? 1 : 0;
+    a.out = c->pairs.p;
+    a.cap = c->pairs.cap;
+    a.counters = c->counters.p;
+    k_traverse<<<grid_for(nq, 128), 128, 0, s>>>(a);
+    IBF_LAUNCH_CHECK();
+    unsigned long long* h = (unsigned long long*)c->host.p;
+    IBF_CUDA(cudaMemcpyAsync(h, c->counters.p, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    IBF_CUDA(cudaStreamSynchronize(s));
+    *count = (int64_t)h[0];
+    *n_candidates = (int64_t)h[1];
+    if (h[0] <= c->pairs.cap) break;
+    IBF_TRY(c->pairs.reserve((size_t)h[0]));
+  }
+  const int64_t cnt = *count;
+  IBF_TRY(c->pairs_sorted.reserve(std::max<int64_t>(cnt, 1)));
+  if (cnt) {
+    size_t need = 0;
+    cub::DeviceRadixSort::SortKeys(nullptr, need, c->pairs.p, c->pairs_sorted.p, (int)cnt, 0, 64, s);
+    IBF_TRY(c->cub_tmp.reserve(need + 16));
+    size_t have = c->cub_tmp.cap;
+    IBF_CUDA(cub::DeviceRadixSort::SortKeys(c->cub_tmp.p, have, c->pairs.p, c->pairs_sorted.p, (int)cnt, 0, 64, s));
+  }
+  return IBF_OK;
+}
+
+}  // namespace ibf
+
+using namespace ibf;
+
+extern "C" int ibf_pair_eval(int kind, int64_t n, const double* pts, double* d, double* grad, double* weights,
+                             uint8_t* degenerate, ibf_stream s) {
+  if (kind != 0 && kind != 1) {
+    set_error("ibf_pair_eval: kind must be 0 (VF) or 1 (EE)");
+    return IBF_ERR_BAD_ARG;
+  }
+  if (n <= 0) return IBF_OK;
+  k_pair_eval<<<grid_for(n), 256, 0, (cudaStream_t)s>>>(kind, n, pts, d, grad, weights, degenerate);
+  IBF_LAUNCH_CHECK();
+  return IBF_OK;
+}
+
+extern "C" int ibf_accd(int kind, int64_t n, const double* x0, const double* x1, double min_gap, double* toi,
+                        ibf_stream s) {
+  if (kind != 0 && kind != 1) {
+    set_error("ibf_accd: kind must be 0 (VF) or 1 (EE)");
+    return IBF_ERR_BAD_ARG;
+  }
+  if (n <= 0) return IBF_OK;
+  k_accd_batch<<<grid_for(n), 128, 0, (cudaStream_t)s>>>(kind, n, x0, x1, min_gap, toi);
+  IBF_LAUNCH_CHECK();
+  return IBF_OK;
+}
+
+extern "C" int ibf_ccd_create(int64_t n_tris, const int64_t* tris, int64_t n_edges, const int64_t* edges,
+                              int64_t n_verts, const int64_t* verts, ibf_ccd** out) {
+  if (n_tris < 0 || n_edges < 0 || n_verts < 0 || !out || n_tris >= (1LL << 31) || n_edges >= (1LL << 31)) {
+    set_error("ibf_ccd_create: bad arguments");
+    return IBF_ERR_BAD_ARG;
+  }
+  ibf_ccd* c = new ibf_ccd();
+  c->nt = n_tris;
+  c->ne = n_edges;
+  c->nv = n_verts;
+  std::vector<int> t(3 * n_tris), e(2 * n_edges), v(n_verts);
+  for (int64_t k = 0; k < 3 * n_tris; ++k) t[k] = (int)tris[k];
+  for (int64_t k = 0; k < 2 * n_edges; ++k) e[k] = (int)edges[k];
+  for (int64_t k = 0; k < n_verts; ++k) v[k] = (int)verts[k];
+  int st = c->tris.upload(t.data(), t.size());
+  if (st == IBF_OK) st = c->edges.upload(e.data(), e.size());
+  if (st == IBF_OK) st = c->verts.upload(v.data(), v.size());
+  if (st == IBF_OK && cudaDeviceSynchronize() != cudaSuccess) st = IBF_ERR_CUDA;
+  if (st != IBF_OK) {
+    delete c;
+    return st;
+  }
+  *out = c;
+  return IBF_OK;
+}
+
+extern "C" void ibf_ccd_destroy(ibf_ccd* c) { delete c; }
+
+// stored candidate quads (for ibf_ccd_get_candidates): reuse b_quad storage
+static ibf::DevBuf<int>& cand_store(ibf_ccd* c) { return c->b_pos; }
+
+extern "C" int ibf_ccd_candidates(ibf_ccd* c, const double* x0, const double* x1, double min_gap, int64_t* n_vf,
+                                  int64_t* n_ee, ibf_stream st) {
+  cudaStream_t s = (cudaStream_t)st;
+  int64_t cnt_vf = 0, cnt_ee = 0, all = 0;
+  IBF_TRY(broad_pass(c, 0, x0, x1, min_gap, false, &cnt_vf, &all, s));
+  DevBuf<int>& store = cand_store(c);
+  IBF_TRY(store.reserve(4 * std::max<int64_t>(cnt_vf, 1)));
+  if (cnt_vf) {
+    k_pair_toi<<<grid_for(cnt_vf), 256, 0, s>>>(cnt_vf, 0, c->pairs_sorted.p, c->verts.p, c->tris.p, x0, x1, 0.0,
+                                                 nullptr, store.p);
+    IBF_LAUNCH_CHECK();
+  }
+  // keep VF quads aside while EE runs
+  std::vector<int> vf_host(4 * cnt_vf);
+  if (cnt_vf)
+    IBF_CUDA(cudaMemcpyAsync(vf_host.data(), store.p, 4 * cnt_vf * sizeof(int), cudaMemcpyDeviceToHost, s));
+  IBF_TRY(broad_pass(c, 1, x0, x1, min_gap, false, &cnt_ee, &all, s));
+  IBF_TRY(store.reserve(4 * std::max<int64_t>(cnt_vf + cnt_ee, 1)));
+  IBF_CUDA(cudaStreamSynchronize(s));
+  if (cnt_vf) IBF_CUDA(cudaMemcpyAsync(store.p, vf_host.data(), 4 * cnt_vf * sizeof(int), cudaMemcpyHostToDevice, s));
+  if (cnt_ee) {
+    k_pair_toi<<<grid_for(cnt_ee), 256, 0, s>>>(cnt_ee, 1, c->pairs_sorted.p, c->edges.p, c->edges.p, x0, x1, 0.0,
+                                                 nullptr, store.p + 4 * cnt_vf);
+    IBF_LAUNCH_CHECK();
+  }
+  IBF_CUDA(cudaStreamSynchronize(s));
+  c->n_vf = cnt_vf;
+  c->n_ee = cnt_ee;
+  *n_vf = cnt_vf;
+  *n_ee = cnt_ee;
+  return IBF_OK;
+}
+
+extern "C" int ibf_ccd_get_candidates(ibf_ccd* c, int64_t* vf_host, int64_t* ee_host, ibf_stream st) {
+  cudaStream_t s = (cudaStream_t)st;
+  const int64_t tot = c->n_vf + c->n_ee;
+  std::vector<int> q(4 * tot);
+  if (tot) IBF_CUDA(cudaMemcpyAsync(q.data(), cand_store(c).p, 4 * tot * sizeof(int), cudaMemcpyDeviceToHost, s));
+  IBF_CUDA(cudaStreamSynchronize(s));
+  for (int64_t k = 0; k < 4 * c->n_vf; ++k) vf_host[k] = q[k];
+  for (int64_t k = 0; k < 4 * c->n_ee; ++k) ee_host[k] = q[4 * c->n_vf + k];
+  return IBF_OK;
+}
+
+extern "C" int ibf_max_step_size(ibf_ccd* c, const double* x, const double* x_hat, double min_gap, double cap,
+                                 double* alpha_host, int64_t* n_blocking_host, ibf_stream st) {
+  cudaStream_t s = (cudaStream_t)st;
+  IBF_TRY(c->dscratch.reserve(8));
+  IBF_TRY(c->host.reserve(64));
+  // survivors of both passes, kept in separate regions of b_* scratch
+  int64_t cnt[2] = {0, 0}, all[2] = {0, 0};
+  DevBuf<int>* quads = c->s_quad;
+  DevBuf<double>* tois = c->s_toi;
+  for (int kind = 0; kind < 2; ++kind) {
+    IBF_TRY(broad_pass(c, kind, x, x_hat, min_gap, true, &cnt[kind], &all[kind], s));
+    if (cnt[kind]) {
+      IBF_TRY(quads[kind].reserve(4 * cnt[kind]));
+      IBF_TRY(tois[kind].reserve(cnt[kind]));
+      k_pair_toi<<<grid_for(cnt[kind], 128), 128, 0, s>>>(
+          cnt[kind], kind, c->pairs_sorted.p, kind == 0 ? c->verts.p : c->edges.p, kind == 0 ? c->tris.p : c->edges.p,
+          x, x_hat, min_gap, tois[kind].p, quads[kind].p);
+      IBF_LAUNCH_CHECK();
+    }
+  }
+  // alpha = min(cap, min TOI over all candidates); non-survivors have TOI 1
+  double base = cap;
+  if ((all[0] + all[1]) > 0) base = std::min(base, 1.0);
+  k_set<<<1, 1, 0, s>>>(c->dscratch.p, INFINITY);
+  for (int kind = 0; kind < 2; ++kind)
+    if (cnt[kind]) {
+      k_min_toi<<<grid_for(cnt[kind]), 256, 0, s>>>(cnt[kind], tois[kind].p, c->dscratch.p);
+      IBF_LAUNCH_CHECK();
+    }
+  // blocking pairs (TOI < 1), VF first then EE, sorted order within kind
+  const int64_t tot = cnt[0] + cnt[1];
+  IBF_TRY(c->b_kind.reserve(std::max<int64_t>(tot, 1)));
+  IBF_TRY(c->b_quad.reserve(4 * std::max<int64_t>(tot, 1)));
+  IBF_TRY(c->b_toi.reserve(std::max<int64_t>(tot, 1)));
+  IBF_TRY(c->b_flag.reserve(tot + 2));
+  DevBuf<int>& pos = c->s_pos;
+  IBF_TRY(pos.reserve(tot + 2));
+  int* hcount = (int*)c->host.p;
+  int64_t nblock = 0;
+  for (int kind = 0; kind < 2; ++kind) {
+    const int64_t n = cnt[kind];
+    if (!n) continue;
+    k_block_flag<<<grid_for(n), 256, 0, s>>>(n, tois[kind].p, c->b_flag.p);
+    IBF_LAUNCH_CHECK();
+    IBF_CUDA(cudaMemsetAsync(c->b_flag.p + n, 0, sizeof(int), s));
+    size_t need = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, need, c->b_flag.p, pos.p, (int)(n + 1), s);
+    IBF_TRY(c->cub_tmp.reserve(need + 16));
+    size_t have = c->cub_tmp.cap;
+    IBF_CUDA(cub::DeviceScan::ExclusiveSum(c->cub_tmp.p, have, c->b_flag.p, pos.p, (int)(n + 1), s));
+    k_block_write<<<grid_for(n), 256, 0, s>>>(n, nblock, kind, c->b_flag.p, pos.p, quads[kind].p, tois[kind].p,
+                                              c->b_kind.p, c->b_quad.p, c->b_toi.p);
+    IBF_LAUNCH_CHECK();
+    IBF_CUDA(cudaMemcpyAsync(hcount, pos.p + n, sizeof(int), cudaMemcpyDeviceToHost, s));
+    IBF_CUDA(cudaStreamSynchronize(s));
+    nblock += hcount[0];
+  }
+  double mt = INFINITY;
+  IBF_CUDA(cudaMemcpyAsync(&mt, c->dscratch.p, sizeof(double), cudaMemcpyDeviceToHost, s));
+  IBF_CUDA(cudaStreamSynchronize(s));
+  *alpha_host = std::min(base, mt);
+  c->n_block = nblock;
+  *n_blocking_host = nblock;
+  return IBF_OK;
+}
+
+extern "C" int ibf_ccd_blocking(ibf_ccd* c, const int32_t** kinds, const int32_t** quads, const double** tois,
+                                int64_t* n) {
+  *kinds = c->b_kind.p;
+  *quads = c->b_quad.p;
+  *tois = c->b_toi.p;
+  *n = c->n_block;
+  return IBF_OK;
+}
+
+extern "C" int ibf_ccd_get_blocking(ibf_ccd* c, int64_t* kinds, int64_t* quads, double* tois, ibf_stream st) {
+  cudaStream_t s = (cudaStream_t)st;
+  const int64_t n = c->n_block;
+  if (!n) return IBF_OK;
+  std::vector<int> k(n), q(4 * n);
+  IBF_CUDA(cudaMemcpyAsync(k.data(), c->b_kind.p, n * sizeof(int), cudaMemcpyDeviceToHost, s));
+  IBF_CUDA(cudaMemcpyAsync(q.data(), c->b_quad.p, 4 * n * sizeof(int), cudaMemcpyDeviceToHost, s));
+  IBF_CUDA(cudaMemcpyAsync(tois, c->b_toi.p, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+  IBF_CUDA(cudaStreamSynchronize(s));
+  for (int64_t j = 0; j < n; ++j) {
+    kinds[j] = k[j];
+    for (int e = 0; e < 4; ++e) quads[4 * j + e] = q[4 * j + e];
+  }
+  return IBF_OK;
+}
+
+namespace ibf {
+int contacts_update_dev(ibf_contacts* c, int64_t nb, const int* bkind, const int* bquad, const double* btoi,
+                        int64_t* admitted, int64_t* pruned, cudaStream_t s);
+}
+
+extern "C" int ibf_contacts_update(ibf_contacts* c, const ibf_ccd* blocking, int64_t* admitted, int64_t* pruned,
+                                   ibf_stream st) {
+  const int64_t nb = blocking ? blocking->n_block : 0;
+  return contacts_update_dev(c, nb, nb ? blocking->b_kind.p : nullptr, nb ? blocking->b_quad.p : nullptr,
+                             nb ? blocking->b_toi.p : nullptr, admitted, pruned, (cudaStream_t)st);
+}

@@ -1,0 +1,160 @@
+// Shared internals of libibf.so: status plumbing, device buffers, deterministic
+// reductions.  sm_100a only.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/ibf.h"
+
+namespace ibf {
+
+void set_error(const std::string& msg);
+
+#define IBF_CUDA(call)                                                              \
+  do {                                                                              \
+    cudaError_t _e = (call);                                                        \
+    if (_e != cudaSuccess) {                                                        \
+      ::ibf::set_error(std::string(#call) + ": " + cudaGetErrorString(_e));         \
+      return _e == cudaErrorMemoryAllocation ? IBF_ERR_OOM : IBF_ERR_CUDA;          \
+    }                                                                               \
+  } while (0)
+
+#define IBF_TRY(call)                  \
+  do {                                 \
+    int _s = (call);                   \
+    if (_s != IBF_OK) return _s;       \
+  } while (0)
+
+#define IBF_LAUNCH_CHECK() IBF_CUDA(cudaGetLastError())
+
+// Growable device buffer owned by a handle.  Never shrinks; growth only
+// happens outside the timed hot loop once capacities settle.
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t cap = 0;
+  int reserve(size_t n) {
+    if (n <= cap) return IBF_OK;
+    size_t want = n + n / 4 + 64;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    IBF_CUDA(cudaMalloc(&p, want * sizeof(T)));
+    cap = want;
+    return IBF_OK;
+  }
+  // grow preserving contents (stream-ordered copy)
+  int grow_keep(size_t n, size_t used, cudaStream_t s) {
+    if (n <= cap) return IBF_OK;
+    size_t want = n + n / 2 + 64;
+    T* q = nullptr;
+    IBF_CUDA(cudaMalloc(&q, want * sizeof(T)));
+    if (p && used) IBF_CUDA(cudaMemcpyAsync(q, p, used * sizeof(T), cudaMemcpyDeviceToDevice, s));
+    if (p) {
+      IBF_CUDA(cudaStreamSynchronize(s));
+      cudaFree(p);
+    }
+    p = q;
+    cap = want;
+    return IBF_OK;
+  }
+  int upload(const T* host, size_t n, cudaStream_t s = 0) {
+    IBF_TRY(reserve(n ? n : 1));
+    if (n) IBF_CUDA(cudaMemcpyAsync(p, host, n * sizeof(T), cudaMemcpyHostToDevice, s));
+    return IBF_OK;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+  ~DevBuf() { release(); }
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+};
+
+// Pinned host scratch for scalar readbacks.
+struct HostScratch {
+  void* p = nullptr;
+  size_t cap = 0;
+  int reserve(size_t bytes) {
+    if (bytes <= cap) return IBF_OK;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    IBF_CUDA(cudaMallocHost(&p, bytes));
+    cap = bytes;
+    return IBF_OK;
+  }
+  ~HostScratch() {
+    if (p) cudaFreeHost(p);
+  }
+};
+
+int sm_count();
+inline int64_t div_up(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// ------------------------------------------------------------------ device side
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ double warp_min(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Deterministic block sum (fixed shuffle tree); result valid in every thread.
+// smem must hold blockDim.x/32 doubles; callers separate consecutive uses with
+// a __syncthreads (done at the end here).
+__device__ __forceinline__ double block_sum(double v, double* smem) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  v = warp_sum(v);
+  if (lane == 0) smem[warp] = v;
+  __syncthreads();
+  double r = (lane < nw) ? smem[lane] : 0.0;
+  r = warp_sum(r);
+  __syncthreads();
+  return r;
+}
+
+__device__ __forceinline__ double block_max(double v, double* smem) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  v = warp_max(v);
+  if (lane == 0) smem[warp] = v;
+  __syncthreads();
+  double r = (lane < nw) ? smem[lane] : -INFINITY;
+  r = warp_max(r);
+  __syncthreads();
+  return r;
+}
+
+// Sum of n partials in a fixed order by one warp (lane-strided, then tree).
+__device__ __forceinline__ double warp_sum_array(const double* a, int n) {
+  const int lane = threadIdx.x & 31;
+  double v = 0.0;
+  for (int i = lane; i < n; i += 32) v += a[i];
+  return warp_sum(v);
+}
+
+// atomicMin / atomicMax on non-negative doubles through their ordered bits.
+__device__ __forceinline__ void atomic_min_nonneg(double* addr, double v) {
+  atomicMin(reinterpret_cast<unsigned long long*>(addr), (unsigned long long)__double_as_longlong(v));
+}
+__device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
+  atomicMax(reinterpret_cast<unsigned long long*>(addr), (unsigned long long)__double_as_longlong(v));
+}
+
+}  // namespace ibf

@@ -1,0 +1,301 @@
+// The AL subproblem's Newton loop and the time-step glue kernels, plus the
+// library's infrastructure entry points.
+//
+// Replaces (paths relative to /root/reference/pkg/src):
+//   solve_subproblem    intact/solver.py:178-233
+//   line_search         intact/solver.py:159-175
+//   x_tilde / clamp_state / velocity_update
+//                       intact/stepper.py:263, :229-239, :225-226
+//
+// Host synchronisation: one device->host read per Newton iteration (PCG
+// count, trial energy, step cap and flags arrive together).  The PCG runs as
+// one persistent kernel; the inversion cap feeds the line search's first
+// trial on the device; the base energy of iteration k+1 is the accepted trial
+// energy of iteration k (bit-identical to re-evaluating it, since x_hat + r p
+// is formed the same way in both places).
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+
+#include "system.cuh"
+
+namespace ibf {
+
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+
+int sm_count() {
+  static int n = -1;
+  if (n < 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+  }
+  return n;
+}
+
+__global__ void k_neg(int64_t n, const double* __restrict__ a, double* __restrict__ b) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    b[i] = -a[i];
+}
+
+// out = sum a*b (fixed order: per-block partials, then one warp)
+__global__ void k_dot_part(int64_t n, const double* __restrict__ a, const double* __restrict__ b,
+                           double* __restrict__ part) {
+  __shared__ double red[8];
+  double v = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    v += a[i] * b[i];
+  v = block_sum(v, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = v;
+}
+
+// descent safeguard (intact/solver.py:216-220): if g.p >= 0, p = -P^-1 g
+__global__ void k_descent_fix(int64_t n, const double* __restrict__ part, int nparts, const double* __restrict__ g,
+                              const double* __restrict__ pinv, double* __restrict__ p) {
+  __shared__ double tot;
+  if (threadIdx.x < 32) {
+    const double v = warp_sum_array(part, nparts);
+    if (threadIdx.x == 0) tot = v;
+  }
+  __syncthreads();
+  if (!(tot >= 0.0)) return;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double* P = pinv + 9 * i;
+    const double g0 = g[3 * i], g1 = g[3 * i + 1], g2 = g[3 * i + 2];
+    p[3 * i] = -(P[0] * g0 + P[1] * g1 + P[2] * g2);
+    p[3 * i + 1] = -(P[3] * g0 + P[4] * g1 + P[5] * g2);
+    p[3 * i + 2] = -(P[6] * g0 + P[7] * g1 + P[8] * g2);
+  }
+}
+
+__global__ void k_first_step(const double* __restrict__ cap, double* __restrict__ r0) { *r0 = fmin(1.0, *cap); }
+
+// x <- x + r p exactly as numpy forms x_hat + r * p
+__global__ void k_step(int64_t n, double r, const double* __restrict__ p, double* __restrict__ x) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    x[i] = __dadd_rn(x[i], __dmul_rn(r, p[i]));
+}
+
+__global__ void k_inertia(int64_t n, const double* __restrict__ x, const double* __restrict__ v, double h, double gx,
+                          double gy, double gz, double* __restrict__ xt) {
+  const double h2 = __dmul_rn(h, h);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i % 3);
+    const double g = c == 0 ? gx : (c == 1 ? gy : gz);
+    xt[i] = __dadd_rn(__dadd_rn(x[i], __dmul_rn(h, v[i])), __dmul_rn(h2, g));
+  }
+}
+
+__global__ void k_clamp(int64_t n, double alpha, double* __restrict__ x, const double* __restrict__ xh) {
+  const double om = __dsub_rn(1.0, alpha);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double a = x[i], b = xh[i];
+    if (alpha >= 1.0) {
+      x[i] = b;
+    } else if (!(a == b)) {
+      x[i] = __dadd_rn(__dmul_rn(om, a), __dmul_rn(alpha, b));
+    }
+  }
+}
+
+__global__ void k_velocity(int64_t n, const double* __restrict__ x, const double* __restrict__ xt, double h,
+                           double* __restrict__ v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    v[i] = __dsub_rn(x[i], xt[i]) / h;
+}
+
+static int grid_for(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>(div_up(n, 256), 148LL * 8)); }
+
+int contacts_refresh(ibf_contacts* c, const double* x, int* degen_dev, cudaStream_t s);
+int contacts_dual(ibf_contacts* c, const double* x_hat, double offset, double mu, double decay, double* worst_dev,
+                  cudaStream_t s);
+
+}  // namespace ibf
+
+using namespace ibf;
+
+extern "C" const char* ibf_version(void) { return "ibf-b200 0.1 (sm_100a)"; }
+extern "C" const char* ibf_last_error(void) { return g_err.c_str(); }
+
+extern "C" int ibf_inertia_target(int64_t n, const double* x, const double* v, double h, const double* g3,
+                                  double* x_tilde, ibf_stream st) {
+  if (n <= 0) return IBF_OK;
+  k_inertia<<<grid_for(3 * n), 256, 0, (cudaStream_t)st>>>(3 * n, x, v, h, g3[0], g3[1], g3[2], x_tilde);
+  IBF_LAUNCH_CHECK();
+  return IBF_OK;
+}
+
+extern "C" int ibf_clamp_state(int64_t n, double* x, const double* x_hat, double alpha, ibf_stream st) {
+  if (n <= 0) return IBF_OK;
+  k_clamp<<<grid_for(3 * n), 256, 0, (cudaStream_t)st>>>(3 * n, alpha, x, x_hat);
+  IBF_LAUNCH_CHECK();
+  return IBF_OK;
+}
+
+extern "C" int ibf_velocity_update(int64_t n, const double* x, const double* x_t, double h, double* v, ibf_stream st) {
+  if (n <= 0) return IBF_OK;
+  k_velocity<<<grid_for(3 * n), 256, 0, (cudaStream_t)st>>>(3 * n, x, x_t, h, v);
+  IBF_LAUNCH_CHECK();
+  return IBF_OK;
+}
+
+extern "C" int ibf_system_spmv_stats(const ibf_system* s, double* bytes_per_spmv) {
+  // algorithmic bytes of one symmetric SpMV:
+  // 72 (N + E_u) + 4 E_u + 4 (N + 1) + 24 N + 24 N
+  const double N = (double)s->n, Eu = (double)s->nl;
+  *bytes_per_spmv = 72.0 * (N + Eu) + 4.0 * Eu + 4.0 * (N + 1.0) + 48.0 * N;
+  return IBF_OK;
+}
+
+extern "C" int ibf_solve_subproblem(ibf_system* s, ibf_contacts* c, const double* x_tilde, const double* x,
+                                    double* x_hat, double mu, double offset, double h, double cg_tol, double decay,
+                                    double* result_host, ibf_stream st) {
+  cudaStream_t stream = (cudaStream_t)st;
+  const int64_t n = s->n;
+  const int64_t n3 = 3 * n;
+  double* grad = s->vec_a.p;
+  double* p = s->vec_b.p;
+  double* rhs = s->vec_c.p;
+  // device scalars: [0..7] energies, [8] cap, [9] r0, [10] worst, [16..] dot partials
+  double* E = s->dscal.p;
+  double* cap = s->dscal.p + 8;
+  double* r0 = s->dscal.p + 9;
+  double* worst = s->dscal.p + 10;
+  const int dot_parts = 64;
+  IBF_TRY(s->dscal.reserve(16 + dot_parts + 8));
+  E = s->dscal.p;
+  cap = E + 8;
+  r0 = E + 9;
+  worst = E + 10;
+  double* dpart = E + 16;
+  IBF_TRY(s->host.reserve(256));
+  double* hd = (double*)s->host.p;      // hd[0..7] energies, hd[8] r0, hd[9..11] pcg info
+  int* hi = (int*)(hd + 16);            // hi[0] nonfinite, hi[1] grad nonzero
+  ibf_contacts* cc = (c && c->n) ? c : nullptr;
+  if (cc) {
+    IBF_TRY(c->iscratch.reserve(2));
+    IBF_CUDA(cudaMemsetAsync(c->iscratch.p, 0, sizeof(int), stream));
+    IBF_TRY(contacts_refresh(c, x, c->iscratch.p, stream));
+    IBF_TRY(contact_build_incidence(c, n, stream));
+  }
+  int newton = 0;
+  int64_t cg_total = 0;
+  bool stalled = false;
+  bool have_base = false;
+  double base = 0.0;
+  bool capped = true;
+  for (int it = 0; it < 64; ++it) {
+    IBF_TRY(system_assemble(s, cc, x_hat, x_tilde, mu, offset, h, true, grad, true, stream));
+    k_neg<<<grid_for(n3), 256, 0, stream>>>(n3, grad, rhs);
+    IBF_LAUNCH_CHECK();
+    IBF_TRY(pcg_solve(s->op(), rhs, p, cg_tol, 10 * n, s->work, stream));
+    k_dot_part<<<dot_parts, 256, 0, stream>>>(n3, grad, p, dpart);
+    IBF_LAUNCH_CHECK();
+    k_descent_fix<<<grid_for(n), 256, 0, stream>>>(n, dpart, dot_parts, grad, s->pinv.p, p);
+    IBF_LAUNCH_CHECK();
+    IBF_TRY(system_inversion_cap_launch(s, x_hat, p, cap, stream));
+    k_first_step<<<1, 1, 0, stream>>>(cap, r0);
+    IBF_LAUNCH_CHECK();
+    const double rs_first[2] = {1.0, 0.0};
+    const int T = have_base ? 1 : 2;  // second trial at r = 0 is the base energy
+    IBF_TRY(system_energy_launch(s, cc, x_hat, p, T, rs_first, r0, x_tilde, mu, offset, h, E, stream));
+    IBF_CUDA(cudaMemcpyAsync(hd, E, 2 * sizeof(double), cudaMemcpyDeviceToHost, stream));
+    IBF_CUDA(cudaMemcpyAsync(hd + 8, r0, sizeof(double), cudaMemcpyDeviceToHost, stream));
+    IBF_CUDA(cudaMemcpyAsync(hd + 9, s->work.info.p, 3 * sizeof(double), cudaMemcpyDeviceToHost, stream));
+    IBF_CUDA(cudaMemcpyAsync(hi, s->flags.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, stream));
+    IBF_CUDA(cudaStreamSynchronize(stream));
+    if (hi[0]) {
+      set_error("elastic energy is not finite at the evaluation point");
+      return IBF_ERR_NONFINITE;
+    }
+    if (!hi[1]) {  // not np.any(grad)
+      capped = false;
+      break;
+    }
+    cg_total += (int64_t)hd[9];
+    if (!have_base) base = hd[1];
+    const double rfirst = hd[8];
+    double r = rfirst, e_acc = hd[0];
+    bool stall = false;
+    if (!(hd[0] < base)) {
+      // backtracking: r0 / 2^k, k = 1..30, strict decrease (intact/solver.py:159-175)
+      double best_r = rfirst, best_e = INFINITY;
+      if (hd[0] < best_e) {
+        best_r = rfirst;
+        best_e = hd[0];
+      }
+      bool found = false;
+      int k = 1;
+      while (k <= 30 && !found) {
+        const int T2 = std::min(8, 31 - k);
+        double rs[8];
+        double sc = 1.0;
+        for (int j = 0; j < k; ++j) sc *= 0.5;
+        for (int j = 0; j < T2; ++j) {
+          rs[j] = sc;
+          sc *= 0.5;
+        }
+        IBF_TRY(system_energy_launch(s, cc, x_hat, p, T2, rs, r0, x_tilde, mu, offset, h, E, stream));
+        IBF_CUDA(cudaMemcpyAsync(hd, E, T2 * sizeof(double), cudaMemcpyDeviceToHost, stream));
+        IBF_CUDA(cudaStreamSynchronize(stream));
+        for (int j = 0; j < T2; ++j) {
+          const double rj = rfirst * rs[j];
+          if (hd[j] < base) {
+            r = rj;
+            e_acc = hd[j];
+            found = true;
+            break;
+          }
+          if (hd[j] < best_e) {
+            best_r = rj;
+            best_e = hd[j];
+          }
+        }
+        k += T2;
+      }
+      if (!found) {
+        r = best_r;
+        e_acc = best_e;
+        stall = true;
+      }
+    }
+    k_step<<<grid_for(n3), 256, 0, stream>>>(n3, r, p, x_hat);
+    IBF_LAUNCH_CHECK();
+    base = e_acc;
+    have_base = e_acc < INFINITY;  // stalled on all-inf trials: recompute next time
+    ++newton;
+    stalled = stalled || stall;
+    if (r == 1.0) {
+      capped = false;
+      break;
+    }
+  }
+  if (capped) stalled = true;
+  double w = 0.0;
+  if (cc) {
+    IBF_TRY(contacts_dual(c, x_hat, offset, mu, decay, worst, stream));
+    IBF_CUDA(cudaMemcpyAsync(hd, worst, sizeof(double), cudaMemcpyDeviceToHost, stream));
+    IBF_CUDA(cudaStreamSynchronize(stream));
+    w = hd[0];
+  }
+  result_host[0] = newton;
+  result_host[1] = (double)cg_total;
+  result_host[2] = stalled ? 1.0 : 0.0;
+  result_host[3] = w;
+  return IBF_OK;
+}
+
+namespace ibf {
+__global__ void k_sub(int64_t n, const double* __restrict__ a, const double* __restrict__ b, double* __restrict__ o) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    o[i] = __dsub_rn(a[i], b[i]);
+}
+}  // namespace ibf
+
+extern "C" int ibf_vec_sub(int64_t n, const double* a, const double* b, double* out, ibf_stream st) {
+  if (n <= 0) return IBF_OK;
+  ibf::k_sub<<<ibf::grid_for(n), 256, 0, (cudaStream_t)st>>>(n, a, b, out);
+  IBF_LAUNCH_CHECK();
+  return IBF_OK;
+}

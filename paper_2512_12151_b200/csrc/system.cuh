@@ -1,0 +1,56 @@
+// The elastic system handle (System + ElasticRegion list) and the contact
+// hooks the assembly needs.
+#pragma once
+
+#include "internal.cuh"
+
+struct ibf_system {
+  int64_t n = 0;        // vertices
+  int64_t m = 0;        // tets
+  int64_t n_tiles = 0;  // ceil(m / 32)
+  int n_regions = 0;
+  bool has_nh = false;
+  std::vector<ibf::RegionDev> regions_host;
+  ibf::DevBuf<ibf::RegionDev> regions;
+  ibf::DevBuf<int> tets;                 // (m,4) int32
+  ibf::DevBuf<double> shape_rows;        // (m,4,3)
+  ibf::DevBuf<double> volumes;           // (m)
+  ibf::DevBuf<double> masses;            // (n)
+  ibf::DevBuf<uint8_t> dbc;              // (n)
+  bool any_dbc = false;
+  // static symmetric BSR pattern (diagonal + strict upper), rows ascending
+  int64_t nb = 0, nl = 0;
+  std::vector<int64_t> rows_h, cols_h;
+  ibf::DevBuf<int> row_ptr, col, brow, low_ptr, low_blk, low_row, diag_blk;
+  ibf::DevBuf<int> blk_ptr, blk_src;     // block <- (tet*10+q) contributions, tet order
+  ibf::DevBuf<int> vt_ptr, vt_src;       // vertex <- (tet*4+l) incidences, tet order
+  // assembled state
+  ibf::DevBuf<double> val, pinv;         // (nb,9), (n,9)
+  ibf::DevBuf<double> elem_grad, elem_blk;  // tile-32 layouts
+  ibf::DevBuf<int> flags;                // [0] nonfinite energy, [1] gradient nonzero
+  ibf::DevBuf<double> dscal;             // device scalars
+  ibf::DevBuf<double> epart;             // energy partials
+  ibf::DevBuf<double> vec_a, vec_b, vec_c;   // (n,3) scratch
+  ibf::HostScratch host;
+  ibf::PcgWork work;
+  ibf_contacts* assembled_contacts = nullptr;  // contact term of the last assembly
+  bool assembled_dbc = false;
+  ibf::Operator op() const;
+};
+
+namespace ibf {
+// contact.cu
+int contact_prepare(ibf_contacts* c, const double* x_hat, double mu, double offset, cudaStream_t s);
+int contact_build_incidence(ibf_contacts* c, int64_t n_verts, cudaStream_t s);
+ContactView contact_view(ibf_contacts* c);
+
+// system.cu
+int system_assemble(ibf_system* s, ibf_contacts* c, const double* x_hat, const double* x_tilde, double mu,
+                    double offset, double h, bool apply_dbc, double* grad, bool contacts_ready,
+                    cudaStream_t st);
+int system_energy_launch(ibf_system* s, ibf_contacts* c, const double* x_hat, const double* p, int n_r,
+                         const double* r_host, const double* r0_dev, const double* x_tilde, double mu,
+                         double offset, double h, double* out_dev, cudaStream_t st);
+int system_inversion_cap_launch(ibf_system* s, const double* x, const double* p, double* out_dev,
+                                cudaStream_t st);
+}  // namespace ibf

@@ -1,0 +1,123 @@
+"""Tet meshes, rest data and simulation state (intact/mesh.py:23-152).
+
+One-time host-side preprocessing (out of the hot path): the outputs —
+shape rows, volumes, lumped masses, surface triangles/edges/vertices — are
+the inputs the device system is built from.  Same conventions as the
+reference so scenes built here and there are interchangeable.
+"""
+
+from __future__ import annotations
+
+import dataclasses
+import logging
+
+import numpy as np
+
+log = logging.getLogger(__name__)
+
+# faces opposite vertices 0..3 of a positively oriented tet, wound outward
+_TET_FACES = np.array([[1, 2, 3], [0, 3, 2], [0, 1, 3], [0, 2, 1]], dtype=np.int64)
+DEGENERATE_VOLUME_FRACTION = 1e-12
+
+
+class MeshError(ValueError):
+    """Malformed mesh input."""
+
+
+@dataclasses.dataclass
+class TetMesh:
+    rest_positions: np.ndarray
+    tets: np.ndarray
+    surface_tris: np.ndarray
+    surface_edges: np.ndarray
+    surface_verts: np.ndarray
+
+    @property
+    def n_verts(self) -> int:
+        return self.rest_positions.shape[0]
+
+    @property
+    def n_tets(self) -> int:
+        return self.tets.shape[0]
+
+
+@dataclasses.dataclass
+class RestData:
+    inv_rest_shape: np.ndarray
+    volumes: np.ndarray
+    shape_rows: np.ndarray
+    masses: np.ndarray
+
+
+@dataclasses.dataclass
+class SimState:
+    """Positions and velocities of every vertex, (n,3) float64 each."""
+
+    x: np.ndarray
+    v: np.ndarray
+
+    def copy(self) -> "SimState":
+        return SimState(self.x.copy(), self.v.copy())
+
+
+def tet_volumes(positions, tets):
+    p = positions[tets]
+    return np.linalg.det((p[:, 1:] - p[:, :1]).transpose(0, 2, 1)) / 6.0
+
+
+def surface_of(tets):
+    """Boundary faces (seen once), their unique sorted edges and vertices."""
+    if len(tets) == 0:
+        return (np.zeros((0, 3), dtype=np.int64), np.zeros((0, 2), dtype=np.int64),
+                np.zeros(0, dtype=np.int64))
+    faces = tets[:, _TET_FACES].reshape(-1, 3)
+    _, inv, cnt = np.unique(np.sort(faces, axis=1), axis=0, return_inverse=True, return_counts=True)
+    bnd = faces[cnt[inv.ravel()] == 1]
+    e = np.sort(bnd[:, [[0, 1], [1, 2], [2, 0]]].reshape(-1, 2), axis=1)
+    edges, ecnt = np.unique(e, axis=0, return_counts=True)
+    if (ecnt > 2).any():
+        log.warning("non-manifold surface: %d edge(s) shared by >2 boundary faces", int((ecnt > 2).sum()))
+    return bnd, edges, np.unique(bnd)
+
+
+def build_tet_mesh(positions, tets) -> TetMesh:
+    """Validate, re-orient negative tets, extract the surface."""
+    positions = np.ascontiguousarray(positions, dtype=np.float64)
+    tets = np.ascontiguousarray(tets, dtype=np.int64)
+    if positions.ndim != 2 or positions.shape[1] != 3:
+        raise MeshError(f"positions must be (n, 3), got {positions.shape}")
+    if tets.ndim != 2 or tets.shape[1] != 4:
+        raise MeshError(f"tets must be (m, 4), got {tets.shape}")
+    if tets.size and (tets.min() < 0 or tets.max() >= len(positions)):
+        raise MeshError("tet index out of range")
+    vols = tet_volumes(positions, tets)
+    neg = vols < 0.0
+    if neg.any():
+        tets = tets.copy()
+        tets[neg, 1], tets[neg, 2] = tets[neg, 2], tets[neg, 1].copy()
+        vols = np.abs(vols)
+    if tets.size:
+        floor = DEGENERATE_VOLUME_FRACTION * float(vols.mean())
+        bad = np.nonzero(vols <= floor)[0]
+        if bad.size:
+            raise MeshError(f"degenerate tet(s) {bad.tolist()[:8]}: volume <= {floor:.3e}")
+    t, e, v = surface_of(tets)
+    return TetMesh(positions, tets, t, e, v)
+
+
+def compute_rest_data(mesh: TetMesh, density: float) -> RestData:
+    """Dm^-1, volumes, shape rows A_i (dF = sum dx_i A_i), lumped masses."""
+    if density <= 0.0:
+        raise MeshError(f"density must be positive, got {density}")
+    p = mesh.rest_positions[mesh.tets]
+    dm = (p[:, 1:] - p[:, :1]).transpose(0, 2, 1)
+    vol = np.linalg.det(dm) / 6.0
+    inv = np.linalg.inv(dm)
+    rows = np.empty((mesh.n_tets, 4, 3))
+    rows[:, 1:] = inv
+    rows[:, 0] = -inv.sum(axis=1)
+    masses = np.zeros(mesh.n_verts)
+    np.add.at(masses, mesh.tets.ravel(), np.repeat(density * vol / 4.0, 4))
+    if mesh.n_tets and not (masses[np.unique(mesh.tets)] > 0.0).all():
+        raise MeshError("non-positive lumped mass")
+    return RestData(inv, vol, rows, masses)

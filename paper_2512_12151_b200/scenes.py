@@ -1,0 +1,198 @@
+"""Procedural meshes and the synthetic benchmark scenes of BASELINE.json.
+
+Primitives follow intact/primitives.py (Kuhn 6-tet boxes, cube-to-sphere
+map); scenes follow SURVEY.md §8(d):
+
+  C1  NH cube (box_mesh(10,10,8), 0.2 m, 4800 tets) dropped at 1 m/s from
+      3 mm onto a Dirichlet-fixed LIN slab, h = 0.01.
+  C4  five hollow cube-to-sphere shells (outermost Kuhn layer of an n-grid;
+      n = 112 gives 443,568 tets and ~147.9k vertices per ball, 2.22M tets in
+      all), COR, rho 1e2, E 1e4, nu 0.4, resting on a fixed slab and
+      compressed by a scripted constant-velocity top plate
+      (PAPER.md:810 parameters).
+  C5  randomized C1-like drops (seeded jitter of translation, rotation and
+      velocity), one scene per seed.
+
+Host-side setup only (numpy); nothing here runs in the timed hot path.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .elasticity import Material, MaterialModel
+from .mesh import SimState, TetMesh, build_tet_mesh, compute_rest_data
+from .solver import ElasticRegion
+from .stepper import BoundaryCondition, StepParams, System
+
+_CUBE_TETS = np.array([[0, 1, 3, 7], [0, 3, 2, 7], [0, 2, 6, 7], [0, 6, 4, 7], [0, 4, 5, 7], [0, 5, 1, 7]],
+                      dtype=np.int64)
+
+
+def grid_points(nx, ny, nz, size):
+    sx, sy, sz = (float(s) for s in np.broadcast_to(size, 3))
+    g = np.stack(np.meshgrid(np.linspace(0.0, sx, nx + 1), np.linspace(0.0, sy, ny + 1),
+                             np.linspace(0.0, sz, nz + 1), indexing="ij"), axis=-1)
+    return g.reshape(-1, 3)
+
+
+def cell_tets(nx, ny, nz, cells=None):
+    """Kuhn tets of the given cells ((k,3) integer cell coords; all if None)."""
+    if cells is None:
+        i, j, k = np.meshgrid(np.arange(nx), np.arange(ny), np.arange(nz), indexing="ij")
+        cells = np.stack([i.ravel(), j.ravel(), k.ravel()], axis=1)
+    i, j, k = cells[:, 0], cells[:, 1], cells[:, 2]
+
+    def vid(a, b, c):
+        return (a * (ny + 1) + b) * (nz + 1) + c
+
+    corner = np.stack([vid(i, j, k), vid(i, j, k + 1), vid(i, j + 1, k), vid(i, j + 1, k + 1),
+                       vid(i + 1, j, k), vid(i + 1, j, k + 1), vid(i + 1, j + 1, k), vid(i + 1, j + 1, k + 1)],
+                      axis=1)
+    return corner[:, _CUBE_TETS].reshape(-1, 4)
+
+
+def box_mesh(nx, ny, nz, size=1.0, origin=(0.0, 0.0, 0.0)) -> TetMesh:
+    return build_tet_mesh(grid_points(nx, ny, nz, size) + np.asarray(origin, dtype=np.float64),
+                          cell_tets(nx, ny, nz))
+
+
+def rotation_matrix(axis, angle):
+    a = np.asarray(axis, dtype=np.float64)
+    a = a / np.linalg.norm(a)
+    c, s = np.cos(angle), np.sin(angle)
+    k = np.array([[0, -a[2], a[1]], [a[2], 0, -a[0]], [-a[1], a[0], 0]])
+    return c * np.eye(3) + s * k + (1 - c) * np.outer(a, a)
+
+
+def transformed(mesh: TetMesh, translate=(0.0, 0.0, 0.0), rotate=None) -> TetMesh:
+    v = mesh.rest_positions
+    if rotate is not None:
+        v = v @ np.asarray(rotate, dtype=np.float64).T
+    return TetMesh(v + np.asarray(translate, dtype=np.float64), mesh.tets.copy(), mesh.surface_tris.copy(),
+                   mesh.surface_edges.copy(), mesh.surface_verts.copy())
+
+
+def shell_sphere(n, radius=0.1, center=(0.0, 0.0, 0.0)) -> TetMesh:
+    """Hollow ball: the outermost Kuhn-cell layer of an n^3 grid on [-1,1]^3,
+    mapped radially onto a sphere (the intact/primitives.py:80-87 map)."""
+    i, j, k = np.meshgrid(np.arange(n), np.arange(n), np.arange(n), indexing="ij")
+    on = (i == 0) | (j == 0) | (k == 0) | (i == n - 1) | (j == n - 1) | (k == n - 1)
+    cells = np.stack([i[on], j[on], k[on]], axis=1)
+    tets = cell_tets(n, n, n, cells)
+    used, tets = np.unique(tets, return_inverse=True)
+    tets = tets.reshape(-1, 4)
+    verts = grid_points(n, n, n, 2.0)[used] - 1.0
+    sup = np.abs(verts).max(axis=1)
+    nrm = np.linalg.norm(verts, axis=1)
+    verts = verts * np.where(nrm > 0.0, sup / np.maximum(nrm, 1e-300), 0.0)[:, None] * radius
+    return build_tet_mesh(verts + np.asarray(center, dtype=np.float64), tets)
+
+
+def merge(bodies, boundary_bodies=(), scripted=None, h=0.01):
+    """Stack bodies [(mesh, material, density, velocity)] into a System.
+
+    boundary_bodies: indices of bodies pinned entirely (fixed DBC);
+    scripted: {body index: velocity} for bodies driven at constant velocity.
+    """
+    scripted = scripted or {}
+    masses, regions, tris, edges, verts, xs, vs = [], [], [], [], [], [], []
+    offs = [0]
+    rest_cache = {}
+    for mesh, mat, rho, vel in bodies:
+        key = (id(mesh.tets), rho)
+        rest = rest_cache.get(key)
+        if rest is None or rest[0] is not mesh:
+            rest = (mesh, compute_rest_data(mesh, rho))
+        rest_cache[key] = rest
+        rd = rest[1]
+        off = offs[-1]
+        regions.append(ElasticRegion(mat, mesh.tets + off, rd.shape_rows, rd.volumes))
+        masses.append(rd.masses)
+        tris.append(mesh.surface_tris + off)
+        edges.append(mesh.surface_edges + off)
+        verts.append(mesh.surface_verts + off)
+        xs.append(mesh.rest_positions)
+        vs.append(np.tile(np.asarray(vel, dtype=np.float64), (mesh.n_verts, 1)))
+        offs.append(off + mesh.n_verts)
+    x = np.vstack(xs)
+    boundary = []
+    for b in boundary_bodies:
+        boundary.append(BoundaryCondition(np.arange(offs[b], offs[b + 1])))
+    for b, vel in scripted.items():
+        ids = np.arange(offs[b], offs[b + 1])
+        traj = _ScriptedLine(x[ids].copy(), np.asarray(vel, dtype=np.float64), h)
+        boundary.append(BoundaryCondition(ids, kind="scripted", trajectory=traj))
+    system = System(np.concatenate(masses), regions, np.vstack(tris), np.vstack(edges), np.concatenate(verts),
+                    boundary)
+    return system, SimState(x, np.vstack(vs)), np.asarray(offs)
+
+
+class _ScriptedLine:
+    """Constant-velocity target at the end of step k (intact/scene.py:459-466);
+    h is bound by the scene builder."""
+
+    def __init__(self, start, velocity, h=0.01):
+        self.start, self.velocity, self.h = start, velocity, h
+
+    def __call__(self, step_index):
+        return self.start + (step_index + 1) * self.h * self.velocity
+
+
+def _slab(size, corner, cells=(2, 2, 1), young=1e7):
+    return (box_mesh(*cells, size=size, origin=corner), Material(MaterialModel.LIN, young, 0.3), 1000.0,
+            (0.0, 0.0, 0.0))
+
+
+def c1_scene(nx=10, ny=10, nz=8, size=0.2, height=0.003, speed=1.0):
+    """NH cube dropped onto a fixed LIN slab."""
+    cube = box_mesh(nx, ny, nz, size=size, origin=(-size / 2, -size / 2, height))
+    bodies = [_slab((0.6, 0.6, 0.05), (-0.3, -0.3, -0.05)),
+              (cube, Material(MaterialModel.NH, 1e5, 0.3), 1000.0, (0.0, 0.0, -speed))]
+    system, state, offs = merge(bodies, boundary_bodies=[0])
+    params = StepParams(h=0.01, offset=1e-3, min_iterations=2)
+    return system, state, params
+
+
+def c4_scene(n=112, radius=0.1, gap=0.001, plate_speed=0.25, h=0.01):
+    """Five squishy-ball proxies compressed by a moving plate.
+
+    Four shells sit in a 2x2 square on a fixed slab, the fifth in the pocket
+    above them; a scripted top plate starts one gap above the top shell and
+    moves down at plate_speed.
+    """
+    ball = shell_sphere(n, radius)
+    mat = Material(MaterialModel.COR, 1e4, 0.4)
+    rho = 1e2
+    c = radius + gap / 2
+    z0 = radius + gap
+    centers = [(-c, -c, z0), (c, -c, z0), (-c, c, z0), (c, c, z0)]
+    dz = np.sqrt((2 * radius + gap) ** 2 - 2 * c * c)
+    centers.append((0.0, 0.0, z0 + dz + gap))
+    bodies = [_slab((1.0, 1.0, 0.05), (-0.5, -0.5, -0.05))]
+    for ctr in centers:
+        bodies.append((transformed(ball, translate=ctr), mat, rho, (0.0, 0.0, 0.0)))
+    top = centers[-1][2] + radius + gap
+    bodies.append(_slab((0.6, 0.6, 0.03), (-0.3, -0.3, top)))
+    system, state, offs = merge(bodies, boundary_bodies=[0], scripted={len(bodies) - 1: (0.0, 0.0, -plate_speed)},
+                                h=h)
+    params = StepParams(h=h, offset=1e-3, min_iterations=2)
+    return system, state, params
+
+
+def c5_scene(seed, nx=10, ny=10, nz=8):
+    """One randomized C1-like drop."""
+    rng = np.random.default_rng(seed)
+    size = 0.2
+    cube = box_mesh(nx, ny, nz, size=size, origin=(-size / 2, -size / 2, -size / 2))
+    axis = rng.standard_normal(3)
+    R = rotation_matrix(axis, rng.uniform(-np.pi, np.pi))
+    cube = transformed(cube, rotate=R)
+    lift = -cube.rest_positions[:, 2].min() + 0.003
+    shift = rng.uniform(-0.005, 0.005, 3)
+    cube = transformed(cube, translate=(shift[0], shift[1], lift + abs(shift[2])))
+    speed = rng.uniform(0.5, 2.0)
+    bodies = [_slab((0.6, 0.6, 0.05), (-0.3, -0.3, -0.05)),
+              (cube, Material(MaterialModel.NH, 1e5, 0.3), 1000.0, (0.0, 0.0, -speed))]
+    system, state, _ = merge(bodies, boundary_bodies=[0])
+    return system, state, StepParams(h=0.01, offset=1e-3, min_iterations=2)

@@ -1,0 +1,203 @@
+"""GPU parity of assembly, PCG, the Newton subproblem and whole steps against
+the CPU oracle and the reference's golden trajectory (marked gpu).
+
+Tolerances (FP64, stated per north star): gradients/matvecs 1e-9 relative
+(different summation order); per-step positions 1e-5 relative; Newton counts
+per outer pass within +-1; active-constraint key sets and penetration-free
+states exact.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import contact as ocontact, geometry, material, newton, timestep
+from tests.conftest import golden
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2512_12151_b200 as p
+    p._lib = __import__("paper_2512_12151_b200._lib", fromlist=["lib"])
+    p._lib.lib()
+    return p
+
+
+def _traj_system(pkg, g):
+    from paper_2512_12151_b200 import ElasticRegion, Material, MaterialModel, System
+    from paper_2512_12151_b200.stepper import BoundaryCondition
+    regions = [ElasticRegion(Material(MaterialModel.LIN, 1e7, 0.3), g["reg0_tets"], g["reg0_rows"], g["reg0_vols"]),
+               ElasticRegion(Material(MaterialModel.SNH, 1e5, 0.3), g["reg1_tets"], g["reg1_rows"], g["reg1_vols"])]
+    n_slab = int(g["n_slab"])
+    return System(g["masses"], regions, g["tris"], g["edges"], g["verts"], [BoundaryCondition(np.arange(n_slab))])
+
+
+def _oracle_regions(g):
+    mu_l, lam_l = material.lame(1e7, 0.3)
+    mu_s, lam_s = material.lame(1e5, 0.3)
+    return [("lin", mu_l, lam_l, g["reg0_tets"], g["reg0_rows"], g["reg0_vols"]),
+            ("snh", mu_s, lam_s, g["reg1_tets"], g["reg1_rows"], g["reg1_vols"])]
+
+
+def _oracle_set_after(g, steps):
+    scene = timestep.Scene(g["masses"], _oracle_regions(g), g["tris"], g["edges"], g["verts"],
+                           [(np.arange(int(g["n_slab"])), None)])
+    x, v = g["x0"].copy(), g["v0"].copy()
+    aset = ocontact.ConstraintSet()
+    for k in range(steps):
+        x, v, _, _, _ = timestep.step(x, v, scene, aset, h=0.01, offset=1e-3, k_min=2, step_index=k)
+    return x, v, aset
+
+
+def test_assemble_with_contacts_matches_oracle(pkg, rng):
+    from paper_2512_12151_b200.contact import ConstraintBatch
+    from paper_2512_12151_b200.solver import assemble, incremental_energy
+    g = golden("trajectory.npz")
+    x, v, aset = _oracle_set_after(g, 2)
+    aset.refresh_anchors(x)
+    ob = aset.snapshot()
+    assert len(ob) > 0
+    x_tilde = x + 0.01 * v + 1e-4 * np.array([0, 0, -9.81])
+    x_hat = x + 1e-4 * rng.standard_normal(x.shape)
+    x_hat[: int(g["n_slab"])] = x[: int(g["n_slab"])]
+    mu, off, h = 50.0, 1e-3, 0.01
+    dbc = np.zeros(len(x), dtype=bool)
+    dbc[: int(g["n_slab"])] = True
+    go, Ho = newton.assemble(x_hat, x_tilde, g["masses"], _oracle_regions(g), ob, mu, off, h, dbc)
+    sysm = _traj_system(pkg, g)
+    batch = ConstraintBatch(ob.kind, ob.quad, ob.lam, ob.gamma, ob.anchor_d, ob.anchor_grad, ob.anchor_x)
+    gg, Hg = assemble(x_hat, x_tilde, sysm.masses, sysm.regions, batch, mu, off, h, dbc)
+    scale = np.abs(go).max()
+    assert np.abs(gg - go).max() <= 1e-9 * scale
+    for _ in range(4):
+        p = rng.standard_normal(x.shape)
+        yo, yg = Ho.matvec(p), Hg.matvec(p)
+        assert np.abs(yg - yo).max() <= 1e-9 * np.abs(yo).max()
+    eo = newton.energy(x_hat, x_tilde, g["masses"], _oracle_regions(g), ob, mu, off, h)
+    eg = incremental_energy(x_hat, x_tilde, sysm.masses, sysm.regions, batch, mu, off, h)
+    assert eg == pytest.approx(eo, rel=1e-12)
+
+
+def test_pcg_sphere_compression(pkg):
+    """Flattened sphere: PCG converges within 250 iterations and matches the
+    oracle's iteration count (tests/test_solver.py:246-255)."""
+    from paper_2512_12151_b200 import ElasticRegion, Material, MaterialModel
+    from paper_2512_12151_b200.mesh import build_tet_mesh, compute_rest_data
+    from paper_2512_12151_b200.scenes import cell_tets, grid_points
+    from paper_2512_12151_b200.solver import DeviceSystem
+    from paper_2512_12151_b200.device import to_dev, empty, to_host
+    n = 6
+    verts = grid_points(n, n, n, 2.0) - 1.0
+    sup = np.abs(verts).max(axis=1)
+    nrm = np.linalg.norm(verts, axis=1)
+    verts = verts * np.where(nrm > 0.0, sup / np.maximum(nrm, 1e-300), 0.0)[:, None] * 0.5
+    mesh = build_tet_mesh(verts, cell_tets(n, n, n))
+    rest = compute_rest_data(mesh, 1000.0)
+    x = mesh.rest_positions * np.array([1.0, 1.0, 0.72])
+    mu_, lam_ = material.lame(1e5, 0.4)
+    go, Ho = newton.assemble(x, x, rest.masses, [("snh", mu_, lam_, mesh.tets, rest.shape_rows, rest.volumes)],
+                             None, 1.0, 0.0, 0.01)
+    po, its, conv, _ = __import__("oracle.blocksparse", fromlist=["pcg"]).pcg(Ho, -go, 1e-4)
+    reg = ElasticRegion(Material(MaterialModel.SNH, 1e5, 0.4), mesh.tets, rest.shape_rows, rest.volumes)
+    dev = DeviceSystem(rest.masses, [reg])
+    xd = to_dev(x)
+    gd = empty(x.shape)
+    dev.assemble(None, xd, xd, 1.0, 0.0, 0.01, False, gd)
+    assert np.abs(to_host(gd) - go).max() <= 1e-9 * np.abs(go).max()
+    rhs = -gd
+    pd = empty(x.shape)
+    it_g, conv_g, rel_g = dev.pcg(rhs, pd, 1e-4)
+    assert conv and conv_g and it_g <= 250
+    assert abs(it_g - its) <= 1
+    np.testing.assert_allclose(to_host(pd), po, rtol=1e-6, atol=1e-9 * np.abs(po).max())
+
+
+def test_plane_settle_kkt(pkg):
+    """tests/test_solver.py:196-227: converged state one offset above the
+    plane, |c| contracts geometrically, lambda = 0.3, DBC rows bit-pinned."""
+    from paper_2512_12151_b200.contact import ActiveSet, Constraint
+    from paper_2512_12151_b200.distance import PairKind
+    from paper_2512_12151_b200.solver import solve_subproblem
+    x0 = np.array([[0.4, 0.4, 0.05], [0.0, 0.0, 0.0], [2.0, 0.0, 0.0], [0.0, 2.0, 0.0]])
+    masses = np.ones(4)
+    dbc = np.array([False, True, True, True])
+    x_tilde = x0.copy()
+    x_tilde[0, 2] = -0.2
+    active = ActiveSet()
+    active.ensure(4)
+    active.add(Constraint(kind=PairKind.VERTEX_FACE, indices=np.array([0, 1, 2, 3])))
+    mu, offset = 10.0, 0.1
+    x_hat = x0.copy()
+    viol = []
+    for _ in range(12):
+        res = solve_subproblem(x_tilde, x0, x_hat, masses, [], active, mu=mu, offset=offset, h=0.01, cg_tol=1e-12,
+                               decay=0.9, dbc_mask=dbc)
+        x_hat = res.x_hat
+        viol.append(res.worst_violation)
+        assert np.array_equal(x_hat[1:], x0[1:])
+    v = np.array(viol)
+    live = v > 1e-9
+    assert (v[1:][live[:-1]] / v[:-1][live[:-1]] < 0.9).all()
+    assert v.min() < 1e-8
+    assert x_hat[0, 2] == pytest.approx(offset, abs=1e-6)
+    lam = active.export_state()[2][0]
+    assert lam == pytest.approx(0.3, rel=1e-5)
+
+
+def _min_distance(x, tris, edges, verts):
+    """Smallest VF / EE distance over all non-adjacent surface pairs (oracle)."""
+    vf = np.array([[v, *t] for v in verts for t in tris if v not in t])
+    ee = np.array([[*a, *b] for i, a in enumerate(edges) for b in edges[i + 1:] if not set(a) & set(b)])
+    return min(geometry.pair_dist(0, x[vf]).min(), geometry.pair_dist(1, x[ee]).min())
+
+
+def test_trajectory_matches_reference(pkg):
+    """Six steps of the golden box-on-slab drop: positions within 1e-5
+    relative, Newton counts +-1 per pass, identical active key sets,
+    penetration-free states."""
+    from paper_2512_12151_b200 import Simulation, StepParams
+    from paper_2512_12151_b200.mesh import SimState
+    g = golden("trajectory.npz")
+    system = _traj_system(pkg, g)
+    sim = Simulation(system, StepParams(h=0.01, offset=1e-3, min_iterations=2), SimState(g["x0"].copy(),
+                                                                                         g["v0"].copy()))
+    scale = np.abs(g["xs"]).max()
+    for k in range(len(g["xs"])):
+        d = sim.advance()
+        x = sim.state.x
+        assert np.abs(x - g["xs"][k]).max() <= 1e-5 * scale, k
+        ref = g[f"rec{k}"]
+        got = np.array([[r.alpha, r.beta, r.n_constraints, r.newton_iters, r.cg_iters] for r in d.iterations])
+        assert len(got) == len(ref)
+        assert np.all(np.abs(got[:, 3] - ref[:, 3]) <= 1)
+        np.testing.assert_allclose(got[:, 0], ref[:, 0], rtol=1e-6, atol=1e-9)
+        keys = sorted(c.key for c in sim.active_set)
+        assert np.array_equal(np.array([[kk[0], *kk[1]] for kk in keys]).reshape(-1, 5), g[f"keys{k}"])
+        assert _min_distance(x, g["tris"], g["edges"], g["verts"]) > 0.0
+
+
+def test_c1_first_frames_match_oracle(pkg):
+    """C1 (NH cube on a slab): first two frames vs the oracle."""
+    from paper_2512_12151_b200 import Simulation, scenes
+    system, state, params = scenes.c1_scene()
+    regions = [(r.material.model.value, r.material.mu, r.material.lam, r.tets, r.shape_rows, r.volumes)
+               for r in system.regions]
+    scene = timestep.Scene(system.masses, regions, system.surface_triangles, system.surface_edges,
+                           system.surface_vertices, [(bc.vertices, None) for bc in system.boundary])
+    x, v = state.x.copy(), state.v.copy()
+    aset = ocontact.ConstraintSet()
+    sim = Simulation(system, params, state.copy())
+    for k in range(2):
+        x, v, rec, _, _ = timestep.step(x, v, scene, aset, h=params.h, offset=params.offset,
+                                        k_min=params.min_iterations, step_index=k)
+        d = sim.advance()
+        xg = sim.state.x
+        assert np.abs(xg - x).max() <= 1e-5 * np.abs(x).max()
+        assert len(d.iterations) == len(rec)
+        assert all(abs(a.newton_iters - b[3]) <= 1 for a, b in zip(d.iterations, rec))
+        keys_o = sorted(ocontact.key_of(kd, q) for kd, q in zip(aset.kind, aset.quad))
+        assert sorted(c.key for c in sim.active_set) == keys_o
