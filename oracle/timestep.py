@@ -77,11 +77,13 @@ class Scene:
 
 def step(x_t, v_t, scene, aset, h, offset, epsilon=1e-3, k_min=1, decay=0.9,
          c_mu=0.1, cg_tol=1e-4, gravity=(0.0, 0.0, -9.81), step_index=0,
-         outer_cap=OUTER_CAP, record_iterates=False):
+         outer_cap=OUTER_CAP, record_iterates=False, trace=None):
     """One step (`step`, :242-371), frictionless.
 
     Returns (x, v, records, mu, offset) with one record per pass:
     (alpha, beta, n_constraints, newton_iters, cg_iters, wall_ms).
+    `trace`, if a list, receives per pass the exact inputs and outputs of
+    the set-maintenance and CCD stages (for identical-input parity tests).
     """
     g = np.asarray(gravity, dtype=float)
     x_tilde = x_t + h * v_t + (h * h) * g
@@ -101,12 +103,20 @@ def step(x_t, v_t, scene, aset, h, offset, epsilon=1e-3, k_min=1, decay=0.9,
         x_hat, nit, cgit, _, _ = subproblem(
             x_tilde, x, x_hat, scene.masses, scene.regions, aset, mu, offset, h,
             cg_tol=cg_tol, decay=decay, dbc=scene.dbc, memo=scene.memo)
+        if trace is not None:
+            rec = {"resident": (aset.kind.copy(), aset.quad.copy(), aset.gamma.copy()),
+                   "blocking": (kinds.copy(), quads.copy(), tois.copy())}
         aset.update(kinds, quads, tois)
         cap = 1.0
         for model, _m, _l, tets, rows, _v in scene.regions:
             cap = min(cap, inversion_cap(model, x, x_hat - x, tets, rows))
         alpha, kinds, quads, tois = step_limit(
             x, x_hat, scene.tris, scene.edges, scene.verts, GAP_FRACTION * offset, cap=cap)
+        if trace is not None:
+            rec.update(updated=(aset.kind.copy(), aset.quad.copy()), x=x.copy(), x_hat=x_hat.copy(),
+                       min_gap=GAP_FRACTION * offset, cap=cap, alpha=alpha,
+                       new_blocking=(kinds.copy(), quads.copy(), tois.copy()))
+            trace.append(rec)
         x = clamp(x, x_hat, alpha)
         beta = beta_next(beta, alpha, k - 1, k_min)
         records.append((alpha, beta, len(aset), nit, cgit, (time.perf_counter() - t0) * 1e3))
