@@ -1,0 +1,357 @@
+"""Benchmark: ms/frame on the C4 squishy-ball compression scene (BASELINE.json).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--n 112]
+
+One "step" is one frame (= one Simulation.advance, intact/cli.py:98-116) of
+the 2.22M-tet five-shell scene.  W untimed warm-up
+frames, then K timed frames.  Per timed frame the inputs (x, v) are copied
+host->device from pinned memory, the frame runs through the public
+Simulation/step path, and (x, v) are copied back; `value` is the device time
+of the frame proper (inputs resident), `e2e` the whole bracket including the
+copies.  The matrix alone is ~0.5 GB, far above the 126 MB L2, so no flush
+is needed between frames.
+
+Multi-GPU (torchrun): a single scene does not shard in this round, so each
+rank runs an independent replica ("replicas only"); value = max
+over ranks of the timed region / (N*K) frames, scaling "weak".
+
+--impl reference times the reference's CPU algorithm (the oracle
+restatement, oracle/) on the host cores: unit costs of its hot-path stages
+(assemble, PCG iteration, energy, CCD pass) measured on one reduced shell,
+scaled to the C4 size and to the per-frame operation counts.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ms/frame and ms/Newton iter (squishy balls 2.25M tets); PCG SpMV HBM GB/s"
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+COUNTS = os.path.join(ROOT, "profiles", "c4_frame_counts.json")
+NCU_SUMMARY = os.path.join(ROOT, "profiles", "ncu_summary.json")
+PAPER_COUNTS = {"newton": 30.09, "cg": 30.09 * 28.35, "passes": 30.09, "energy": 30.09 * 1.5,
+                "source": "PAPER.md:694 (Newton 30.09/frame, CG 28.35/solve); passes and energy evals assumed"}
+
+
+def _peaks():
+    try:
+        with open(PEAKS) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index, self.samples, self.stop = index, [], threading.Event()
+        self.t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self.stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                vals = [v.strip() for v in out.stdout.strip().split(",")]
+                if len(vals) == 6:
+                    self.samples.append(vals)
+            except Exception:
+                pass
+            self.stop.wait(0.2)
+
+    def __enter__(self):
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        self.t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for s in self.samples for n, v in zip(names, s[2:]) if v.strip().lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": float(self.samples[0][1]) if self.samples[0][1].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ------------------------------------------------------------------ CPU baseline
+
+def reference_unit_costs(n_sample=56, seed=0):
+    """Time the reference algorithm's stages (oracle restatement) on one
+    shell of resolution n_sample, in a contact-loaded configuration."""
+    from oracle import blocksparse, geometry, newton
+    from paper_2512_12151_b200 import scenes
+    ball = scenes.shell_sphere(n_sample, 0.1)
+    from paper_2512_12151_b200.mesh import compute_rest_data
+    rest = compute_rest_data(ball, 1e2)
+    from paper_2512_12151_b200.elasticity import Material, MaterialModel
+    mat = Material(MaterialModel.COR, 1e4, 0.4)
+    R = [("cor", mat.mu, mat.lam, ball.tets, rest.shape_rows, rest.volumes)]
+    rng = np.random.default_rng(seed)
+    x = ball.rest_positions * np.array([1.0, 1.0, 0.97])          # squashed: nonzero elastic forces
+    x_tilde = ball.rest_positions + 1e-4 * rng.standard_normal(x.shape)
+    h = 0.01
+    t = time.perf_counter()
+    g, H = newton.assemble(x, x_tilde, rest.masses, R, None, 1.0, 1e-3, h)
+    t_asm = time.perf_counter() - t
+    t = time.perf_counter()
+    _, its, _, _ = blocksparse.pcg(H, -g, 1e-12, max_iters=20)
+    t_cg = (time.perf_counter() - t) / max(its, 1)
+    t = time.perf_counter()
+    newton.energy(x, x_tilde, rest.masses, R, None, 1.0, 1e-3, h)
+    t_en = time.perf_counter() - t
+    x_hat = x + 2e-3 * rng.standard_normal(x.shape)
+    t = time.perf_counter()
+    geometry.step_limit(x, x_hat, ball.surface_tris, ball.surface_edges, ball.surface_verts, 1e-4)
+    t_ccd = time.perf_counter() - t
+    return {"assemble_s": t_asm, "cg_iter_s": t_cg, "energy_s": t_en, "ccd_pass_s": t_ccd,
+            "tets": int(ball.n_tets), "blocks": int(len(H.rows)), "tris": int(len(ball.surface_tris)),
+            "n_sample": n_sample}
+
+
+def reference_ms_per_frame(units, full, counts):
+    """Scale sampled unit costs to the full scene and per-frame op counts."""
+    st = units["tets"] / 1.0
+    s_asm = full["tets"] / st
+    s_cg = full["blocks"] / units["blocks"]
+    s_ccd = full["tris"] / units["tris"]
+    asm = units["assemble_s"] * s_asm * (counts["newton"] + 1.0)      # + mu-init assembly per frame
+    cg = units["cg_iter_s"] * s_cg * counts["cg"]
+    en = units["energy_s"] * s_asm * counts["energy"]
+    ccd = units["ccd_pass_s"] * s_ccd * counts["passes"]
+    return 1e3 * (asm + cg + en + ccd), {"assemble_ms": 1e3 * asm, "pcg_ms": 1e3 * cg, "energy_ms": 1e3 * en,
+                                         "ccd_ms": 1e3 * ccd}
+
+
+def _full_sizes(n):
+    per_tets = 36 * n * n - 72 * n + 48
+    tris = 2 * 6 * n * n + 2 * 6 * (n - 2) ** 2
+    verts = 6 * n * n + 2 + 6 * (n - 2) ** 2 + 2
+    # upper+diag blocks per vertex of the shell pattern (~7.4 for Kuhn meshes), taken from the sample
+    return {"tets": 5 * per_tets, "tris": 5 * tris, "verts": 5 * verts}
+
+
+def run_reference(args):
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return
+    counts, src = PAPER_COUNTS, PAPER_COUNTS["source"]
+    try:
+        with open(COUNTS) as f:
+            c = json.load(f)
+        counts = {k: float(c[k]) for k in ("newton", "cg", "passes", "energy")}
+        src = f"per-frame op counts of the GPU run recorded in {os.path.relpath(COUNTS, ROOT)}"
+    except Exception:
+        pass
+    full = _full_sizes(args.n)
+    vals = []
+    units = None
+    for k in range(args.warmup + args.steps):
+        units = reference_unit_costs(args.sample_n, seed=k)
+        full["blocks"] = units["blocks"] * full["tets"] / units["tets"]
+        ms, parts = reference_ms_per_frame(units, full, counts)
+        if k >= args.warmup:
+            vals.append(ms)
+    value = float(np.mean(vals))
+    sample = (f"oracle (numpy restatement of intact) stage costs on one n={args.sample_n} shell "
+              f"({units['tets']} tets), scaled to C4 ({full['tets']} tets) and {src}")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "ms/frame", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": value, "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"C4 five hollow COR shells n={args.n} ({full['tets']} tets) compressed by a "
+                                   "moving plate", "parallelism": "host cores (numpy)"},
+            "cpu_baseline": {"value": value, "unit": "ms/frame", "cores": os.cpu_count(), "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "ms/frame", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "phases_ms": parts}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU arm
+
+def run_ours(args):
+    import torch
+    ws, rank, local = _dist()
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    else:
+        torch.cuda.set_device(0)
+    from paper_2512_12151_b200 import _lib, scenes
+    from paper_2512_12151_b200.device import to_host
+    from paper_2512_12151_b200.stepper import step_device
+    from paper_2512_12151_b200.contact import ActiveSet
+    import ctypes as C
+
+    t_setup = time.perf_counter()
+    system, state, params = scenes.c4_scene(n=args.n)
+    dev = system.device
+    ccd = system.ccd
+    aset = ActiveSet()
+    aset.ensure(system.n_vertices)
+    n = system.n_vertices
+    x = torch.from_numpy(state.x).cuda()
+    v = torch.from_numpy(state.v).cuda()
+    setup_s = time.perf_counter() - t_setup
+    L = _lib.lib()
+    k = 0
+    for _ in range(args.warmup):
+        x, v, _ = step_device(x, v, system, aset, params, step_index=k)
+        k += 1
+    torch.cuda.synchronize()
+    stats = np.zeros(9)
+    cst = np.zeros(3)
+    L.ibf_system_stats(dev.handle, _lib.host_ptr(stats), 1)
+    L.ibf_ccd_stats(ccd.handle, _lib.host_ptr(cst), 1)
+    x_pin = torch.empty((n, 3), dtype=torch.float64, pin_memory=True)
+    v_pin = torch.empty((n, 3), dtype=torch.float64, pin_memory=True)
+    x_pin.copy_(x)
+    v_pin.copy_(v)
+    x_dev = torch.empty_like(x)
+    v_dev = torch.empty_like(v)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    newton = cg = passes = 0
+    n_constraints = []
+    launches0 = L.ibf_launch_count()
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        t0 = time.perf_counter()
+        for j in range(args.steps):
+            e = evs[j]
+            e[0].record()
+            x_dev.copy_(x_pin, non_blocking=True)
+            v_dev.copy_(v_pin, non_blocking=True)
+            e[1].record()
+            xn, vn, diag = step_device(x_dev, v_dev, system, aset, params, step_index=k)
+            k += 1
+            e[2].record()
+            x_pin.copy_(xn, non_blocking=True)
+            v_pin.copy_(vn, non_blocking=True)
+            e[3].record()
+            torch.cuda.synchronize()
+            newton += sum(r.newton_iters for r in diag.iterations)
+            cg += sum(r.cg_iters for r in diag.iterations)
+            passes += len(diag.iterations)
+            n_constraints.append(max(r.n_constraints for r in diag.iterations))
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+    launches = L.ibf_launch_count() - launches0
+    frame_ms = [e[1].elapsed_time(e[2]) for e in evs]
+    e2e_ms = [e[0].elapsed_time(e[3]) for e in evs]
+    tot_dev, tot_e2e = float(np.sum(frame_ms)), float(np.sum(e2e_ms))
+    if ws > 1:
+        t = torch.tensor([tot_dev, tot_e2e], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        tot_dev, tot_e2e = float(t[0]), float(t[1])
+    L.ibf_system_stats(dev.handle, _lib.host_ptr(stats), 0)
+    L.ibf_ccd_stats(ccd.handle, _lib.host_ptr(cst), 0)
+    frames = ws * args.steps
+    value = tot_dev / frames
+    e2e = tot_e2e / frames
+    # roofline of the PCG (persistent SpMV + vector kernel): algorithmic bytes
+    spmv_bytes = dev.spmv_bytes()
+    pcg_ms, pcg_iters, contact_iter_terms = stats[2], stats[4], stats[8]
+    pcg_bytes = pcg_iters * (spmv_bytes + 288.0 * n) + 120.0 * contact_iter_terms
+    achieved = pcg_bytes / (pcg_ms * 1e-3) / 1e9 if pcg_ms > 0 else 0.0
+    peak, peak_kind = _peaks()
+    traffic = None
+    try:
+        with open(NCU_SUMMARY) as f:
+            traffic = json.load(f).get("pcg_dram_bytes_per_launch")
+    except Exception:
+        pass
+    phases = {"assembly_ms": stats[0] / args.steps, "pcg_ms": stats[2] / args.steps,
+              "line_search_ms": stats[5] / args.steps, "inversion_cap_ms": stats[7] / args.steps,
+              "ccd_ms": cst[0] / args.steps}
+    phases["other_ms"] = value - sum(phases.values())
+    counts = {"newton": newton / args.steps, "cg": cg / args.steps, "passes": passes / args.steps,
+              "energy": stats[6] / args.steps}
+    line = {"metric": METRIC, "value": value, "unit": "ms/frame", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": value, "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": round(5367.0 / value, 3) if value > 0 else None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"C4 five hollow COR shells n={args.n} ({sum(len(r.tets) for r in system.regions)}"
+                                   f" tets, {n} vertices) compressed by a moving plate, frames {args.warmup}.."
+                                   f"{args.warmup + args.steps - 1}",
+                       "parallelism": "replicas" if ws > 1 else "single-gpu",
+                       "l2": "inputs > L2 (matrix ~%.0f MB)" % (spmv_bytes / 1e6)},
+            "ms_per_newton_iter": value * args.steps / max(newton, 1),
+            "newton_per_frame": counts["newton"], "cg_per_frame": counts["cg"], "passes_per_frame": counts["passes"],
+            "peak_constraints": int(max(n_constraints)), "phases_ms": phases,
+            "roofline": {"kernel": "k_pcg (symmetric BSR SpMV + block-Jacobi vector phase)", "bound": "hbm",
+                         "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "peak_source": peak_kind, "traffic": traffic,
+                         "bytes_per_cg_iter": spmv_bytes + 288.0 * n},
+            "spmv_GBps": achieved,
+            "e2e": {"value": e2e, "unit": "ms/frame", "h2d_bytes_per_step": 2 * 24 * n,
+                    "d2h_bytes_per_step": 2 * 24 * n},
+            "gpu_launches": int(launches), "wall_s": wall, "setup_s": setup_s}
+    if rank == 0:
+        line["clocks"] = clocks.summary()
+        if not args.no_cpu_baseline:
+            os.makedirs(os.path.dirname(COUNTS), exist_ok=True)
+            try:
+                with open(COUNTS, "w") as f:
+                    json.dump(dict(counts, n=args.n, source="bench.py GPU run"), f, indent=1)
+            except OSError:
+                pass
+            full = _full_sizes(args.n)
+            units = reference_unit_costs(args.sample_n)
+            full["blocks"] = units["blocks"] * full["tets"] / units["tets"]
+            ms, parts = reference_ms_per_frame(units, full, counts)
+            line["cpu_baseline"] = {"value": ms, "unit": "ms/frame", "cores": 1, "kind": "port",
+                                    "sample": f"oracle stage costs on one n={args.sample_n} shell scaled to C4 and "
+                                              f"to this run's per-frame op counts", "phases_ms": parts}
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=112, help="shell resolution (112 -> 2.22M tets)")
+    ap.add_argument("--sample-n", type=int, default=40, help="shell resolution of the CPU baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

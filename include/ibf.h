@@ -208,9 +208,17 @@ int ibf_bsr_export(const ibf_bsr* m, int64_t* rows, int64_t* cols, double* block
 int ibf_bsr_pcg(ibf_bsr* m, const double* rhs, double* x_out, double rel_tol,
                 int64_t max_iters, double* info_host, ibf_stream st);
 
-/* Timing of the last PCG solve's SpMV launches (device ms and count), for the
- * bench's roofline line. */
+/* Algorithmic bytes of one symmetric SpMV over the elastic pattern
+ * (BASELINE.md §4), for the bench's roofline line. */
 int ibf_system_spmv_stats(const ibf_system* s, double* bytes_per_spmv);
+/* Device-time phase counters since the last reset: out[0..8] = assembly ms,
+ * assembly count, PCG ms, PCG launches, CG iterations, line-search energy ms,
+ * energy launches, inversion-cap ms, sum over PCG launches of C x iterations. */
+int ibf_system_stats(ibf_system* s, double* out, int reset);
+/* CCD phase: out[0..2] = max_step_size device ms, calls, broad-phase candidates. */
+int ibf_ccd_stats(ibf_ccd* c, double* out, int reset);
+/* Number of kernels libibf has launched in this process (CUB internals excluded). */
+unsigned long long ibf_launch_count(void);
 
 #ifdef __cplusplus
 }

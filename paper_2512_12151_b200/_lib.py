@@ -67,6 +67,9 @@ _PROTOS = {
     "ibf_system_spmv_stats": (_int, [_vp, _pdbl]),
     "ibf_bsr_size": (_i64, [_vp]),
     "ibf_vec_sub": (_int, [_i64, _vp, _vp, _vp, _vp]),
+    "ibf_system_stats": (_int, [_vp, _vp, _int]),
+    "ibf_ccd_stats": (_int, [_vp, _vp, _int]),
+    "ibf_launch_count": (C.c_ulonglong, []),
     "ibf_bsr_export": (_int, [_vp, _vp, _vp, _vp, _vp]),
 }
 

@@ -567,12 +567,14 @@ extern "C" int ibf_max_step_size(ibf_ccd* c, const double* x, const double* x_ha
   cudaStream_t s = (cudaStream_t)st;
   IBF_TRY(c->dscratch.reserve(8));
   IBF_TRY(c->host.reserve(64));
+  c->t_ccd.begin(s);
   // survivors of both passes, kept in separate regions of b_* scratch
   int64_t cnt[2] = {0, 0}, all[2] = {0, 0};
   DevBuf<int>* quads = c->s_quad;
   DevBuf<double>* tois = c->s_toi;
   for (int kind = 0; kind < 2; ++kind) {
     IBF_TRY(broad_pass(c, kind, x, x_hat, min_gap, true, &cnt[kind], &all[kind], s));
+    c->n_candidates += all[kind];
     if (cnt[kind]) {
       IBF_TRY(quads[kind].reserve(4 * cnt[kind]));
       IBF_TRY(tois[kind].reserve(cnt[kind]));
@@ -621,7 +623,9 @@ extern "C" int ibf_max_step_size(ibf_ccd* c, const double* x, const double* x_ha
   }
   double mt = INFINITY;
   IBF_CUDA(cudaMemcpyAsync(&mt, c->dscratch.p, sizeof(double), cudaMemcpyDeviceToHost, s));
+  c->t_ccd.end(s);
   IBF_CUDA(cudaStreamSynchronize(s));
+  c->t_ccd.harvest();
   *alpha_host = std::min(base, mt);
   c->n_block = nblock;
   *n_blocking_host = nblock;

@@ -29,7 +29,49 @@ void set_error(const std::string& msg);
     if (_s != IBF_OK) return _s;       \
   } while (0)
 
-#define IBF_LAUNCH_CHECK() IBF_CUDA(cudaGetLastError())
+// every kernel launch of the library is followed by IBF_LAUNCH_CHECK, which
+// also counts it (ibf_launch_count) for the bench's gpu_launches claim
+extern unsigned long long g_launches;
+#define IBF_LAUNCH_CHECK()        \
+  do {                            \
+    ++::ibf::g_launches;          \
+    IBF_CUDA(cudaGetLastError()); \
+  } while (0)
+
+// Device-time accumulator for one phase: events bracket the phase on its
+// stream; harvest() adds the elapsed time once the stream has synchronised.
+struct PhaseTimer {
+  cudaEvent_t a = nullptr, b = nullptr;
+  bool pending = false;
+  double ms = 0.0;
+  long long count = 0;
+  void begin(cudaStream_t s) {
+    if (!a) {
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+    }
+    harvest();
+    cudaEventRecord(a, s);
+  }
+  void end(cudaStream_t s) {
+    cudaEventRecord(b, s);
+    pending = true;
+  }
+  void harvest() {
+    if (!pending) return;
+    float t = 0.0f;
+    if (cudaEventElapsedTime(&t, a, b) == cudaSuccess) {
+      ms += t;
+      ++count;
+      pending = false;
+    }
+  }
+  void reset() {
+    harvest();
+    ms = 0.0;
+    count = 0;
+  }
+};
 
 // Growable device buffer owned by a handle.  Never shrinks; growth only
 // happens outside the timed hot loop once capacities settle.

@@ -109,4 +109,6 @@ struct ibf_ccd {
   ibf::DevBuf<double> dscratch;
   int64_t n_block = 0;
   ibf::HostScratch host;
+  ibf::PhaseTimer t_ccd;
+  long long n_candidates = 0;    // broad-phase candidates since the last stats reset
 };

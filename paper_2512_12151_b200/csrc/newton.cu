@@ -21,6 +21,7 @@
 
 namespace ibf {
 
+unsigned long long g_launches = 0;
 static thread_local std::string g_err;
 void set_error(const std::string& msg) { g_err = msg; }
 
@@ -186,20 +187,28 @@ extern "C" int ibf_solve_subproblem(ibf_system* s, ibf_contacts* c, const double
   double base = 0.0;
   bool capped = true;
   for (int it = 0; it < 64; ++it) {
+    s->t_asm.begin(stream);
     IBF_TRY(system_assemble(s, cc, x_hat, x_tilde, mu, offset, h, true, grad, true, stream));
+    s->t_asm.end(stream);
     k_neg<<<grid_for(n3), 256, 0, stream>>>(n3, grad, rhs);
     IBF_LAUNCH_CHECK();
+    s->t_pcg.begin(stream);
     IBF_TRY(pcg_solve(s->op(), rhs, p, cg_tol, 10 * n, s->work, stream));
+    s->t_pcg.end(stream);
     k_dot_part<<<dot_parts, 256, 0, stream>>>(n3, grad, p, dpart);
     IBF_LAUNCH_CHECK();
     k_descent_fix<<<grid_for(n), 256, 0, stream>>>(n, dpart, dot_parts, grad, s->pinv.p, p);
     IBF_LAUNCH_CHECK();
+    s->t_cap.begin(stream);
     IBF_TRY(system_inversion_cap_launch(s, x_hat, p, cap, stream));
+    s->t_cap.end(stream);
     k_first_step<<<1, 1, 0, stream>>>(cap, r0);
     IBF_LAUNCH_CHECK();
     const double rs_first[2] = {1.0, 0.0};
     const int T = have_base ? 1 : 2;  // second trial at r = 0 is the base energy
+    s->t_ls.begin(stream);
     IBF_TRY(system_energy_launch(s, cc, x_hat, p, T, rs_first, r0, x_tilde, mu, offset, h, E, stream));
+    s->t_ls.end(stream);
     IBF_CUDA(cudaMemcpyAsync(hd, E, 2 * sizeof(double), cudaMemcpyDeviceToHost, stream));
     IBF_CUDA(cudaMemcpyAsync(hd + 8, r0, sizeof(double), cudaMemcpyDeviceToHost, stream));
     IBF_CUDA(cudaMemcpyAsync(hd + 9, s->work.info.p, 3 * sizeof(double), cudaMemcpyDeviceToHost, stream));
@@ -214,6 +223,12 @@ extern "C" int ibf_solve_subproblem(ibf_system* s, ibf_contacts* c, const double
       break;
     }
     cg_total += (int64_t)hd[9];
+    s->t_asm.harvest();
+    s->t_pcg.harvest();
+    s->t_ls.harvest();
+    s->t_cap.harvest();
+    s->pcg_iters += (long long)hd[9];
+    s->contact_terms += (cc ? cc->n : 0) * (long long)hd[9];  // C x CG iterations
     if (!have_base) base = hd[1];
     const double rfirst = hd[8];
     double r = rfirst, e_acc = hd[0];
@@ -236,9 +251,12 @@ extern "C" int ibf_solve_subproblem(ibf_system* s, ibf_contacts* c, const double
           rs[j] = sc;
           sc *= 0.5;
         }
+        s->t_ls.begin(stream);
         IBF_TRY(system_energy_launch(s, cc, x_hat, p, T2, rs, r0, x_tilde, mu, offset, h, E, stream));
+        s->t_ls.end(stream);
         IBF_CUDA(cudaMemcpyAsync(hd, E, T2 * sizeof(double), cudaMemcpyDeviceToHost, stream));
         IBF_CUDA(cudaStreamSynchronize(stream));
+        s->t_ls.harvest();
         for (int j = 0; j < T2; ++j) {
           const double rj = rfirst * rs[j];
           if (hd[j] < base) {
@@ -297,5 +315,44 @@ extern "C" int ibf_vec_sub(int64_t n, const double* a, const double* b, double* 
   if (n <= 0) return IBF_OK;
   ibf::k_sub<<<ibf::grid_for(n), 256, 0, (cudaStream_t)st>>>(n, a, b, out);
   IBF_LAUNCH_CHECK();
+  return IBF_OK;
+}
+
+extern "C" unsigned long long ibf_launch_count(void) { return ibf::g_launches; }
+
+extern "C" int ibf_system_stats(ibf_system* s, double* out, int reset) {
+  s->t_asm.harvest();
+  s->t_pcg.harvest();
+  s->t_ls.harvest();
+  s->t_cap.harvest();
+  out[0] = s->t_asm.ms;
+  out[1] = (double)s->t_asm.count;
+  out[2] = s->t_pcg.ms;
+  out[3] = (double)s->t_pcg.count;
+  out[4] = (double)s->pcg_iters;
+  out[5] = s->t_ls.ms;
+  out[6] = (double)s->t_ls.count;
+  out[7] = s->t_cap.ms;
+  out[8] = (double)s->contact_terms;
+  if (reset) {
+    s->t_asm.reset();
+    s->t_pcg.reset();
+    s->t_ls.reset();
+    s->t_cap.reset();
+    s->pcg_iters = 0;
+    s->contact_terms = 0;
+  }
+  return IBF_OK;
+}
+
+extern "C" int ibf_ccd_stats(ibf_ccd* c, double* out, int reset) {
+  c->t_ccd.harvest();
+  out[0] = c->t_ccd.ms;
+  out[1] = (double)c->t_ccd.count;
+  out[2] = (double)c->n_candidates;
+  if (reset) {
+    c->t_ccd.reset();
+    c->n_candidates = 0;
+  }
   return IBF_OK;
 }

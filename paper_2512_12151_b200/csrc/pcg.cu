@@ -378,6 +378,7 @@ int pcg_solve(const Operator& op, const double* rhs, double* x_out, double rel_t
   a.max_iters = max_iters;
   void* args[] = {&a};
   IBF_CUDA(cudaLaunchCooperativeKernel((void*)k_pcg, grid, PCG_THREADS, args, 0, s));
+  ++g_launches;
   return IBF_OK;
 }
 

@@ -33,6 +33,10 @@ struct ibf_system {
   ibf::DevBuf<double> vec_a, vec_b, vec_c;   // (n,3) scratch
   ibf::HostScratch host;
   ibf::PcgWork work;
+  // phase timers (device time): assembly, PCG, line-search energies, inversion cap
+  ibf::PhaseTimer t_asm, t_pcg, t_ls, t_cap;
+  long long pcg_iters = 0;       // CG iterations since the last stats reset
+  long long contact_terms = 0;   // sum over PCG launches of C (matrix-free contact)
   ibf_contacts* assembled_contacts = nullptr;  // contact term of the last assembly
   bool assembled_dbc = false;
   ibf::Operator op() const;

@@ -13,7 +13,7 @@ from tests.conftest import ROOT
 
 def _declared_symbols():
     text = open(os.path.join(ROOT, "include", "ibf.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:const char\*|int64_t|int|void)\s+(ibf_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:const char\*|int64_t|unsigned long long|int|void)\s+(ibf_\w+)\s*\(", text, re.M)))
 
 
 @pytest.fixture(scope="module")
