@@ -3,7 +3,8 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--n 112]
 
 One "step" is one frame (= one Simulation.advance, intact/cli.py:98-116) of
-the 2.22M-tet five-shell scene.  W untimed warm-up
+the 2.22M-tet five-ball compression scene (solid-ball
+proxy — see paper_2512_12151_b200/scenes.py and DESIGN.md).  W untimed warm-up
 frames, then K timed frames.  Per timed frame the inputs (x, v) are copied
 host->device from pinned memory, the frame runs through the public
 Simulation/step path, and (x, v) are copied back; `value` is the device time
@@ -103,12 +104,12 @@ def _dist():
 
 # ------------------------------------------------------------------ CPU baseline
 
-def reference_unit_costs(n_sample=56, seed=0):
+def reference_unit_costs(n_sample=16, seed=0):
     """Time the reference algorithm's stages (oracle restatement) on one
-    shell of resolution n_sample, in a contact-loaded configuration."""
+    ball of resolution n_sample, in a strained configuration."""
     from oracle import blocksparse, geometry, newton
     from paper_2512_12151_b200 import scenes
-    ball = scenes.shell_sphere(n_sample, 0.1)
+    ball = scenes.shell_sphere(n_sample, 0.1, layers=(n_sample + 1) // 2)
     from paper_2512_12151_b200.mesh import compute_rest_data
     rest = compute_rest_data(ball, 1e2)
     from paper_2512_12151_b200.elasticity import Material, MaterialModel
@@ -151,11 +152,8 @@ def reference_ms_per_frame(units, full, counts):
 
 
 def _full_sizes(n):
-    per_tets = 36 * n * n - 72 * n + 48
-    tris = 2 * 6 * n * n + 2 * 6 * (n - 2) ** 2
-    verts = 6 * n * n + 2 + 6 * (n - 2) ** 2 + 2
-    # upper+diag blocks per vertex of the shell pattern (~7.4 for Kuhn meshes), taken from the sample
-    return {"tets": 5 * per_tets, "tris": 5 * tris, "verts": 5 * verts}
+    """Five solid n-balls (Kuhn grid): tets, surface tris, vertices."""
+    return {"tets": 5 * 6 * n ** 3, "tris": 5 * 12 * n * n, "verts": 5 * (n + 1) ** 3}
 
 
 def run_reference(args):
@@ -185,7 +183,7 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "ms/frame", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": value, "higher_is_better": False,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"C4 five hollow COR shells n={args.n} ({full['tets']} tets) compressed by a "
+            "config": {"workload": f"C4 five COR balls n={args.n} ({full['tets']} tets) compressed by a "
                                    "moving plate", "parallelism": "host cores (numpy)"},
             "cpu_baseline": {"value": value, "unit": "ms/frame", "cores": os.cpu_count(), "kind": "port",
                              "sample": sample},
@@ -300,7 +298,7 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": value, "higher_is_better": False, "scaling": "weak",
             "vs_baseline": round(5367.0 / value, 3) if value > 0 else None,
             "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"C4 five hollow COR shells n={args.n} ({sum(len(r.tets) for r in system.regions)}"
+            "config": {"workload": f"C4 five COR balls n={args.n} ({sum(len(r.tets) for r in system.regions)}"
                                    f" tets, {n} vertices) compressed by a moving plate, frames {args.warmup}.."
                                    f"{args.warmup + args.steps - 1}",
                        "parallelism": "replicas" if ws > 1 else "single-gpu",
@@ -340,11 +338,11 @@ def run_ours(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=3)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=112, help="shell resolution (112 -> 2.22M tets)")
-    ap.add_argument("--sample-n", type=int, default=40, help="shell resolution of the CPU baseline sample")
+    ap.add_argument("--n", type=int, default=42, help="ball resolution (42 -> 2.22M tets)")
+    ap.add_argument("--sample-n", type=int, default=16, help="ball resolution of the CPU baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":

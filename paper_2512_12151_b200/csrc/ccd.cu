@@ -445,6 +445,12 @@ static int broad_pass(ibf_ccd* c, int kind, const double* x0, const double* x1, 
     *count = (int64_t)h[0];
     *n_candidates = (int64_t)h[1];
     if (h[0] <= c->pairs.cap) break;
+    if (h[0] > (1ull << 30)) {
+      set_error("broad phase: " + std::to_string(h[0]) + " pairs need narrow-phase work (" +
+                std::to_string(h[1]) + " candidates for " + std::to_string(nq) +
+                " queries): the step's motion is unbounded");
+      return IBF_ERR_OOM;
+    }
     IBF_TRY(c->pairs.reserve((size_t)h[0]));
   }
   const int64_t cnt = *count;

@@ -5,11 +5,15 @@ map); scenes follow SURVEY.md §8(d):
 
   C1  NH cube (box_mesh(10,10,8), 0.2 m, 4800 tets) dropped at 1 m/s from
       3 mm onto a Dirichlet-fixed LIN slab, h = 0.01.
-  C4  five hollow cube-to-sphere shells (outermost Kuhn layer of an n-grid;
-      n = 112 gives 443,568 tets and ~147.9k vertices per ball, 2.22M tets in
-      all), COR, rho 1e2, E 1e4, nu 0.4, resting on a fixed slab and
-      compressed by a scripted constant-velocity top plate
-      (PAPER.md:810 parameters).
+  C4  five cube-to-sphere balls of 444,528 tets each (solid n = 42 grid,
+      2.22M tets, 0.40M vertices in all), COR, rho 1e2, E 1e4, nu 0.4
+      (PAPER.md:810), four in a 2x2 square on a fixed slab and one in the
+      pocket above, compressed by a scripted top plate at 0.1 m/s.  The
+      survey's one-cell hollow-shell proxy (n = 112, 0.74M vertices) is kept
+      behind `layers=1`; it is not used for the benchmark because the
+      reference algorithm itself blows up on it after a few frames (ultra-light
+      shells escape tangentially under the linearised constraints; GPU and
+      oracle agree on identical inputs — DESIGN.md §Scenes).
   C5  randomized C1-like drops (seeded jitter of translation, rotation and
       velocity), one scene per seed.
 
@@ -73,11 +77,13 @@ def transformed(mesh: TetMesh, translate=(0.0, 0.0, 0.0), rotate=None) -> TetMes
                    mesh.surface_edges.copy(), mesh.surface_verts.copy())
 
 
-def shell_sphere(n, radius=0.1, center=(0.0, 0.0, 0.0)) -> TetMesh:
-    """Hollow ball: the outermost Kuhn-cell layer of an n^3 grid on [-1,1]^3,
-    mapped radially onto a sphere (the intact/primitives.py:80-87 map)."""
+def shell_sphere(n, radius=0.1, center=(0.0, 0.0, 0.0), layers=1) -> TetMesh:
+    """Hollow ball: the outermost `layers` Kuhn-cell layers of an n^3 grid on
+    [-1,1]^3 (layers >= n/2 gives the solid ball), mapped radially onto a
+    sphere (the intact/primitives.py:80-87 map)."""
     i, j, k = np.meshgrid(np.arange(n), np.arange(n), np.arange(n), indexing="ij")
-    on = (i == 0) | (j == 0) | (k == 0) | (i == n - 1) | (j == n - 1) | (k == n - 1)
+    depth = np.minimum(np.minimum(np.minimum(i, j), k), np.minimum(np.minimum(n - 1 - i, n - 1 - j), n - 1 - k))
+    on = depth < layers
     cells = np.stack([i[on], j[on], k[on]], axis=1)
     tets = cell_tets(n, n, n, cells)
     used, tets = np.unique(tets, return_inverse=True)
@@ -154,14 +160,15 @@ def c1_scene(nx=10, ny=10, nz=8, size=0.2, height=0.003, speed=1.0):
     return system, state, params
 
 
-def c4_scene(n=112, radius=0.1, gap=0.001, plate_speed=0.25, h=0.01):
+def c4_scene(n=42, radius=0.1, gap=0.001, plate_speed=0.1, h=0.01, layers=None):
     """Five squishy-ball proxies compressed by a moving plate.
+    layers=None builds solid balls; layers=k keeps the outer k cell layers.
 
     Four shells sit in a 2x2 square on a fixed slab, the fifth in the pocket
     above them; a scripted top plate starts one gap above the top shell and
     moves down at plate_speed.
     """
-    ball = shell_sphere(n, radius)
+    ball = shell_sphere(n, radius, layers=(n + 1) // 2 if layers is None else layers)
     mat = Material(MaterialModel.COR, 1e4, 0.4)
     rho = 1e2
     c = radius + gap / 2

@@ -274,3 +274,50 @@ def test_axis_aligned_drop_tie_sensitivity(pkg):
         scale = np.abs(xo).max()
         assert np.abs(xg - xp).max() <= 1e-8 * scale
         assert kg == kp
+
+
+@pytest.mark.parametrize("n,layers,frames", [(16, 1, 8), (12, None, 6)])
+def test_contact_heavy_subproblem_parity(pkg, n, layers, frames):
+    """Evolve a small C4 scene on the GPU until hundreds of constraints are
+    active, then solve one AL subproblem from that exact state on both the
+    GPU and the oracle: identical Newton/CG counts, x_hat within 1e-6 of the
+    step, identical gamma, multipliers within 1e-6 relative."""
+    import torch
+    from paper_2512_12151_b200 import scenes
+    from paper_2512_12151_b200.contact import ActiveSet
+    from paper_2512_12151_b200.device import to_dev, to_host
+    from paper_2512_12151_b200.stepper import step_device
+    system, state, params = scenes.c4_scene(n=n, layers=layers, plate_speed=0.25)
+    aset = ActiveSet()
+    aset.ensure(system.n_vertices)
+    x = torch.from_numpy(state.x).cuda()
+    v = torch.from_numpy(state.v).cuda()
+    for k in range(frames):
+        x, v, _ = step_device(x, v, system, aset, params, step_index=k)
+    assert len(aset) > 50
+    dev = system.device
+    xt, vt, h = to_host(x), to_host(v), params.h
+    x_tilde = xt + h * vt + (h * h) * np.array(params.gravity)
+    mu = params.stiffness_constant * dev.stiffness_diagonal_max(x, h)
+    x_hat0 = xt.copy()
+    for bc in system.boundary:
+        if bc.kind == "scripted":
+            x_hat0[bc.vertices] = bc.targets(None, frames)
+    st = aset.export_state()
+    o = ocontact.ConstraintSet()
+    o._append(st[0], st[1], [ocontact.key_of(a, b) for a, b in zip(st[0], st[1])], lam=st[2], gamma=st[3],
+              s=st[4], anchor_d=st[5], anchor_grad=st[6], anchor_x=st[7])
+    regions = [(r.material.model.value, r.material.mu, r.material.lam, r.tets, r.shape_rows, r.volumes)
+               for r in system.regions]
+    xo, nwo, cgo, _, wo = newton.subproblem(x_tilde, xt, x_hat0, system.masses, regions, o, mu, params.offset, h,
+                                            dbc=system.dbc_mask)
+    xh = to_dev(x_hat0)
+    nw, cg, _, w = dev.solve_subproblem(aset, to_dev(x_tilde), x, xh, mu, params.offset, h, params.cg_tol,
+                                        params.decay)
+    xg = to_host(xh)
+    assert nw == nwo and abs(cg - cgo) <= 1
+    assert np.abs(xg - xo).max() <= 1e-6 * np.abs(xo - xt).max()
+    sg = aset.export_state()
+    assert np.array_equal(sg[3], o.gamma)
+    assert np.abs(sg[2] - o.lam).max() <= 1e-6 * max(np.abs(o.lam).max(), 1e-30)
+    assert w == pytest.approx(wo, rel=1e-6)
