@@ -35,8 +35,7 @@ struct Operator {
   const int* col = nullptr;           // (nb)
   const double* val = nullptr;        // (nb,9)
   const int* low_ptr = nullptr;       // (n+1)
-  const int* low_blk = nullptr;       // (nl) block ids b with col(b) = row, row(b) < col
-  const int* low_row = nullptr;       // (nl) row(b)
+  const int2* low_pair = nullptr;     // (nl) (block b, row(b)) with col(b) = row, row(b) < col
   const uint8_t* mask = nullptr;      // (n) DBC mask (contact masking) or null
   const double* pinv = nullptr;       // (n,9) inverse diagonal blocks
   ContactView contact;

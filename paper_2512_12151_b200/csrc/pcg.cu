@@ -46,22 +46,60 @@ __device__ __forceinline__ void contact_dot(const Operator& op, const double* __
   cv.t[c] = cv.coef[c] * acc;
 }
 
-// (H p)_i[r] for one row and component: upper blocks, transposed lower
-// blocks, then the contact gather.
+// 9 doubles of block b with 16-byte loads: val is a library allocation
+// (256B-aligned), so 72b bytes is 16B-aligned exactly for even b.
+template <bool NC>
+__device__ __forceinline__ void load_block(const double* __restrict__ val, int b, double B[9]) {
+  const double* src = val + 9 * (size_t)b;
+  if ((b & 1) == 0) {
+    const double2* v2 = reinterpret_cast<const double2*>(src);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const double2 t = NC ? __ldg(v2 + k) : v2[k];
+      B[2 * k] = t.x;
+      B[2 * k + 1] = t.y;
+    }
+    B[8] = NC ? __ldg(src + 8) : src[8];
+  } else {
+    B[0] = NC ? __ldg(src) : src[0];
+    const double2* v2 = reinterpret_cast<const double2*>(src + 1);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const double2 t = NC ? __ldg(v2 + k) : v2[k];
+      B[1 + 2 * k] = t.x;
+      B[2 + 2 * k] = t.y;
+    }
+  }
+}
+
+// p_j: caller-owned vectors carry no alignment promise beyond 8 bytes, so
+// the gather stays scalar (these reads are L1/L2 hits).
+__device__ __forceinline__ void load_vec3(const double* __restrict__ p, int j, double v[3]) {
+  const double* src = p + 3 * (size_t)j;
+  v[0] = src[0];
+  v[1] = src[1];
+  v[2] = src[2];
+}
+
+// (H p)_i[r] for one row and component (three threads per row): upper
+// blocks, transposed lower blocks via the transpose index, then the
+// matrix-free contact gather.  Block values are read-only for the whole
+// solve (non-coherent loads are safe); p is rewritten between phases of the
+// persistent kernel, so it is loaded coherently.
 __device__ __forceinline__ double row_product(const Operator& op, const double* __restrict__ p, int i, int r) {
   double acc = 0.0;
   const int b0 = op.row_ptr[i], b1 = op.row_ptr[i + 1];
   for (int b = b0; b < b1; ++b) {
-    const int j = op.col[b];
+    const int j = __ldg(op.col + b);
     const double* B = op.val + 9 * (size_t)b + 3 * r;
-    acc += B[0] * p[3 * j] + B[1] * p[3 * j + 1] + B[2] * p[3 * j + 2];
+    acc += __ldg(B) * p[3 * j] + __ldg(B + 1) * p[3 * j + 1] + __ldg(B + 2) * p[3 * j + 2];
   }
   const int l0 = op.low_ptr[i], l1 = op.low_ptr[i + 1];
   for (int e = l0; e < l1; ++e) {
-    const int b = op.low_blk[e];
-    const int k = op.low_row[e];
-    const double* B = op.val + 9 * (size_t)b + r;
-    acc += B[0] * p[3 * k] + B[3] * p[3 * k + 1] + B[6] * p[3 * k + 2];
+    const int2 bk = __ldg(op.low_pair + e);
+    const double* B = op.val + 9 * (size_t)bk.x + r;
+    const int k = bk.y;
+    acc += __ldg(B) * p[3 * k] + __ldg(B + 3) * p[3 * k + 1] + __ldg(B + 6) * p[3 * k + 2];
   }
   if (op.contact.n && !(op.mask && op.mask[i])) {
     const ContactView& cv = op.contact;
@@ -94,8 +132,7 @@ int spmv(const Operator& op, const double* x, double* y, cudaStream_t s) {
     k_contact_dot<<<(int)div_up(op.contact.n, 256), 256, 0, s>>>(op, x);
     IBF_LAUNCH_CHECK();
   }
-  const int64_t n3 = 3LL * op.n;
-  const int grid = (int)std::min<int64_t>(div_up(n3, 256), 148LL * 16);
+  const int grid = (int)std::min<int64_t>(div_up(3LL * op.n, 256), 148LL * 16);
   k_spmv<<<grid, 256, 0, s>>>(op, x, y);
   IBF_LAUNCH_CHECK();
   return IBF_OK;
@@ -410,8 +447,7 @@ struct ibf_bsr {
     o.col = col.p;
     o.val = val.p;
     o.low_ptr = low_ptr.p;
-    o.low_blk = low_blk.p;
-    o.low_row = low_row.p;
+    o.low_pair = reinterpret_cast<const int2*>(low_blk.p);
     o.pinv = pinv.p;
     return o;
   }
@@ -422,6 +458,7 @@ namespace ibf {
 int build_upper_structure(int64_t n, const std::vector<int64_t>& rows, const std::vector<int64_t>& cols,
                           DevBuf<int>& row_ptr, DevBuf<int>& col, DevBuf<int>& low_ptr, DevBuf<int>& low_blk,
                           DevBuf<int>& low_row, DevBuf<int>& diag_blk, DevBuf<int>& brow) {
+  // low_blk holds (block, row) pairs interleaved (int2), low_row is unused
   const int64_t nb = (int64_t)rows.size();
   std::vector<int> rp(n + 1, 0), cl(nb), db(n, -1), br(nb);
   for (int64_t b = 0; b < nb; ++b) {
@@ -446,7 +483,12 @@ int build_upper_structure(int64_t n, const std::vector<int64_t>& rows, const std
   IBF_TRY(row_ptr.upload(rp.data(), rp.size()));
   IBF_TRY(col.upload(cl.data(), cl.size()));
   IBF_TRY(low_ptr.upload(lp.data(), lp.size()));
-  IBF_TRY(low_blk.upload(lb.data(), lb.size()));
+  std::vector<int> pairs(2 * lb.size());
+  for (size_t k = 0; k < lb.size(); ++k) {
+    pairs[2 * k] = lb[k];
+    pairs[2 * k + 1] = lr[k];
+  }
+  IBF_TRY(low_blk.upload(pairs.data(), pairs.size()));
   IBF_TRY(low_row.upload(lr.data(), lr.size()));
   IBF_TRY(diag_blk.upload(db.data(), db.size()));
   IBF_TRY(brow.upload(br.data(), br.size()));

@@ -687,8 +687,7 @@ ibf::Operator ibf_system::op() const {
   o.col = col.p;
   o.val = val.p;
   o.low_ptr = low_ptr.p;
-  o.low_blk = low_blk.p;
-  o.low_row = low_row.p;
+  o.low_pair = reinterpret_cast<const int2*>(low_blk.p);
   o.pinv = pinv.p;
   o.mask = assembled_dbc ? dbc.p : nullptr;
   if (assembled_contacts) o.contact = ibf::contact_view(assembled_contacts);
