@@ -319,5 +319,12 @@ def test_contact_heavy_subproblem_parity(pkg, n, layers, frames):
     assert np.abs(xg - xo).max() <= 1e-6 * np.abs(xo - xt).max()
     sg = aset.export_state()
     assert np.array_equal(sg[3], o.gamma)
-    assert np.abs(sg[2] - o.lam).max() <= 1e-6 * max(np.abs(o.lam).max(), 1e-30)
-    assert w == pytest.approx(wo, rel=1e-6)
+    # lambda <- lambda - mu c with c = d + grad_d . (x_hat - anchor) - offset
+    # (intact/contact.py:91-106): a position difference dx propagates as
+    # |dc| <= sum_k |w_k| |dx_k|_2 <= 2 sqrt(3) max|dx| (witness weights sum
+    # to 2 in absolute value), so the multipliers and the worst violation can
+    # only agree to that bound — a relative bound on lambda alone is wrong
+    # for constraints whose c is near zero.
+    dc = 2.0 * np.sqrt(3.0) * np.abs(xg - xo).max()
+    assert np.abs(sg[2] - o.lam).max() <= mu * dc + 1e-12 * np.abs(o.lam).max()
+    assert abs(w - wo) <= dc + 1e-12 * abs(wo)
