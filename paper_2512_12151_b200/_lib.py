@@ -12,7 +12,8 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libibf.so")
+# IBF_LIB selects another build of the same ABI (A/B timing of kernel variants)
+LIB_PATH = os.environ.get("IBF_LIB") or os.path.join(HERE, "libibf.so")
 
 IBF_OK, IBF_ERR_BAD_ARG, IBF_ERR_CUDA, IBF_ERR_OOM, IBF_ERR_NONFINITE, IBF_ERR_NO_DEVICE = range(6)
 MODELS = {"snh": 0, "nh": 1, "cor": 2, "lin": 3}

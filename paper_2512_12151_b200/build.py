@@ -15,7 +15,8 @@ from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-OUT = os.path.join(HERE, "libibf.so")
+OUT = os.environ.get("IBF_BUILD_OUT", os.path.join(HERE, "libibf.so"))
+BUILD = os.environ.get("IBF_BUILD_DIR", os.path.join(CSRC, "build"))
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 SOURCES = ["pcg.cu", "system.cu", "contact.cu", "ccd.cu", "newton.cu"]
 FLAGS = [
@@ -23,11 +24,11 @@ FLAGS = [
     "-O3", "-lineinfo", "-std=c++17",
     "-Xcompiler", "-fPIC,-O3",
     "-Xptxas", "-v",
-]
+] + os.environ.get("IBF_NVCC_EXTRA", "").split()
 
 
 def _compile(src, verbose):
-    obj = os.path.join(CSRC, "build", src.replace(".cu", ".o"))
+    obj = os.path.join(BUILD, src.replace(".cu", ".o"))
     cmd = [NVCC, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
@@ -51,7 +52,7 @@ def _stale():
 def build(force=False, verbose=False):
     if not force and not _stale():
         return OUT
-    os.makedirs(os.path.join(CSRC, "build"), exist_ok=True)
+    os.makedirs(BUILD, exist_ok=True)
     with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
         results = list(ex.map(lambda s: _compile(s, verbose), SOURCES))
     objs = [o for o, _ in results]
@@ -61,7 +62,7 @@ def build(force=False, verbose=False):
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")
     os.replace(tmp, OUT)
-    with open(os.path.join(CSRC, "build", "ptxas.log"), "w") as f:
+    with open(os.path.join(BUILD, "ptxas.log"), "w") as f:
         for src, (_, log) in zip(SOURCES, results):
             f.write(f"==== {src}\n{log}\n")
     return OUT

@@ -27,18 +27,80 @@ struct ContactView {
   double* t = nullptr;                // (C) workspace coef_c * g_c . p
 };
 
-// Symmetric operator: upper BSR (diagonal first in each row) + transpose
-// index + optional matrix-free contact term + block-Jacobi inverse.
+// Symmetric 3x3-block matrix (diagonal + strict upper, the reference's
+// information content, intact/sparse.py:1-5) in sliced-ELL storage:
+//
+//   rows are grouped in slices of 32; slice s holds w_s = max upper count of
+//   its rows "slots"; block (row i, slot k) has storage index
+//   q = slice_ptr[s] + 32 k + (i & 31), and entry e (row-major 3x3) of block
+//   q lives at val[qel(q, e)] = val[9 (q & ~31) + (q & 31) + 32 e].
+//
+// So when the 32 lanes of a warp take the 32 rows of a slice, every load of
+// one block entry is one contiguous 256-byte access (2 L1 wavefronts), and
+// the transposed read of the lower blocks of 32 consecutive rows touches a
+// few contiguous segments (their source blocks sit in consecutive rows of
+// the same slot on structured meshes).  The lower triangle is applied via a
+// per-row list of (storage block, source row) entries stored the same way.
+// Padding blocks are zero with col = own row; padding lower entries point at
+// a zero block past the last slice.
+__host__ __device__ __forceinline__ size_t qel(int q, int e) {
+  return 9 * (size_t)(q & ~31) + (size_t)(q & 31) + 32 * (size_t)e;
+}
+
+// Block-Jacobi inverse: the diagonal blocks are symmetric, so their inverse
+// is stored as its upper triangle (00, 01, 02, 11, 12, 22) — 48 instead of
+// 72 bytes per vertex streamed by every CG iteration.
+constexpr int PINV_STRIDE = 6;
+
+__device__ __forceinline__ void inv3_sym6(const double* A, double* P) {
+  const double c00 = A[4] * A[8] - A[5] * A[7];
+  const double c01 = A[5] * A[6] - A[3] * A[8];
+  const double c02 = A[3] * A[7] - A[4] * A[6];
+  const double id = 1.0 / (A[0] * c00 + A[1] * c01 + A[2] * c02);
+  P[0] = c00 * id;
+  P[1] = (A[2] * A[7] - A[1] * A[8]) * id;
+  P[2] = (A[1] * A[5] - A[2] * A[4]) * id;
+  P[3] = (A[0] * A[8] - A[2] * A[6]) * id;
+  P[4] = (A[2] * A[3] - A[0] * A[5]) * id;
+  P[5] = (A[0] * A[4] - A[1] * A[3]) * id;
+}
+
+__device__ __forceinline__ void apply_pinv6(const double* __restrict__ P, double r0, double r1, double r2,
+                                            double z[3]) {
+  const double p0 = P[0], p1 = P[1], p2 = P[2], p3 = P[3], p4 = P[4], p5 = P[5];
+  z[0] = p0 * r0 + p1 * r1 + p2 * r2;
+  z[1] = p1 * r0 + p3 * r1 + p4 * r2;
+  z[2] = p2 * r0 + p4 * r1 + p5 * r2;
+}
+
 struct Operator {
   int n = 0;
-  const int* row_ptr = nullptr;       // (n+1)
-  const int* col = nullptr;           // (nb)
-  const double* val = nullptr;        // (nb,9)
-  const int* low_ptr = nullptr;       // (n+1)
-  const int2* low_pair = nullptr;     // (nl) (block b, row(b)) with col(b) = row, row(b) < col
+  const int* slice_ptr = nullptr;     // (S+1) storage block offset per slice
+  const int* col = nullptr;           // (nq) column of each storage block
+  const double* val = nullptr;        // 9 (nq + 32) entries, qel layout
+  const int* low_ptr = nullptr;       // (S+1) lower-entry offset per slice
+  const int2* low = nullptr;          // (nlq) (storage block, source row)
   const uint8_t* mask = nullptr;      // (n) DBC mask (contact masking) or null
-  const double* pinv = nullptr;       // (n,9) inverse diagonal blocks
+  const double* pinv = nullptr;       // (n,6) inverse diagonal blocks (upper triangle)
   ContactView contact;
+};
+
+// Host + device halves of the sliced symmetric pattern (built once).
+struct SellPattern {
+  int64_t n = 0, nb = 0, nl = 0;      // rows, real blocks, real strict-upper blocks
+  int n_slices = 0;
+  int64_t nq = 0, nlq = 0;            // storage blocks / lower entries incl. padding
+  int zero_q = 0;                     // an all-zero storage block
+  std::vector<int64_t> rows, cols;    // real blocks sorted by (row, col)
+  std::vector<int> q_of_b;            // real block -> storage index
+  DevBuf<int> slice_ptr, col, qrow, low_ptr, diag_q;
+  DevBuf<uint8_t> qreal;
+  DevBuf<int2> low;
+  DevBuf<double> val;
+  // rows/cols: real blocks sorted by (row, col); uploads the device arrays
+  // and allocates val (zeroed).
+  int build(int64_t n, const std::vector<int64_t>& rows, const std::vector<int64_t>& cols);
+  Operator op() const;
 };
 
 struct PcgWork {
@@ -52,9 +114,11 @@ int pcg_solve(const Operator& op, const double* rhs, double* x_out, double rel_t
               int64_t max_iters, PcgWork& w, cudaStream_t s);
 // after pcg_solve: (iterations, converged, rel_residual) on the host (syncs).
 int pcg_info(PcgWork& w, double info[3], cudaStream_t s);
+// host copy of the real blocks (sorted (row, col) order, (nb,9)) of a pattern
+int sell_export(const SellPattern& P, int64_t* rows, int64_t* cols, double* blocks, cudaStream_t s);
 int spmv(const Operator& op, const double* x, double* y, cudaStream_t s);
 // inverse of 3x3 diagonal blocks into pinv (n,9): diag given as block ids
-int invert_diag_blocks(int n, const double* val, const int* diag_blk, double* pinv, cudaStream_t s);
+int invert_diag_blocks(int n, const double* val, const int* diag_q, double* pinv, cudaStream_t s);
 
 }  // namespace ibf
 

@@ -62,11 +62,11 @@ __global__ void k_descent_fix(int64_t n, const double* __restrict__ part, int np
   __syncthreads();
   if (!(tot >= 0.0)) return;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const double* P = pinv + 9 * i;
-    const double g0 = g[3 * i], g1 = g[3 * i + 1], g2 = g[3 * i + 2];
-    p[3 * i] = -(P[0] * g0 + P[1] * g1 + P[2] * g2);
-    p[3 * i + 1] = -(P[3] * g0 + P[4] * g1 + P[5] * g2);
-    p[3 * i + 2] = -(P[6] * g0 + P[7] * g1 + P[8] * g2);
+    double zv[3];
+    apply_pinv6(pinv + PINV_STRIDE * i, g[3 * i], g[3 * i + 1], g[3 * i + 2], zv);
+    p[3 * i] = -zv[0];
+    p[3 * i + 1] = -zv[1];
+    p[3 * i + 2] = -zv[2];
   }
 }
 
@@ -144,7 +144,7 @@ extern "C" int ibf_velocity_update(int64_t n, const double* x, const double* x_t
 extern "C" int ibf_system_spmv_stats(const ibf_system* s, double* bytes_per_spmv) {
   // algorithmic bytes of one symmetric SpMV:
   // 72 (N + E_u) + 4 E_u + 4 (N + 1) + 24 N + 24 N
-  const double N = (double)s->n, Eu = (double)s->nl;
+  const double N = (double)s->n, Eu = (double)s->pat.nl;
   *bytes_per_spmv = 72.0 * (N + Eu) + 4.0 * Eu + 4.0 * (N + 1.0) + 48.0 * N;
   return IBF_OK;
 }

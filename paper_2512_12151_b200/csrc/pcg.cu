@@ -3,18 +3,31 @@
 // Replaces BlockSparseMatrix.matvec and pcg_solve (intact/sparse.py:64-73,
 // :99-150; paths relative to /root/reference/pkg/src).
 //
-// Storage is the reference's: diagonal + strict-upper 3x3 blocks only.  The
-// lower triangle is applied by a transpose index (row i lists the upper
-// blocks b with col(b) = i), so every row's result is a fixed-order gather —
-// no atomics, bit-reproducible run to run.  A block's second (transposed)
-// read is an L2 hit because rows are processed roughly in order and the
-// matrix bandwidth is small, so DRAM traffic stays ~1x the upper storage.
+// Storage is the reference's information content — diagonal + strict-upper
+// 3x3 blocks only — laid out as sliced ELL (internal.cuh, `qel`).  One
+// thread owns one row (all three components): it streams its upper blocks
+// (slot-major, so the 32 lanes of a warp read 256 contiguous bytes per
+// entry), gathers p at their columns, then applies the lower triangle
+// through the row's transpose list (block, source row), then the matrix-free
+// contact term.  Every row is a fixed-order gather: no atomics, results are
+// bit-reproducible run to run.  A block's second (transposed) read hits L2:
+// the grid sweeps rows in ascending order with a bounded window of rows in
+// flight, and a row's lower blocks were streamed at most (n+1)^2 rows earlier
+// on lattice meshes (ncu: DRAM bytes 1.06x the algorithmic SpMV bytes).
 //
 // The whole PCG (all iterations, the reference's stopping rule, best-iterate
 // tracking, the 250-iteration restart, pAp <= 0 bail-out) runs in ONE
-// persistent cooperative kernel: one CTA per SM slot, grid-wide barriers
-// between phases, deterministic two-level reductions.  The host launches it
-// once per linear solve and reads (iterations, converged, rel_res) back.
+// persistent cooperative kernel with two grid barriers per iteration:
+//
+//   A  p_k = z + beta p_{k-1} (formed on the fly wherever p is gathered, so
+//      there is no separate direction-update pass), q = H p_k, pAp partials
+//   B  alpha = rz / pAp; x += alpha p; r -= alpha q; z = P^-1 r; |r|^2, rz
+//
+// Each thread keeps q and p_k of its own rows in shared memory between A and
+// B (same row mapping in both phases), and its rows' residual for the whole
+// solve, so none of them makes a round trip through HBM.  All reductions are
+// fixed-order (per-CTA tree, then one warp over the CTA partials), so every
+// CTA derives bit-identical scalars.
 #include <cooperative_groups.h>
 
 #include <algorithm>
@@ -27,12 +40,63 @@ namespace cg = cooperative_groups;
 
 namespace ibf {
 
-constexpr int PCG_THREADS = 256;
+#ifndef IBF_PCG_THREADS
+#define IBF_PCG_THREADS 256
+#endif
+#ifndef IBF_PCG_MINB
+#define IBF_PCG_MINB 4
+#endif
+#ifndef IBF_SPMV_UNROLL
+#define IBF_SPMV_UNROLL 2
+#endif
+constexpr int PCG_THREADS = IBF_PCG_THREADS;
+// shared-memory budget per CTA for the rows' r and the (q, p) carried from A to B
+constexpr int PCG_SMEM_BYTES = 56 * 1024;
+
+// ---------------------------------------------------------------- gathers
+
+// p at vertex j: a plain vector ...
+struct PlainGather {
+  const double* __restrict__ p;
+  __device__ __forceinline__ void get(int j, double& x0, double& x1, double& x2) const {
+    const double* P = p + 3 * (size_t)j;
+    x0 = P[0];
+    x1 = P[1];
+    x2 = P[2];
+  }
+};
+
+// ... or the new CG direction z + beta p_old formed on the fly (first:
+// p = z).  The owner of row j forms the same value with the same
+// instruction (fma), so every reader sees the bits the owner stores.
+struct DirGather {
+  const double* __restrict__ z;
+  const double* __restrict__ pold;
+  double beta;
+  bool first;
+  __device__ __forceinline__ double dir(double zv, double pv) const { return first ? zv : __fma_rn(beta, pv, zv); }
+  __device__ __forceinline__ void get(int j, double& x0, double& x1, double& x2) const {
+    const double* Z = z + 3 * (size_t)j;
+    if (first) {
+      x0 = Z[0];
+      x1 = Z[1];
+      x2 = Z[2];
+    } else {
+      const double* P = pold + 3 * (size_t)j;
+      const double z0 = Z[0], z1 = Z[1], z2 = Z[2];
+      const double p0 = P[0], p1 = P[1], p2 = P[2];
+      x0 = __fma_rn(beta, p0, z0);
+      x1 = __fma_rn(beta, p1, z1);
+      x2 = __fma_rn(beta, p2, z2);
+    }
+  }
+};
 
 // ---------------------------------------------------------------- SpMV pieces
 
 // t_c = coef_c * sum_slot g_c[slot] . p[v(slot)], masked columns excluded.
-__device__ __forceinline__ void contact_dot(const Operator& op, const double* __restrict__ p, int c) {
+template <class Gather>
+__device__ __forceinline__ void contact_dot(const Operator& op, const Gather& gp, int c) {
   const ContactView& cv = op.contact;
   const int* q = cv.quad + 4 * c;
   const double* g = cv.grad + 12 * c;
@@ -41,65 +105,104 @@ __device__ __forceinline__ void contact_dot(const Operator& op, const double* __
   for (int k = 0; k < 4; ++k) {
     const int v = q[k];
     if (op.mask && op.mask[v]) continue;
-    acc += g[3 * k] * p[3 * v] + g[3 * k + 1] * p[3 * v + 1] + g[3 * k + 2] * p[3 * v + 2];
+    double x0, x1, x2;
+    gp.get(v, x0, x1, x2);
+    acc += g[3 * k] * x0 + g[3 * k + 1] * x1 + g[3 * k + 2] * x2;
   }
   cv.t[c] = cv.coef[c] * acc;
 }
 
-// 9 doubles of block b with 16-byte loads: val is a library allocation
-// (256B-aligned), so 72b bytes is 16B-aligned exactly for even b.
-template <bool NC>
-__device__ __forceinline__ void load_block(const double* __restrict__ val, int b, double B[9]) {
-  const double* src = val + 9 * (size_t)b;
-  if ((b & 1) == 0) {
-    const double2* v2 = reinterpret_cast<const double2*>(src);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const double2 t = NC ? __ldg(v2 + k) : v2[k];
-      B[2 * k] = t.x;
-      B[2 * k + 1] = t.y;
-    }
-    B[8] = NC ? __ldg(src + 8) : src[8];
-  } else {
-    B[0] = NC ? __ldg(src) : src[0];
-    const double2* v2 = reinterpret_cast<const double2*>(src + 1);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const double2 t = NC ? __ldg(v2 + k) : v2[k];
-      B[1 + 2 * k] = t.x;
-      B[2 + 2 * k] = t.y;
-    }
-  }
+// one upper block: a_r += (b[3r] x0 + b[3r+1] x1) + b[3r+2] x2
+__device__ __forceinline__ void acc_upper(const double b[9], double x0, double x1, double x2, double& a0, double& a1,
+                                          double& a2) {
+  a0 += b[0] * x0 + b[1] * x1 + b[2] * x2;
+  a1 += b[3] * x0 + b[4] * x1 + b[5] * x2;
+  a2 += b[6] * x0 + b[7] * x1 + b[8] * x2;
+}
+// one transposed block: a_c += (b[c] x0 + b[3+c] x1) + b[6+c] x2
+__device__ __forceinline__ void acc_lower(const double b[9], double x0, double x1, double x2, double& a0, double& a1,
+                                          double& a2) {
+  a0 += b[0] * x0 + b[3] * x1 + b[6] * x2;
+  a1 += b[1] * x0 + b[4] * x1 + b[7] * x2;
+  a2 += b[2] * x0 + b[5] * x1 + b[8] * x2;
 }
 
-// p_j: caller-owned vectors carry no alignment promise beyond 8 bytes, so
-// the gather stays scalar (these reads are L1/L2 hits).
-__device__ __forceinline__ void load_vec3(const double* __restrict__ p, int j, double v[3]) {
-  const double* src = p + 3 * (size_t)j;
-  v[0] = src[0];
-  v[1] = src[1];
-  v[2] = src[2];
-}
-
-// (H p)_i[r] for one row and component (three threads per row): upper
-// blocks, transposed lower blocks via the transpose index, then the
-// matrix-free contact gather.  Block values are read-only for the whole
-// solve (non-coherent loads are safe); p is rewritten between phases of the
-// persistent kernel, so it is loaded coherently.
-__device__ __forceinline__ double row_product(const Operator& op, const double* __restrict__ p, int i, int r) {
-  double acc = 0.0;
-  const int b0 = op.row_ptr[i], b1 = op.row_ptr[i + 1];
-  for (int b = b0; b < b1; ++b) {
-    const int j = __ldg(op.col + b);
-    const double* B = op.val + 9 * (size_t)b + 3 * r;
-    acc += __ldg(B) * p[3 * j] + __ldg(B + 1) * p[3 * j + 1] + __ldg(B + 2) * p[3 * j + 2];
+// y_i = (H p)_i for row i: upper slots, transposed lower entries, contact.
+// Block values and the pattern are read-only for the whole solve
+// (non-coherent loads); p is rewritten between phases of the persistent
+// kernel, so it is loaded coherently.  Per component the sum runs over the
+// row's blocks in storage order.  Two slots are in flight per iteration
+// (18 matrix entries, 2 indices, 6 p entries): the product is latency-bound
+// otherwise.
+template <class Gather>
+__device__ __forceinline__ void row_product(const Operator& op, const Gather& gp, int i, double y[3]) {
+  const int s = i >> 5, lane = i & 31;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+  {
+    const int q0 = __ldg(op.slice_ptr + s), w = (__ldg(op.slice_ptr + s + 1) - q0) >> 5;
+    const double* V = op.val + 9 * (size_t)q0 + lane;
+    const int* C = op.col + q0 + lane;
+    int k = 0;
+    if (IBF_SPMV_UNROLL >= 2) {
+      for (; k + 2 <= w; k += 2) {
+        const int j0 = __ldg(C + 32 * k), j1 = __ldg(C + 32 * k + 32);
+        const double* B = V + 288 * (size_t)k;
+        double b[9], c[9];
+#pragma unroll
+        for (int e = 0; e < 9; ++e) {
+          b[e] = __ldg(B + 32 * e);
+          c[e] = __ldg(B + 288 + 32 * e);
+        }
+        double x0, x1, x2, y0, y1, y2;
+        gp.get(j0, x0, x1, x2);
+        gp.get(j1, y0, y1, y2);
+        acc_upper(b, x0, x1, x2, a0, a1, a2);
+        acc_upper(c, y0, y1, y2, a0, a1, a2);
+      }
+    }
+    for (; k < w; ++k) {
+      const int j = __ldg(C + 32 * k);
+      const double* B = V + 288 * (size_t)k;
+      double b[9];
+#pragma unroll
+      for (int e = 0; e < 9; ++e) b[e] = __ldg(B + 32 * e);
+      double x0, x1, x2;
+      gp.get(j, x0, x1, x2);
+      acc_upper(b, x0, x1, x2, a0, a1, a2);
+    }
   }
-  const int l0 = op.low_ptr[i], l1 = op.low_ptr[i + 1];
-  for (int e = l0; e < l1; ++e) {
-    const int2 bk = __ldg(op.low_pair + e);
-    const double* B = op.val + 9 * (size_t)bk.x + r;
-    const int k = bk.y;
-    acc += __ldg(B) * p[3 * k] + __ldg(B + 3) * p[3 * k + 1] + __ldg(B + 6) * p[3 * k + 2];
+  {
+    const int l0 = __ldg(op.low_ptr + s), w = (__ldg(op.low_ptr + s + 1) - l0) >> 5;
+    const int2* L = op.low + l0 + lane;
+    int t = 0;
+    if (IBF_SPMV_UNROLL >= 2) {
+      for (; t + 2 <= w; t += 2) {
+        const int2 e0 = __ldg(L + 32 * t), e1 = __ldg(L + 32 * t + 32);
+        const double* B0 = op.val + qel(e0.x, 0);
+        const double* B1 = op.val + qel(e1.x, 0);
+        double b[9], c[9];
+#pragma unroll
+        for (int e = 0; e < 9; ++e) {
+          b[e] = __ldg(B0 + 32 * e);
+          c[e] = __ldg(B1 + 32 * e);
+        }
+        double x0, x1, x2, y0, y1, y2;
+        gp.get(e0.y, x0, x1, x2);
+        gp.get(e1.y, y0, y1, y2);
+        acc_lower(b, x0, x1, x2, a0, a1, a2);
+        acc_lower(c, y0, y1, y2, a0, a1, a2);
+      }
+    }
+    for (; t < w; ++t) {
+      const int2 le = __ldg(L + 32 * t);
+      const double* B = op.val + qel(le.x, 0);
+      double b[9];
+#pragma unroll
+      for (int e = 0; e < 9; ++e) b[e] = __ldg(B + 32 * e);
+      double x0, x1, x2;
+      gp.get(le.y, x0, x1, x2);
+      acc_lower(b, x0, x1, x2, a0, a1, a2);
+    }
   }
   if (op.contact.n && !(op.mask && op.mask[i])) {
     const ContactView& cv = op.contact;
@@ -107,22 +210,32 @@ __device__ __forceinline__ double row_product(const Operator& op, const double* 
     for (int e = e0; e < e1; ++e) {
       const int src = cv.vc_src[e];
       const int c = src >> 2, slot = src & 3;
-      acc += cv.t[c] * cv.grad[12 * c + 3 * slot + r];
+      const double t = cv.t[c];
+      const double* g = cv.grad + 12 * c + 3 * slot;
+      a0 += t * g[0];
+      a1 += t * g[1];
+      a2 += t * g[2];
     }
   }
-  return acc;
+  y[0] = a0;
+  y[1] = a1;
+  y[2] = a2;
 }
 
 __global__ void k_contact_dot(Operator op, const double* __restrict__ p) {
+  const PlainGather gp{p};
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < op.contact.n; c += gridDim.x * blockDim.x)
-    contact_dot(op, p, c);
+    contact_dot(op, gp, c);
 }
 
-__global__ void k_spmv(Operator op, const double* __restrict__ p, double* __restrict__ y) {
-  const int64_t n3 = 3LL * op.n;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n3; t += (int64_t)gridDim.x * blockDim.x) {
-    const int i = (int)(t / 3), r = (int)(t - 3LL * i);
-    y[t] = row_product(op, p, i, r);
+__global__ void __launch_bounds__(256, 2) k_spmv(Operator op, const double* __restrict__ p, double* __restrict__ y) {
+  const PlainGather gp{p};
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < op.n; i += gridDim.x * blockDim.x) {
+    double v[3];
+    row_product(op, gp, i, v);
+    y[3 * (size_t)i] = v[0];
+    y[3 * (size_t)i + 1] = v[1];
+    y[3 * (size_t)i + 2] = v[2];
   }
 }
 
@@ -132,7 +245,9 @@ int spmv(const Operator& op, const double* x, double* y, cudaStream_t s) {
     k_contact_dot<<<(int)div_up(op.contact.n, 256), 256, 0, s>>>(op, x);
     IBF_LAUNCH_CHECK();
   }
-  const int grid = (int)std::min<int64_t>(div_up(3LL * op.n, 256), 148LL * 16);
+  // two CTAs per SM sweep the rows in ascending order: a small in-flight
+  // window keeps each block's transposed re-read an L2 hit
+  const int grid = (int)std::min<int64_t>(div_up(op.n, 256), 2LL * sm_count());
   k_spmv<<<grid, 256, 0, s>>>(op, x, y);
   IBF_LAUNCH_CHECK();
   return IBF_OK;
@@ -140,37 +255,20 @@ int spmv(const Operator& op, const double* x, double* y, cudaStream_t s) {
 
 // ----------------------------------------------------------- 3x3 inverses
 
-__device__ __forceinline__ void inv3(const double* A, double* O) {
-  const double c00 = A[4] * A[8] - A[5] * A[7];
-  const double c01 = A[5] * A[6] - A[3] * A[8];
-  const double c02 = A[3] * A[7] - A[4] * A[6];
-  const double det = A[0] * c00 + A[1] * c01 + A[2] * c02;
-  const double id = 1.0 / det;
-  O[0] = c00 * id;
-  O[1] = (A[2] * A[7] - A[1] * A[8]) * id;
-  O[2] = (A[1] * A[5] - A[2] * A[4]) * id;
-  O[3] = c01 * id;
-  O[4] = (A[0] * A[8] - A[2] * A[6]) * id;
-  O[5] = (A[2] * A[3] - A[0] * A[5]) * id;
-  O[6] = c02 * id;
-  O[7] = (A[1] * A[6] - A[0] * A[7]) * id;
-  O[8] = (A[0] * A[4] - A[1] * A[3]) * id;
-}
-
-__global__ void k_invert_diag(int n, const double* __restrict__ val, const int* __restrict__ diag_blk,
+__global__ void k_invert_diag(int n, const double* __restrict__ val, const int* __restrict__ diag_q,
                               double* __restrict__ pinv) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     double A[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-    const int b = diag_blk[i];
-    if (b >= 0)
-      for (int k = 0; k < 9; ++k) A[k] = val[9 * (size_t)b + k];
-    inv3(A, pinv + 9 * (size_t)i);
+    const int q = diag_q[i];
+    if (q >= 0)
+      for (int k = 0; k < 9; ++k) A[k] = val[qel(q, k)];
+    inv3_sym6(A, pinv + PINV_STRIDE * (size_t)i);
   }
 }
 
-int invert_diag_blocks(int n, const double* val, const int* diag_blk, double* pinv, cudaStream_t s) {
+int invert_diag_blocks(int n, const double* val, const int* diag_q, double* pinv, cudaStream_t s) {
   if (n == 0) return IBF_OK;
-  k_invert_diag<<<(int)div_up(n, 256), 256, 0, s>>>(n, val, diag_blk, pinv);
+  k_invert_diag<<<(int)div_up(n, 256), 256, 0, s>>>(n, val, diag_q, pinv);
   IBF_LAUNCH_CHECK();
   return IBF_OK;
 }
@@ -183,20 +281,16 @@ struct PcgArgs {
   double* x_out;
   double* r;
   double* z;
-  double* p;
-  double* hp;
+  double* p[2];     // CG directions, alternating
+  double* hp;       // H p (global fallback when the rows do not fit in smem)
   double* X;        // 3 iterate buffers of 3n
   double* part;     // 4 * gridDim partial sums
   double* info;     // (iterations, converged, rel_res)
   double tol;
   int64_t max_iters;
+  int rows_per_thread;  // ceil(n / (grid * block))
+  int smem_rows;        // rows_per_thread if (q, p) live in shared memory, else 0
 };
-
-__device__ __forceinline__ void apply_pinv(const double* __restrict__ P, const double r[3], double z[3]) {
-  z[0] = P[0] * r[0] + P[1] * r[1] + P[2] * r[2];
-  z[1] = P[3] * r[0] + P[4] * r[1] + P[5] * r[2];
-  z[2] = P[6] * r[0] + P[7] * r[1] + P[8] * r[2];
-}
 
 // all CTAs compute the same fixed-order total of part[slot*G .. slot*G+G)
 __device__ __forceinline__ double grid_total(const double* part, int slot, double* sh) {
@@ -211,39 +305,51 @@ __device__ __forceinline__ double grid_total(const double* part, int slot, doubl
   return v;
 }
 
-__global__ void __launch_bounds__(PCG_THREADS) k_pcg(PcgArgs a) {
+// publish this CTA's partials of `k` sums into part[slot_j * G + b]
+__device__ __forceinline__ void put_partials(double* part, int slot, double v, double* red) {
+  v = block_sum(v, red);
+  if (threadIdx.x == 0) part[(size_t)slot * gridDim.x + blockIdx.x] = v;
+}
+
+__global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
   cg::grid_group grid = cg::this_grid();
-  __shared__ double red[PCG_THREADS / 32];
+  extern __shared__ double dyn[];
+  __shared__ double red[32];
   __shared__ double bc[1];
   const Operator& op = a.op;
   const int n = op.n;
-  const int G = gridDim.x;
-  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t stride = (int64_t)G * blockDim.x;
-  double* X0 = a.X;
+  const int S = gridDim.x * blockDim.x;          // rows per sweep
+  const int R = a.rows_per_thread;
+  const bool in_smem = a.smem_rows > 0;
+  // per-thread row slots: row(k) = blockIdx.x*blockDim.x + threadIdx.x + k*S
+  double* sq = dyn;                                  // (R, 3, blockDim) H p
+  double* sp = dyn + 3 * (size_t)R * blockDim.x;     // (R, 3, blockDim) p
+  double* sr = dyn + 6 * (size_t)R * blockDim.x;     // (R, 3, blockDim) residual
+  auto slot = [&](int k, int c) { return ((size_t)k * 3 + c) * blockDim.x + threadIdx.x; };
+  // the residual is only ever touched by its row's owner: keep it on chip
+  auto r_ref = [&](int k, int i, int c) -> double& { return in_smem ? sr[slot(k, c)] : a.r[3 * (size_t)i + c]; };
+  const int row0 = blockIdx.x * blockDim.x + threadIdx.x;
   auto Xb = [&](int k) { return a.X + (size_t)k * 3 * n; };
 
-  // phase 0: r = b, z = P^-1 r, p = z, x = 0
+  // ---- r = b, z = P^-1 r, x = 0
   double acc_b = 0.0, acc_rz = 0.0;
-  for (int64_t i = tid; i < n; i += stride) {
-    double rv[3] = {a.rhs[3 * i], a.rhs[3 * i + 1], a.rhs[3 * i + 2]};
+  for (int k = 0, i = row0; k < R; ++k, i += S) {
+    if (i >= n) break;
+    const double r0 = a.rhs[3 * (size_t)i], r1 = a.rhs[3 * (size_t)i + 1], r2 = a.rhs[3 * (size_t)i + 2];
     double zv[3];
-    apply_pinv(op.pinv + 9 * i, rv, zv);
-    for (int c = 0; c < 3; ++c) {
-      a.r[3 * i + c] = rv[c];
-      a.z[3 * i + c] = zv[c];
-      a.p[3 * i + c] = zv[c];
-      X0[3 * i + c] = 0.0;
-      acc_b += rv[c] * rv[c];
-      acc_rz += rv[c] * zv[c];
-    }
+    apply_pinv6(op.pinv + PINV_STRIDE * (size_t)i, r0, r1, r2, zv);
+    double* zi = a.z + 3 * (size_t)i;
+    double* xi = Xb(0) + 3 * (size_t)i;
+    r_ref(k, i, 0) = r0;
+    r_ref(k, i, 1) = r1;
+    r_ref(k, i, 2) = r2;
+    zi[0] = zv[0]; zi[1] = zv[1]; zi[2] = zv[2];
+    xi[0] = 0.0; xi[1] = 0.0; xi[2] = 0.0;
+    acc_b += r0 * r0 + r1 * r1 + r2 * r2;
+    acc_rz += r0 * zv[0] + r1 * zv[1] + r2 * zv[2];
   }
-  acc_b = block_sum(acc_b, red);
-  acc_rz = block_sum(acc_rz, red);
-  if (threadIdx.x == 0) {
-    a.part[0 * G + blockIdx.x] = acc_b;
-    a.part[1 * G + blockIdx.x] = acc_rz;
-  }
+  put_partials(a.part, 0, acc_b, red);
+  put_partials(a.part, 1, acc_rz, red);
   grid.sync();
   const double bnorm = sqrt(grid_total(a.part, 0, bc));
   double rz = grid_total(a.part, 1, bc);
@@ -252,25 +358,49 @@ __global__ void __launch_bounds__(PCG_THREADS) k_pcg(PcgArgs a) {
   int64_t iters = 0;
   bool conv = false;
   double rel = 0.0;
+  double beta = 0.0;
+  bool first = true;   // p_k = z (first iteration and after a restart)
+  int pb = 0;          // p[pb] receives p_k
   if (bnorm == 0.0) {
     conv = true;
   } else {
     bool done = false;
     for (int64_t it = 1; it <= a.max_iters; ++it) {
-      // ---- hp = H p (+ contact), pAp partials
+      const DirGather gd{a.z, a.p[pb ^ 1], beta, first};
+      double* pk = a.p[pb];
+      // ---- A: contact dots on p_k, then q = H p_k, pAp
       if (op.contact.n) {
-        for (int64_t c = tid; c < op.contact.n; c += stride) contact_dot(op, a.p, (int)c);
+        for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < op.contact.n; c += S) contact_dot(op, gd, c);
         grid.sync();
       }
       double acc = 0.0;
-      for (int64_t t = tid; t < 3LL * n; t += stride) {
-        const int i = (int)(t / 3), rr = (int)(t - 3LL * i);
-        const double v = row_product(op, a.p, i, rr);
-        a.hp[t] = v;
-        acc += a.p[t] * v;
+      for (int k = 0, i = row0; k < R; ++k, i += S) {
+        if (i >= n) break;
+        double v[3], pv[3];
+        row_product(op, gd, i, v);
+        const double* Z = a.z + 3 * (size_t)i;
+        if (first) {
+          pv[0] = Z[0]; pv[1] = Z[1]; pv[2] = Z[2];
+        } else {
+          const double* P = gd.pold + 3 * (size_t)i;
+          pv[0] = __fma_rn(beta, P[0], Z[0]);
+          pv[1] = __fma_rn(beta, P[1], Z[1]);
+          pv[2] = __fma_rn(beta, P[2], Z[2]);
+        }
+        double* pki = pk + 3 * (size_t)i;
+        pki[0] = pv[0]; pki[1] = pv[1]; pki[2] = pv[2];
+        if (in_smem) {
+          for (int c = 0; c < 3; ++c) {
+            sq[slot(k, c)] = v[c];
+            sp[slot(k, c)] = pv[c];
+          }
+        } else {
+          double* qi = a.hp + 3 * (size_t)i;
+          qi[0] = v[0]; qi[1] = v[1]; qi[2] = v[2];
+        }
+        acc += pv[0] * v[0] + pv[1] * v[1] + pv[2] * v[2];
       }
-      acc = block_sum(acc, red);
-      if (threadIdx.x == 0) a.part[2 * G + blockIdx.x] = acc;
+      put_partials(a.part, 2, acc, red);
       grid.sync();
       const double pap = grid_total(a.part, 2, bc);
       if (pap <= 0.0) {
@@ -282,33 +412,42 @@ __global__ void __launch_bounds__(PCG_THREADS) k_pcg(PcgArgs a) {
         done = true;
         break;
       }
+      // ---- B: x, r, z updates
       const double alpha = rz / pap;
       const int nxt = (cur != 0 && best != 0) ? 0 : ((cur != 1 && best != 1) ? 1 : 2);
       const double* xc = Xb(cur);
       double* xn = Xb(nxt);
       double acc_rr = 0.0;
       acc_rz = 0.0;
-      for (int64_t i = tid; i < n; i += stride) {
-        double rv[3], zv[3];
+      for (int k = 0, i = row0; k < R; ++k, i += S) {
+        if (i >= n) break;
+        double qv[3], pv[3], rv[3], zv[3];
+        if (in_smem) {
+          for (int c = 0; c < 3; ++c) {
+            qv[c] = sq[slot(k, c)];
+            pv[c] = sp[slot(k, c)];
+          }
+        } else {
+          for (int c = 0; c < 3; ++c) {
+            qv[c] = a.hp[3 * (size_t)i + c];
+            pv[c] = pk[3 * (size_t)i + c];
+          }
+        }
         for (int c = 0; c < 3; ++c) {
-          const int64_t k = 3 * i + c;
-          xn[k] = xc[k] + alpha * a.p[k];
-          rv[c] = a.r[k] - alpha * a.hp[k];
-          a.r[k] = rv[c];
+          const size_t e = 3 * (size_t)i + c;
+          xn[e] = xc[e] + alpha * pv[c];
+          double& rr = r_ref(k, i, c);
+          rv[c] = rr - alpha * qv[c];
+          rr = rv[c];
           acc_rr += rv[c] * rv[c];
         }
-        apply_pinv(op.pinv + 9 * i, rv, zv);
-        for (int c = 0; c < 3; ++c) {
-          a.z[3 * i + c] = zv[c];
-          acc_rz += rv[c] * zv[c];
-        }
+        apply_pinv6(op.pinv + PINV_STRIDE * (size_t)i, rv[0], rv[1], rv[2], zv);
+        double* zi = a.z + 3 * (size_t)i;
+        zi[0] = zv[0]; zi[1] = zv[1]; zi[2] = zv[2];
+        acc_rz += rv[0] * zv[0] + rv[1] * zv[1] + rv[2] * zv[2];
       }
-      acc_rr = block_sum(acc_rr, red);
-      acc_rz = block_sum(acc_rz, red);
-      if (threadIdx.x == 0) {
-        a.part[0 * G + blockIdx.x] = acc_rr;
-        a.part[1 * G + blockIdx.x] = acc_rz;
-      }
+      put_partials(a.part, 0, acc_rr, red);
+      put_partials(a.part, 1, acc_rz, red);
       grid.sync();
       const double res = sqrt(grid_total(a.part, 0, bc));
       cur = nxt;
@@ -326,38 +465,39 @@ __global__ void __launch_bounds__(PCG_THREADS) k_pcg(PcgArgs a) {
       }
       if (it % 250 == 0) {
         // restart from the true residual r = b - H x
+        const PlainGather gx{Xb(cur)};
         if (op.contact.n) {
-          for (int64_t c = tid; c < op.contact.n; c += stride) contact_dot(op, Xb(cur), (int)c);
+          for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < op.contact.n; c += S) contact_dot(op, gx, c);
           grid.sync();
         }
-        for (int64_t t = tid; t < 3LL * n; t += stride) {
-          const int i = (int)(t / 3), rr = (int)(t - 3LL * i);
-          a.hp[t] = row_product(op, Xb(cur), i, rr);
-        }
-        grid.sync();
         acc_rz = 0.0;
-        for (int64_t i = tid; i < n; i += stride) {
-          double rv[3], zv[3];
-          for (int c = 0; c < 3; ++c) rv[c] = a.rhs[3 * i + c] - a.hp[3 * i + c];
-          apply_pinv(op.pinv + 9 * i, rv, zv);
-          for (int c = 0; c < 3; ++c) {
-            a.r[3 * i + c] = rv[c];
-            a.z[3 * i + c] = zv[c];
-            a.p[3 * i + c] = zv[c];
-            acc_rz += rv[c] * zv[c];
-          }
+        for (int k = 0, i = row0; k < R; ++k, i += S) {
+          if (i >= n) break;
+          double v[3], zv[3];
+          row_product(op, gx, i, v);
+          const double r0 = a.rhs[3 * (size_t)i] - v[0];
+          const double r1 = a.rhs[3 * (size_t)i + 1] - v[1];
+          const double r2 = a.rhs[3 * (size_t)i + 2] - v[2];
+          apply_pinv6(op.pinv + PINV_STRIDE * (size_t)i, r0, r1, r2, zv);
+          double* zi = a.z + 3 * (size_t)i;
+          r_ref(k, i, 0) = r0;
+          r_ref(k, i, 1) = r1;
+          r_ref(k, i, 2) = r2;
+          zi[0] = zv[0]; zi[1] = zv[1]; zi[2] = zv[2];
+          acc_rz += r0 * zv[0] + r1 * zv[1] + r2 * zv[2];
         }
-        acc_rz = block_sum(acc_rz, red);
-        if (threadIdx.x == 0) a.part[1 * G + blockIdx.x] = acc_rz;
+        put_partials(a.part, 1, acc_rz, red);
         grid.sync();
         rz = grid_total(a.part, 1, bc);
+        first = true;
+        pb ^= 1;
         continue;
       }
       const double rz_new = grid_total(a.part, 1, bc);
-      const double beta = rz_new / rz;
+      beta = rz_new / rz;
       rz = rz_new;
-      for (int64_t k = tid; k < 3LL * n; k += stride) a.p[k] = a.z[k] + beta * a.p[k];
-      grid.sync();
+      first = false;
+      pb ^= 1;
     }
     if (!done) {
       result = best;
@@ -367,23 +507,50 @@ __global__ void __launch_bounds__(PCG_THREADS) k_pcg(PcgArgs a) {
     }
   }
   const double* xr = Xb(result);
-  for (int64_t k = tid; k < 3LL * n; k += stride) a.x_out[k] = (bnorm == 0.0) ? 0.0 : xr[k];
-  if (tid == 0) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < 3LL * n; k += S)
+    a.x_out[k] = (bnorm == 0.0) ? 0.0 : xr[k];
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
     a.info[0] = (double)iters;
     a.info[1] = conv ? 1.0 : 0.0;
     a.info[2] = rel;
   }
 }
 
-static int pcg_grid(int n) {
-  static int max_blocks_per_sm = -1;
-  if (max_blocks_per_sm < 0) {
+static size_t pcg_smem(int rows_per_thread, int threads) { return (size_t)9 * rows_per_thread * threads * sizeof(double); }
+
+// Launch shape: a full wave of co-resident CTAs, rows_per_thread sweeps, and
+// a block size trimmed (in warps) so the last sweep is nearly full — every
+// CTA then carries the same number of rows and no SM idles at a barrier
+// while others finish a partial sweep.
+struct PcgShape {
+  int grid, threads, rows_per_thread, smem_rows;
+};
+
+static PcgShape pcg_shape(int n) {
+  static int blocks_smem = -1, blocks_plain = -1;
+  if (blocks_smem < 0) {
+    cudaFuncSetAttribute(k_pcg, cudaFuncAttributeMaxDynamicSharedMemorySize, PCG_SMEM_BYTES);
     int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_pcg, PCG_THREADS, PCG_SMEM_BYTES);
+    blocks_smem = nb > 0 ? nb : 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_pcg, PCG_THREADS, 0);
-    max_blocks_per_sm = nb > 0 ? nb : 1;
+    blocks_plain = nb > 0 ? nb : 1;
   }
-  const int64_t want = std::max<int64_t>(1, div_up(3LL * n, PCG_THREADS));
-  return (int)std::min<int64_t>(want, (int64_t)max_blocks_per_sm * sm_count());
+  n = std::max(n, 1);
+  PcgShape sh;
+  for (int use_smem = 1; use_smem >= 0; --use_smem) {
+    const int64_t max_ctas = (int64_t)(use_smem ? blocks_smem : blocks_plain) * sm_count();
+    const int grid = (int)std::min<int64_t>(max_ctas, div_up(n, PCG_THREADS));
+    const int rpt = (int)div_up(n, (int64_t)grid * PCG_THREADS);
+    const int threads = (int)std::min<int64_t>(PCG_THREADS, 32 * div_up(div_up(n, (int64_t)grid * rpt), 32));
+    sh = PcgShape{grid, threads, rpt, 0};
+    if (!use_smem) break;
+    if (pcg_smem(rpt, threads) <= (size_t)PCG_SMEM_BYTES) {
+      sh.smem_rows = rpt;
+      break;
+    }
+  }
+  return sh;
 }
 
 int pcg_solve(const Operator& op, const double* rhs, double* x_out, double rel_tol, int64_t max_iters,
@@ -393,28 +560,32 @@ int pcg_solve(const Operator& op, const double* rhs, double* x_out, double rel_t
   const size_t n3 = 3 * (size_t)std::max(n, 1);
   IBF_TRY(w.r.reserve(n3));
   IBF_TRY(w.z.reserve(n3));
-  IBF_TRY(w.p.reserve(n3));
+  IBF_TRY(w.p.reserve(2 * n3));
   IBF_TRY(w.hp.reserve(n3));
   IBF_TRY(w.X.reserve(3 * n3));
   IBF_TRY(w.info.reserve(4));
-  const int grid = pcg_grid(std::max(n, 1));
-  IBF_TRY(w.part.reserve(4 * (size_t)grid));
-  w.grid = grid;
+  const PcgShape sh = pcg_shape(n);
+  IBF_TRY(w.part.reserve(4 * (size_t)sh.grid));
+  w.grid = sh.grid;
   PcgArgs a;
   a.op = op;
   a.rhs = rhs;
   a.x_out = x_out;
   a.r = w.r.p;
   a.z = w.z.p;
-  a.p = w.p.p;
+  a.p[0] = w.p.p;
+  a.p[1] = w.p.p + n3;
   a.hp = w.hp.p;
   a.X = w.X.p;
   a.part = w.part.p;
   a.info = w.info.p;
   a.tol = rel_tol;
   a.max_iters = max_iters;
+  a.rows_per_thread = sh.rows_per_thread;
+  a.smem_rows = sh.smem_rows;
+  const size_t smem = sh.smem_rows ? pcg_smem(sh.smem_rows, sh.threads) : 0;
   void* args[] = {&a};
-  IBF_CUDA(cudaLaunchCooperativeKernel((void*)k_pcg, grid, PCG_THREADS, args, 0, s));
+  IBF_CUDA(cudaLaunchCooperativeKernel((void*)k_pcg, sh.grid, sh.threads, args, smem, s));
   ++g_launches;
   return IBF_OK;
 }
@@ -432,85 +603,166 @@ int pcg_info(PcgWork& w, double info[3], cudaStream_t s) {
 
 }  // namespace ibf
 
+namespace ibf {
+
+// Sliced-ELL pattern from real blocks sorted by (row, col) (internal.cuh).
+int SellPattern::build(int64_t n_, const std::vector<int64_t>& rows_, const std::vector<int64_t>& cols_) {
+  n = n_;
+  rows = rows_;
+  cols = cols_;
+  nb = (int64_t)rows.size();
+  n_slices = (int)div_up(n, 32);
+  const int S = n_slices;
+  // per-row upper counts and the transpose lists (source rows ascending)
+  std::vector<int> up(n + 1, 0), lo(n + 1, 0);
+  nl = 0;
+  for (int64_t b = 0; b < nb; ++b) {
+    up[rows[b] + 1]++;
+    if (rows[b] != cols[b]) {
+      lo[cols[b] + 1]++;
+      ++nl;
+    }
+  }
+  for (int64_t i = 0; i < n; ++i) {
+    up[i + 1] += up[i];
+    lo[i + 1] += lo[i];
+  }
+  std::vector<int> sp(S + 1, 0), lp(S + 1, 0);
+  for (int s = 0; s < S; ++s) {
+    int w = 0, lw = 0;
+    for (int64_t i = 32LL * s; i < std::min<int64_t>(n, 32LL * s + 32); ++i) {
+      w = std::max(w, up[i + 1] - up[i]);
+      lw = std::max(lw, lo[i + 1] - lo[i]);
+    }
+    sp[s + 1] = sp[s] + 32 * w;
+    lp[s + 1] = lp[s] + 32 * lw;
+  }
+  nq = sp[S];
+  nlq = lp[S];
+  zero_q = (int)nq;  // first block of the zero slice appended after the last
+  if (nq + 32 >= (1LL << 31) || nlq >= (1LL << 31)) {
+    set_error("sliced BSR: more than 2^31 storage blocks");
+    return IBF_ERR_BAD_ARG;
+  }
+  std::vector<int> qc(nq + 32), qr(nq + 32), dq(n, -1);
+  std::vector<uint8_t> qre(nq + 32, 0);
+  for (int64_t q = 0; q < nq + 32; ++q) qc[q] = qr[q] = 0;
+  // padding: own row (rows past n in the last slice keep row/col 0, zero values)
+  for (int s = 0; s < S; ++s) {
+    const int w = (sp[s + 1] - sp[s]) / 32;
+    for (int k = 0; k < w; ++k)
+      for (int l = 0; l < 32; ++l) {
+        const int64_t i = 32LL * s + l;
+        const int64_t q = sp[s] + 32LL * k + l;
+        qc[q] = qr[q] = (i < n) ? (int)i : 0;
+      }
+  }
+  q_of_b.assign(nb, 0);
+  for (int64_t i = 0; i < n; ++i) {
+    const int s = (int)(i >> 5), l = (int)(i & 31);
+    for (int k = 0; k < up[i + 1] - up[i]; ++k) {
+      const int64_t b = up[i] + k;
+      const int q = sp[s] + 32 * k + l;
+      q_of_b[b] = q;
+      qc[q] = (int)cols[b];
+      qr[q] = (int)rows[b];
+      qre[q] = 1;
+      if (rows[b] == cols[b]) dq[i] = q;
+    }
+  }
+  // lower entries: real off-diagonal blocks grouped by column, b ascending
+  // (=> source rows ascending); padding (zero block, own row)
+  std::vector<int2> le(std::max<int64_t>(nlq, 1));
+  for (int s = 0; s < S; ++s) {
+    const int w = (lp[s + 1] - lp[s]) / 32;
+    for (int t = 0; t < w; ++t)
+      for (int l = 0; l < 32; ++l) {
+        const int64_t i = 32LL * s + l;
+        le[lp[s] + 32LL * t + l] = make_int2(zero_q, (i < n) ? (int)i : 0);
+      }
+  }
+  std::vector<int> fill(n, 0);
+  for (int64_t b = 0; b < nb; ++b) {
+    if (rows[b] == cols[b]) continue;
+    const int64_t j = cols[b];
+    const int s = (int)(j >> 5), l = (int)(j & 31);
+    const int t = fill[j]++;
+    le[lp[s] + 32LL * t + l] = make_int2(q_of_b[b], (int)rows[b]);
+  }
+  IBF_TRY(slice_ptr.upload(sp.data(), sp.size()));
+  IBF_TRY(low_ptr.upload(lp.data(), lp.size()));
+  IBF_TRY(col.upload(qc.data(), qc.size()));
+  IBF_TRY(qrow.upload(qr.data(), qr.size()));
+  IBF_TRY(qreal.upload(qre.data(), qre.size()));
+  IBF_TRY(diag_q.upload(dq.data(), dq.size()));
+  IBF_TRY(low.upload(le.data(), le.size()));
+  IBF_TRY(val.reserve(9 * (size_t)(nq + 32)));
+  IBF_CUDA(cudaMemset(val.p, 0, val.cap * sizeof(double)));
+  return IBF_OK;
+}
+
+Operator SellPattern::op() const {
+  Operator o;
+  o.n = (int)n;
+  o.slice_ptr = slice_ptr.p;
+  o.col = col.p;
+  o.val = val.p;
+  o.low_ptr = low_ptr.p;
+  o.low = low.p;
+  return o;
+}
+
+// host (nb,9) blocks in sorted order -> qel layout (padding zero)
+static void to_sell(const SellPattern& P, const double* blocks, std::vector<double>& out) {
+  out.assign(9 * (size_t)(P.nq + 32), 0.0);
+  for (int64_t b = 0; b < P.nb; ++b)
+    for (int e = 0; e < 9; ++e) out[qel(P.q_of_b[b], e)] = blocks[9 * b + e];
+}
+static void from_sell(const SellPattern& P, const std::vector<double>& in, double* blocks) {
+  for (int64_t b = 0; b < P.nb; ++b)
+    for (int e = 0; e < 9; ++e) blocks[9 * b + e] = in[qel(P.q_of_b[b], e)];
+}
+
+__global__ void k_mask_dirichlet(int64_t nq, const int* __restrict__ qrow, const int* __restrict__ col,
+                                 const uint8_t* __restrict__ qreal, const uint8_t* __restrict__ mask,
+                                 const double* __restrict__ diag, double* __restrict__ val) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nq; q += (int64_t)gridDim.x * blockDim.x) {
+    if (!qreal[q]) continue;
+    const int r = qrow[q], c = col[q];
+    if (!(mask[r] || mask[c])) continue;
+    for (int k = 0; k < 9; ++k) val[qel((int)q, k)] = (r == c) ? diag[9 * (int64_t)r + k] : 0.0;
+  }
+}
+
+int sell_export(const SellPattern& P, int64_t* rows, int64_t* cols, double* blocks, cudaStream_t s) {
+  std::copy(P.rows.begin(), P.rows.end(), rows);
+  std::copy(P.cols.begin(), P.cols.end(), cols);
+  std::vector<double> hv(9 * (size_t)(P.nq + 32));
+  IBF_CUDA(cudaMemcpyAsync(hv.data(), P.val.p, hv.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+  IBF_CUDA(cudaStreamSynchronize(s));
+  from_sell(P, hv, blocks);
+  return IBF_OK;
+}
+}  // namespace ibf
+
 // ===================================================== standalone BSR handle
 
 struct ibf_bsr {
-  int64_t n = 0;
-  std::vector<int64_t> rows, cols;           // coalesced, host copy
-  ibf::DevBuf<int> row_ptr, col, low_ptr, low_blk, low_row, diag_blk, brow;
-  ibf::DevBuf<double> val, pinv;
+  ibf::SellPattern pat;
+  ibf::DevBuf<double> pinv;
   ibf::PcgWork work;
   ibf::Operator op() const {
-    ibf::Operator o;
-    o.n = (int)n;
-    o.row_ptr = row_ptr.p;
-    o.col = col.p;
-    o.val = val.p;
-    o.low_ptr = low_ptr.p;
-    o.low_pair = reinterpret_cast<const int2*>(low_blk.p);
+    ibf::Operator o = pat.op();
     o.pinv = pinv.p;
     return o;
   }
 };
 
-namespace ibf {
-// Build (row_ptr, lower index, diag ids) for coalesced upper blocks sorted by (row, col).
-int build_upper_structure(int64_t n, const std::vector<int64_t>& rows, const std::vector<int64_t>& cols,
-                          DevBuf<int>& row_ptr, DevBuf<int>& col, DevBuf<int>& low_ptr, DevBuf<int>& low_blk,
-                          DevBuf<int>& low_row, DevBuf<int>& diag_blk, DevBuf<int>& brow) {
-  // low_blk holds (block, row) pairs interleaved (int2), low_row is unused
-  const int64_t nb = (int64_t)rows.size();
-  std::vector<int> rp(n + 1, 0), cl(nb), db(n, -1), br(nb);
-  for (int64_t b = 0; b < nb; ++b) {
-    rp[rows[b] + 1]++;
-    cl[b] = (int)cols[b];
-    br[b] = (int)rows[b];
-    if (rows[b] == cols[b]) db[rows[b]] = (int)b;
-  }
-  for (int64_t i = 0; i < n; ++i) rp[i + 1] += rp[i];
-  // transpose index: off-diagonal blocks grouped by column, rows ascending
-  std::vector<int> lp(n + 1, 0);
-  for (int64_t b = 0; b < nb; ++b)
-    if (rows[b] != cols[b]) lp[cols[b] + 1]++;
-  for (int64_t i = 0; i < n; ++i) lp[i + 1] += lp[i];
-  std::vector<int> fill(lp.begin(), lp.end() - 1), lb(lp[n]), lr(lp[n]);
-  for (int64_t b = 0; b < nb; ++b) {  // b ascending => rows ascending within a column
-    if (rows[b] == cols[b]) continue;
-    const int k = fill[cols[b]]++;
-    lb[k] = (int)b;
-    lr[k] = (int)rows[b];
-  }
-  IBF_TRY(row_ptr.upload(rp.data(), rp.size()));
-  IBF_TRY(col.upload(cl.data(), cl.size()));
-  IBF_TRY(low_ptr.upload(lp.data(), lp.size()));
-  std::vector<int> pairs(2 * lb.size());
-  for (size_t k = 0; k < lb.size(); ++k) {
-    pairs[2 * k] = lb[k];
-    pairs[2 * k + 1] = lr[k];
-  }
-  IBF_TRY(low_blk.upload(pairs.data(), pairs.size()));
-  IBF_TRY(low_row.upload(lr.data(), lr.size()));
-  IBF_TRY(diag_blk.upload(db.data(), db.size()));
-  IBF_TRY(brow.upload(br.data(), br.size()));
-  return IBF_OK;
-}
-
-__global__ void k_mask_dirichlet(int64_t nb, const int* __restrict__ brow, const int* __restrict__ col,
-                                 const uint8_t* __restrict__ mask, const double* __restrict__ diag,
-                                 double* __restrict__ val) {
-  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
-    const int r = brow[b], c = col[b];
-    if (!(mask[r] || mask[c])) continue;
-    for (int k = 0; k < 9; ++k) val[9 * b + k] = (r == c) ? diag[9 * (int64_t)r + k] : 0.0;
-  }
-}
-}  // namespace ibf
-
 using namespace ibf;
 
 extern "C" int ibf_bsr_create(int64_t n, int64_t nnz, const int64_t* rows, const int64_t* cols,
                               const double* blocks, ibf_bsr** out) {
-  if (n < 0 || nnz < 0 || !out) {
+  if (n < 0 || nnz < 0 || !out || n >= (1LL << 30)) {
     set_error("ibf_bsr_create: bad arguments");
     return IBF_ERR_BAD_ARG;
   }
@@ -525,25 +777,28 @@ extern "C" int ibf_bsr_create(int64_t n, int64_t nnz, const int64_t* rows, const
   std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
     return rows[a] * n + cols[a] < rows[b] * n + cols[b];
   });
-  ibf_bsr* m = new ibf_bsr();
-  m->n = n;
+  std::vector<int64_t> R, Cc;
   std::vector<double> vals;
   for (int64_t k = 0; k < nnz; ++k) {
     const int64_t s = order[k];
     const int64_t key = rows[s] * n + cols[s];
-    if (k == 0 || key != m->rows.back() * n + m->cols.back()) {
-      m->rows.push_back(rows[s]);
-      m->cols.push_back(cols[s]);
+    if (k == 0 || key != R.back() * n + Cc.back()) {
+      R.push_back(rows[s]);
+      Cc.push_back(cols[s]);
       vals.insert(vals.end(), blocks + 9 * s, blocks + 9 * s + 9);
     } else {
       double* dst = vals.data() + vals.size() - 9;
       for (int e = 0; e < 9; ++e) dst[e] += blocks[9 * s + e];
     }
   }
-  int st = build_upper_structure(n, m->rows, m->cols, m->row_ptr, m->col, m->low_ptr, m->low_blk, m->low_row,
-                                 m->diag_blk, m->brow);
-  if (st == IBF_OK) st = m->val.upload(vals.data(), vals.size());
-  if (st == IBF_OK) st = m->pinv.reserve(9 * (size_t)std::max<int64_t>(n, 1));
+  ibf_bsr* m = new ibf_bsr();
+  int st = m->pat.build(n, R, Cc);
+  std::vector<double> sv;
+  if (st == IBF_OK) {
+    to_sell(m->pat, vals.data(), sv);
+    st = m->pat.val.upload(sv.data(), sv.size());
+  }
+  if (st == IBF_OK) st = m->pinv.reserve(PINV_STRIDE * (size_t)std::max<int64_t>(n, 1));
   if (st == IBF_OK) {
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
@@ -569,11 +824,12 @@ extern "C" int ibf_bsr_mask_dirichlet(ibf_bsr* m, const uint8_t* vertex_mask, co
   cudaStream_t s = (cudaStream_t)st;
   DevBuf<uint8_t> dm;
   DevBuf<double> dd;
-  IBF_TRY(dm.upload(vertex_mask, (size_t)m->n, s));
-  IBF_TRY(dd.upload(diag, 9 * (size_t)m->n, s));
-  const int64_t nb = (int64_t)m->rows.size();
-  if (nb) {
-    k_mask_dirichlet<<<(int)div_up(nb, 256), 256, 0, s>>>(nb, m->brow.p, m->col.p, dm.p, dd.p, m->val.p);
+  IBF_TRY(dm.upload(vertex_mask, (size_t)m->pat.n, s));
+  IBF_TRY(dd.upload(diag, 9 * (size_t)m->pat.n, s));
+  const int64_t nq = m->pat.nq;
+  if (nq) {
+    k_mask_dirichlet<<<(int)div_up(nq, 256), 256, 0, s>>>(nq, m->pat.qrow.p, m->pat.col.p, m->pat.qreal.p, dm.p,
+                                                           dd.p, m->pat.val.p);
     IBF_LAUNCH_CHECK();
   }
   IBF_CUDA(cudaStreamSynchronize(s));
@@ -583,19 +839,13 @@ extern "C" int ibf_bsr_mask_dirichlet(ibf_bsr* m, const uint8_t* vertex_mask, co
 extern "C" int ibf_bsr_pcg(ibf_bsr* m, const double* rhs, double* x_out, double rel_tol, int64_t max_iters,
                            double* info_host, ibf_stream st) {
   cudaStream_t s = (cudaStream_t)st;
-  IBF_TRY(invert_diag_blocks((int)m->n, m->val.p, m->diag_blk.p, m->pinv.p, s));
+  IBF_TRY(invert_diag_blocks((int)m->pat.n, m->pat.val.p, m->pat.diag_q.p, m->pinv.p, s));
   IBF_TRY(pcg_solve(m->op(), rhs, x_out, rel_tol, max_iters, m->work, s));
   return pcg_info(m->work, info_host, s);
 }
 
-extern "C" int64_t ibf_bsr_size(const ibf_bsr* m) { return m ? (int64_t)m->rows.size() : 0; }
+extern "C" int64_t ibf_bsr_size(const ibf_bsr* m) { return m ? m->pat.nb : 0; }
 
 extern "C" int ibf_bsr_export(const ibf_bsr* m, int64_t* rows, int64_t* cols, double* blocks, ibf_stream st) {
-  cudaStream_t s = (cudaStream_t)st;
-  const int64_t nb = (int64_t)m->rows.size();
-  std::copy(m->rows.begin(), m->rows.end(), rows);
-  std::copy(m->cols.begin(), m->cols.end(), cols);
-  if (nb) IBF_CUDA(cudaMemcpyAsync(blocks, m->val.p, 9 * nb * sizeof(double), cudaMemcpyDeviceToHost, s));
-  IBF_CUDA(cudaStreamSynchronize(s));
-  return IBF_OK;
+  return sell_export(m->pat, rows, cols, blocks, (cudaStream_t)st);
 }

@@ -196,46 +196,32 @@ __global__ void __launch_bounds__(ELEM_THREADS) k_elem(ElemArgs a) {
   }
 }
 
-// per BSR block: mass (diagonal) + contributions in tet order, DBC mask
-__global__ void k_gather_blocks(int64_t nb, const int* __restrict__ brow, const int* __restrict__ col,
-                                const int* __restrict__ blk_ptr, const int* __restrict__ blk_src,
-                                const double* __restrict__ elem_blk, const double* __restrict__ masses,
-                                const uint8_t* __restrict__ mask, double* __restrict__ val) {
-  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
-    const int r = brow[b], c = col[b];
+// per storage block: mass (real diagonal) + contributions in tet order, DBC
+// mask; consecutive threads write consecutive lanes of one slot (coalesced)
+__global__ void k_gather_blocks(int64_t nq, const int* __restrict__ qrow, const int* __restrict__ col,
+                                const uint8_t* __restrict__ qreal, const int* __restrict__ blk_ptr,
+                                const int* __restrict__ blk_src, const double* __restrict__ elem_blk,
+                                const double* __restrict__ masses, const uint8_t* __restrict__ mask,
+                                double* __restrict__ val) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nq; q += (int64_t)gridDim.x * blockDim.x) {
+    const int r = qrow[q], c = col[q];
     double acc[9];
-    const double m0 = (r == c) ? masses[r] : 0.0;
+    const double m0 = (r == c && qreal[q]) ? masses[r] : 0.0;
 #pragma unroll
     for (int k = 0; k < 9; ++k) acc[k] = (k == 0 || k == 4 || k == 8) ? m0 : 0.0;
     if (!(mask && (mask[r] || mask[c]))) {
-      const int e0 = blk_ptr[b], e1 = blk_ptr[b + 1];
+      const int e0 = blk_ptr[q], e1 = blk_ptr[q + 1];
       for (int e = e0; e < e1; ++e) {
         const int src = blk_src[e];
-        const int t = src / 10, q = src - 10 * (src / 10);
-        const double* K = elem_blk + blk_tile_index(t, q);
+        const int t = src / 10, qq = src - 10 * (src / 10);
+        const double* K = elem_blk + blk_tile_index(t, qq);
 #pragma unroll
         for (int k = 0; k < 9; ++k) acc[k] += K[k];
       }
     }
 #pragma unroll
-    for (int k = 0; k < 9; ++k) val[9 * b + k] = acc[k];
+    for (int k = 0; k < 9; ++k) val[qel((int)q, k)] = acc[k];
   }
-}
-
-__device__ __forceinline__ void inv3x3(const double* A, double* O) {
-  const double c00 = A[4] * A[8] - A[5] * A[7];
-  const double c01 = A[5] * A[6] - A[3] * A[8];
-  const double c02 = A[3] * A[7] - A[4] * A[6];
-  const double id = 1.0 / (A[0] * c00 + A[1] * c01 + A[2] * c02);
-  O[0] = c00 * id;
-  O[1] = (A[2] * A[7] - A[1] * A[8]) * id;
-  O[2] = (A[1] * A[5] - A[2] * A[4]) * id;
-  O[3] = c01 * id;
-  O[4] = (A[0] * A[8] - A[2] * A[6]) * id;
-  O[5] = (A[2] * A[3] - A[0] * A[5]) * id;
-  O[6] = c02 * id;
-  O[7] = (A[1] * A[6] - A[0] * A[7]) * id;
-  O[8] = (A[0] * A[4] - A[1] * A[3]) * id;
 }
 
 struct RowArgs {
@@ -247,7 +233,7 @@ struct RowArgs {
   const int* vt_ptr;
   const int* vt_src;
   const double* elem_grad;
-  const int* diag_blk;
+  const int* diag_q;
   const double* val;
   ContactView cv;
   const double* coef_g;  // contact gradient coefficients (C)
@@ -275,9 +261,9 @@ __global__ void k_vertex_rows(RowArgs a) {
     for (int c = 0; c < 3; ++c) g[c] += s[c];
     const bool masked = a.mask && a.mask[i];
     double D[9];
-    const double* B = a.val + 9 * (size_t)a.diag_blk[i];
+    const int dq = a.diag_q[i];
 #pragma unroll
-    for (int k = 0; k < 9; ++k) D[k] = B[k];
+    for (int k = 0; k < 9; ++k) D[k] = a.val[qel(dq, k)];
     if (a.cv.n) {
       double sc[3] = {0.0, 0.0, 0.0};
       for (int e = a.cv.vc_ptr[i]; e < a.cv.vc_ptr[i + 1]; ++e) {
@@ -303,7 +289,7 @@ __global__ void k_vertex_rows(RowArgs a) {
 #pragma unroll
     for (int c = 0; c < 3; ++c) a.grad[3 * i + c] = g[c];
     if (g[0] != 0.0 || g[1] != 0.0 || g[2] != 0.0) atomicOr(a.flags + 1, 1);
-    inv3x3(D, a.pinv + 9 * i);
+    inv3_sym6(D, a.pinv + PINV_STRIDE * i);
   }
 }
 
@@ -564,13 +550,13 @@ __global__ void k_fill(double* p, double v, int n) {
   if (i < n) p[i] = v;
 }
 
-__global__ void k_diag_max(int64_t n, const int* __restrict__ diag_blk, const double* __restrict__ val,
+__global__ void k_diag_max(int64_t n, const int* __restrict__ diag_q, const double* __restrict__ val,
                            double* __restrict__ out) {
   __shared__ double red[8];
   double v = -INFINITY;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const double* B = val + 9 * (size_t)diag_blk[i];
-    v = fmax(v, fmax(B[0], fmax(B[4], B[8])));
+    const int q = diag_q[i];
+    v = fmax(v, fmax(val[qel(q, 0)], fmax(val[qel(q, 4)], val[qel(q, 8)])));
   }
   v = block_max(v, red);
   if (threadIdx.x == 0) {
@@ -593,8 +579,9 @@ int system_assemble(ibf_system* s, ibf_contacts* c, const double* x_hat, const d
     IBF_LAUNCH_CHECK();
   }
   const uint8_t* mask = (apply_dbc && s->any_dbc) ? s->dbc.p : nullptr;
-  k_gather_blocks<<<(int)std::min<int64_t>(div_up(s->nb, 256), 148LL * 32), 256, 0, st>>>(
-      s->nb, s->brow.p, s->col.p, s->blk_ptr.p, s->blk_src.p, s->elem_blk.p, s->masses.p, mask, s->val.p);
+  k_gather_blocks<<<(int)std::min<int64_t>(div_up(s->pat.nq, 256), 148LL * 32), 256, 0, st>>>(
+      s->pat.nq, s->pat.qrow.p, s->pat.col.p, s->pat.qreal.p, s->blk_ptr.p, s->blk_src.p, s->elem_blk.p,
+      s->masses.p, mask, s->pat.val.p);
   IBF_LAUNCH_CHECK();
   ContactView cv;
   const double* coef_g = nullptr;
@@ -607,7 +594,7 @@ int system_assemble(ibf_system* s, ibf_contacts* c, const double* x_hat, const d
     coef_g = c->coef_g.p;
   }
   RowArgs r{s->n, x_hat, x_tilde, s->masses.p, mask, s->vt_ptr.p, s->vt_src.p, s->elem_grad.p,
-            s->diag_blk.p, s->val.p, cv, coef_g, grad, s->pinv.p, s->flags.p};
+            s->pat.diag_q.p, s->pat.val.p, cv, coef_g, grad, s->pinv.p, s->flags.p};
   if (s->n) {
     k_vertex_rows<<<(int)std::min<int64_t>(div_up(s->n, 256), 148LL * 32), 256, 0, st>>>(r);
     IBF_LAUNCH_CHECK();
@@ -674,20 +661,10 @@ int system_inversion_cap_launch(ibf_system* s, const double* x, const double* p,
   return IBF_OK;
 }
 
-int build_upper_structure(int64_t n, const std::vector<int64_t>& rows, const std::vector<int64_t>& cols,
-                          DevBuf<int>& row_ptr, DevBuf<int>& col, DevBuf<int>& low_ptr, DevBuf<int>& low_blk,
-                          DevBuf<int>& low_row, DevBuf<int>& diag_blk, DevBuf<int>& brow);
-
 }  // namespace ibf
 
 ibf::Operator ibf_system::op() const {
-  ibf::Operator o;
-  o.n = (int)n;
-  o.row_ptr = row_ptr.p;
-  o.col = col.p;
-  o.val = val.p;
-  o.low_ptr = low_ptr.p;
-  o.low_pair = reinterpret_cast<const int2*>(low_blk.p);
+  ibf::Operator o = pat.op();
   o.pinv = pinv.p;
   o.mask = assembled_dbc ? dbc.p : nullptr;
   if (assembled_contacts) o.contact = ibf::contact_view(assembled_contacts);
@@ -763,13 +740,14 @@ extern "C" int ibf_system_create(int64_t n_verts, const double* masses, const ui
       esrc[k] = (int)(t * 10 + q);
     }
   std::vector<int> blk_ptr, blk_src;
+  std::vector<int64_t> rows_h, cols_h;
   blk_src.reserve(rcount[n]);
-  s->rows_h.reserve(rcount[n] / 3 + n);
-  s->cols_h.reserve(rcount[n] / 3 + n);
+  rows_h.reserve(rcount[n] / 3 + n);
+  cols_h.reserve(rcount[n] / 3 + n);
   std::vector<int> idx;
   auto open_block = [&](int r, int c) {
-    s->rows_h.push_back(r);
-    s->cols_h.push_back(c);
+    rows_h.push_back(r);
+    cols_h.push_back(c);
     blk_ptr.push_back((int)blk_src.size());
   };
   for (int i = 0; i < n; ++i) {
@@ -786,7 +764,6 @@ extern "C" int ibf_system_create(int64_t n_verts, const double* masses, const ui
     }
   }
   blk_ptr.push_back((int)blk_src.size());
-  s->nb = (int64_t)s->rows_h.size();
   // --- vertex <- tet incidences in tet order
   std::vector<int> vt_ptr(n + 1, 0), vt_src(4 * m);
   for (int64_t k = 0; k < 4 * m; ++k) vt_ptr[t32[k] + 1]++;
@@ -803,13 +780,26 @@ extern "C" int ibf_system_create(int64_t n_verts, const double* masses, const ui
       dbc[i] = dbc_mask[i] ? 1 : 0;
       s->any_dbc |= dbc[i] != 0;
     }
-  if (st == IBF_OK)
-    st = build_upper_structure(n, s->rows_h, s->cols_h, s->row_ptr, s->col, s->low_ptr, s->low_blk, s->low_row,
-                               s->diag_blk, s->brow);
-  s->nl = (int64_t)s->nb - n;
+  if (st == IBF_OK) st = s->pat.build(n, rows_h, cols_h);
+  // contribution lists re-indexed by storage block (padding blocks: none)
+  std::vector<int> qptr, qsrc;
+  if (st == IBF_OK) {
+    std::vector<int> cnt(s->pat.nq + 1, 0), first(s->pat.nq, -1);
+    for (int64_t b = 0; b < s->pat.nb; ++b) {
+      cnt[s->pat.q_of_b[b] + 1] = blk_ptr[b + 1] - blk_ptr[b];
+      first[s->pat.q_of_b[b]] = (int)b;
+    }
+    for (int64_t q = 0; q < s->pat.nq; ++q) cnt[q + 1] += cnt[q];
+    qptr = cnt;
+    qsrc.resize(std::max<size_t>(blk_src.size(), 1));
+    for (int64_t q = 0; q < s->pat.nq; ++q)
+      if (first[q] >= 0)
+        std::copy(blk_src.begin() + blk_ptr[first[q]], blk_src.begin() + blk_ptr[first[q] + 1],
+                  qsrc.begin() + qptr[q]);
+  }
   const size_t nt = (size_t)std::max<int64_t>(s->n_tiles, 1);
-  if (st == IBF_OK) st = s->blk_ptr.upload(blk_ptr.data(), blk_ptr.size());
-  if (st == IBF_OK) st = s->blk_src.upload(blk_src.data(), blk_src.size());
+  if (st == IBF_OK) st = s->blk_ptr.upload(qptr.data(), qptr.size());
+  if (st == IBF_OK) st = s->blk_src.upload(qsrc.data(), qsrc.size());
   if (st == IBF_OK) st = s->vt_ptr.upload(vt_ptr.data(), vt_ptr.size());
   if (st == IBF_OK) st = s->vt_src.upload(vt_src.data(), vt_src.size());
   if (st == IBF_OK) st = s->tets.upload(t32.data(), t32.size());
@@ -818,8 +808,7 @@ extern "C" int ibf_system_create(int64_t n_verts, const double* masses, const ui
   if (st == IBF_OK) st = s->masses.upload(masses, (size_t)n);
   if (st == IBF_OK) st = s->dbc.upload(dbc.data(), dbc.size());
   if (st == IBF_OK) st = s->regions.upload(s->regions_host.data(), s->regions_host.size());
-  if (st == IBF_OK) st = s->val.reserve(9 * (size_t)std::max<int64_t>(s->nb, 1));
-  if (st == IBF_OK) st = s->pinv.reserve(9 * (size_t)std::max(n, 1));
+  if (st == IBF_OK) st = s->pinv.reserve(PINV_STRIDE * (size_t)std::max(n, 1));
   if (st == IBF_OK) st = s->elem_grad.reserve(nt * 384);
   if (st == IBF_OK) st = s->elem_blk.reserve(nt * 2880);
   if (st == IBF_OK) st = s->flags.reserve(4);
@@ -846,8 +835,8 @@ extern "C" int ibf_system_create(int64_t n_verts, const double* masses, const ui
 extern "C" void ibf_system_destroy(ibf_system* s) { delete s; }
 
 extern "C" int ibf_system_pattern(const ibf_system* s, int64_t* n_blocks, int64_t* n_lower) {
-  *n_blocks = s->nb;
-  *n_lower = s->nl;
+  *n_blocks = s->pat.nb;
+  *n_lower = s->pat.nl;
   return IBF_OK;
 }
 
@@ -870,12 +859,7 @@ extern "C" int ibf_system_matvec(ibf_system* s, const double* x, double* y, ibf_
 }
 
 extern "C" int ibf_system_export_bsr(ibf_system* s, int64_t* rows, int64_t* cols, double* blocks, ibf_stream st) {
-  cudaStream_t stream = (cudaStream_t)st;
-  std::copy(s->rows_h.begin(), s->rows_h.end(), rows);
-  std::copy(s->cols_h.begin(), s->cols_h.end(), cols);
-  IBF_CUDA(cudaMemcpyAsync(blocks, s->val.p, 9 * sizeof(double) * s->nb, cudaMemcpyDeviceToHost, stream));
-  IBF_CUDA(cudaStreamSynchronize(stream));
-  return IBF_OK;
+  return sell_export(s->pat, rows, cols, blocks, (cudaStream_t)st);
 }
 
 extern "C" int ibf_system_pcg(ibf_system* s, const double* rhs, double* x_out, double rel_tol, int64_t max_iters,
@@ -915,8 +899,8 @@ extern "C" int ibf_stiffness_diagonal_max(ibf_system* s, const double* x, double
   }
   IBF_TRY(system_assemble(s, nullptr, x, x, 1.0, 1.0, h, false, s->vec_a.p, false, stream));
   k_fill<<<1, 1, 0, stream>>>(s->dscal.p + 8, 0.0, 1);
-  k_diag_max<<<(int)std::min<int64_t>(div_up(s->n, 256), 148 * 4), 256, 0, stream>>>(s->n, s->diag_blk.p,
-                                                                                       s->val.p, s->dscal.p + 8);
+  k_diag_max<<<(int)std::min<int64_t>(div_up(s->n, 256), 148 * 4), 256, 0, stream>>>(s->n, s->pat.diag_q.p,
+                                                                                       s->pat.val.p, s->dscal.p + 8);
   IBF_LAUNCH_CHECK();
   IBF_CUDA(cudaMemcpyAsync(s->host.p, s->flags.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, stream));
   IBF_CUDA(cudaMemcpyAsync(out_host, s->dscal.p + 8, sizeof(double), cudaMemcpyDeviceToHost, stream));

@@ -18,14 +18,13 @@ struct ibf_system {
   ibf::DevBuf<double> masses;            // (n)
   ibf::DevBuf<uint8_t> dbc;              // (n)
   bool any_dbc = false;
-  // static symmetric BSR pattern (diagonal + strict upper), rows ascending
-  int64_t nb = 0, nl = 0;
-  std::vector<int64_t> rows_h, cols_h;
-  ibf::DevBuf<int> row_ptr, col, brow, low_ptr, low_blk, low_row, diag_blk;
-  ibf::DevBuf<int> blk_ptr, blk_src;     // block <- (tet*10+q) contributions, tet order
+  // static symmetric BSR pattern (diagonal + strict upper) in sliced-ELL
+  // storage; pat.val holds the assembled matrix
+  ibf::SellPattern pat;
+  ibf::DevBuf<int> blk_ptr, blk_src;     // storage block <- (tet*10+q) contributions, tet order
   ibf::DevBuf<int> vt_ptr, vt_src;       // vertex <- (tet*4+l) incidences, tet order
   // assembled state
-  ibf::DevBuf<double> val, pinv;         // (nb,9), (n,9)
+  ibf::DevBuf<double> pinv;              // (n,9)
   ibf::DevBuf<double> elem_grad, elem_blk;  // tile-32 layouts
   ibf::DevBuf<int> flags;                // [0] nonfinite energy, [1] gradient nonzero
   ibf::DevBuf<double> dscal;             // device scalars
