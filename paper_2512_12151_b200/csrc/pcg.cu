@@ -67,14 +67,16 @@ struct PlainGather {
 };
 
 // ... or the new CG direction z + beta p_old formed on the fly (first:
-// p = z).  The owner of row j forms the same value with the same
-// instruction (fma), so every reader sees the bits the owner stores.
+// p = z).  Rounded exactly as numpy's `z + (rz_new / rz) * p`
+// (intact/sparse.py:148; no fused multiply-add), and every reader forms the
+// same bits the owner stores.
+__device__ __forceinline__ double cg_dir(double beta, double p, double z) { return __dadd_rn(z, __dmul_rn(beta, p)); }
+
 struct DirGather {
   const double* __restrict__ z;
   const double* __restrict__ pold;
   double beta;
   bool first;
-  __device__ __forceinline__ double dir(double zv, double pv) const { return first ? zv : __fma_rn(beta, pv, zv); }
   __device__ __forceinline__ void get(int j, double& x0, double& x1, double& x2) const {
     const double* Z = z + 3 * (size_t)j;
     if (first) {
@@ -85,9 +87,9 @@ struct DirGather {
       const double* P = pold + 3 * (size_t)j;
       const double z0 = Z[0], z1 = Z[1], z2 = Z[2];
       const double p0 = P[0], p1 = P[1], p2 = P[2];
-      x0 = __fma_rn(beta, p0, z0);
-      x1 = __fma_rn(beta, p1, z1);
-      x2 = __fma_rn(beta, p2, z2);
+      x0 = cg_dir(beta, p0, z0);
+      x1 = cg_dir(beta, p1, z1);
+      x2 = cg_dir(beta, p2, z2);
     }
   }
 };
@@ -383,9 +385,9 @@ __global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
           pv[0] = Z[0]; pv[1] = Z[1]; pv[2] = Z[2];
         } else {
           const double* P = gd.pold + 3 * (size_t)i;
-          pv[0] = __fma_rn(beta, P[0], Z[0]);
-          pv[1] = __fma_rn(beta, P[1], Z[1]);
-          pv[2] = __fma_rn(beta, P[2], Z[2]);
+          pv[0] = cg_dir(beta, P[0], Z[0]);
+          pv[1] = cg_dir(beta, P[1], Z[1]);
+          pv[2] = cg_dir(beta, P[2], Z[2]);
         }
         double* pki = pk + 3 * (size_t)i;
         pki[0] = pv[0]; pki[1] = pv[1]; pki[2] = pv[2];

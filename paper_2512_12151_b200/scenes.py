@@ -150,6 +150,25 @@ def _slab(size, corner, cells=(2, 2, 1), young=1e7):
             (0.0, 0.0, 0.0))
 
 
+def _pinned_slab(size, corner, cells, young, rho, edge):
+    """A Dirichlet-pinned slab whose per-vertex mass and stiffness match a
+    body of (young, rho) meshed at element size `edge`.
+
+    Pinned vertices never move, but the reference's penalty stiffness
+    mu = C_mu * max diag(M + h^2 K) is taken over ALL vertices, Dirichlet
+    ones included (intact/stepper.py:191-200, :265-268).  A coarse dense
+    stiff slab (decimetre cells, 1e3 kg/m^3, 1e7 Pa) would set mu ~1e4x above
+    the balls' own diagonal and drive the AL iteration into divergence;
+    scaling E by edge/cell and rho by (edge/cell)^3 gives the slab's
+    vertices the balls' diagonal scale, as for a press modelled as a moving
+    boundary (PAPER.md:596).
+    """
+    cell = max(float(np.max(np.asarray(size, dtype=float) / np.asarray(cells, dtype=float))), edge)
+    ratio = edge / cell
+    return (box_mesh(*cells, size=size, origin=corner), Material(MaterialModel.LIN, young * ratio, 0.3),
+            rho * ratio ** 3, (0.0, 0.0, 0.0))
+
+
 def c1_scene(nx=10, ny=10, nz=8, size=0.2, height=0.003, speed=1.0):
     """NH cube dropped onto a fixed LIN slab."""
     cube = box_mesh(nx, ny, nz, size=size, origin=(-size / 2, -size / 2, height))
@@ -176,11 +195,12 @@ def c4_scene(n=42, radius=0.1, gap=0.001, plate_speed=0.1, h=0.01, layers=None):
     centers = [(-c, -c, z0), (c, -c, z0), (-c, c, z0), (c, c, z0)]
     dz = np.sqrt((2 * radius + gap) ** 2 - 2 * c * c)
     centers.append((0.0, 0.0, z0 + dz + gap))
-    bodies = [_slab((1.0, 1.0, 0.05), (-0.5, -0.5, -0.05))]
+    edge = 2.0 * radius / n
+    bodies = [_pinned_slab((1.0, 1.0, 0.05), (-0.5, -0.5, -0.05), (4, 4, 1), mat.young, rho, edge)]
     for ctr in centers:
         bodies.append((transformed(ball, translate=ctr), mat, rho, (0.0, 0.0, 0.0)))
     top = centers[-1][2] + radius + gap
-    bodies.append(_slab((0.6, 0.6, 0.03), (-0.3, -0.3, top)))
+    bodies.append(_pinned_slab((0.6, 0.6, 0.03), (-0.3, -0.3, top), (4, 4, 1), mat.young, rho, edge))
     system, state, offs = merge(bodies, boundary_bodies=[0], scripted={len(bodies) - 1: (0.0, 0.0, -plate_speed)},
                                 h=h)
     params = StepParams(h=h, offset=1e-3, min_iterations=2)

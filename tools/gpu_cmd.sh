@@ -1,2 +1,1 @@
-python tools/bench_spmv.py > gpurun_out/spmv_new.json 2> gpurun_out/spmv_new.err
-timeout 600 python -m pytest tests -m gpu -q -x 2>&1 | tail -15 > gpurun_out/pytest_gpu3.log
+timeout 900 python -m pytest tests/test_gpu_solver.py -m gpu -q -x -k contact_heavy 2>&1 | grep -E "assert|Error|where|passed|failed" | head -20 > gpurun_out/pytest_ch.log
