@@ -309,15 +309,17 @@ static int reserve_soa(ibf_contacts* c, int64_t want, cudaStream_t s) {
   return IBF_OK;
 }
 
+// Stable compaction of one SoA field through the handle's scratch buffer
+// (compacted into scratch, copied back): no allocation per prune, and the
+// field keeps its capacity.
 template <typename T, int W>
 static int compact_field(ibf_contacts* c, DevBuf<T>& field, int64_t n, int64_t n_new, cudaStream_t s) {
-  DevBuf<T> tmp;
-  IBF_TRY(tmp.reserve(W * std::max<int64_t>(std::max<int64_t>(n_new, field.cap / W), 1)));
-  k_compact<T, W><<<grid_for(n), 256, 0, s>>>(n, c->flags.p, c->pos.p, field.p, tmp.p);
+  const size_t bytes = (size_t)W * std::max<int64_t>(n_new, 1) * sizeof(T);
+  IBF_TRY(c->compact_tmp.reserve(div_up((int64_t)W * n * sizeof(T), 8) + 1));
+  T* tmp = reinterpret_cast<T*>(c->compact_tmp.p);
+  k_compact<T, W><<<grid_for(n), 256, 0, s>>>(n, c->flags.p, c->pos.p, field.p, tmp);
   IBF_LAUNCH_CHECK();
-  std::swap(field.p, tmp.p);
-  std::swap(field.cap, tmp.cap);
-  IBF_CUDA(cudaStreamSynchronize(s));  // tmp (old storage) is freed at scope exit
+  if (n_new) IBF_CUDA(cudaMemcpyAsync(field.p, tmp, bytes, cudaMemcpyDeviceToDevice, s));
   return IBF_OK;
 }
 

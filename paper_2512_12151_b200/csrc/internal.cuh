@@ -145,6 +145,7 @@ struct ibf_contacts {
   ibf::DevBuf<double> tmp_tois;
   ibf::DevBuf<double> dscratch;
   ibf::DevBuf<int> iscratch;
+  ibf::DevBuf<double> compact_tmp;            // pruning scratch (8-byte words)
   ibf::HostScratch host;
 };
 

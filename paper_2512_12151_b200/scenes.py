@@ -95,7 +95,7 @@ def shell_sphere(n, radius=0.1, center=(0.0, 0.0, 0.0), layers=1) -> TetMesh:
     return build_tet_mesh(verts + np.asarray(center, dtype=np.float64), tets)
 
 
-def merge(bodies, boundary_bodies=(), scripted=None, h=0.01):
+def merge(bodies, boundary_bodies=(), scripted=None, h=0.01, scripted_stop=None):
     """Stack bodies [(mesh, material, density, velocity)] into a System.
 
     boundary_bodies: indices of bodies pinned entirely (fixed DBC);
@@ -127,7 +127,8 @@ def merge(bodies, boundary_bodies=(), scripted=None, h=0.01):
         boundary.append(BoundaryCondition(np.arange(offs[b], offs[b + 1])))
     for b, vel in scripted.items():
         ids = np.arange(offs[b], offs[b + 1])
-        traj = _ScriptedLine(x[ids].copy(), np.asarray(vel, dtype=np.float64), h)
+        traj = _ScriptedLine(x[ids].copy(), np.asarray(vel, dtype=np.float64), h,
+                             None if scripted_stop is None else scripted_stop.get(b))
         boundary.append(BoundaryCondition(ids, kind="scripted", trajectory=traj))
     system = System(np.concatenate(masses), regions, np.vstack(tris), np.vstack(edges), np.concatenate(verts),
                     boundary)
@@ -136,13 +137,17 @@ def merge(bodies, boundary_bodies=(), scripted=None, h=0.01):
 
 class _ScriptedLine:
     """Constant-velocity target at the end of step k (intact/scene.py:459-466);
-    h is bound by the scene builder."""
+    h is bound by the scene builder.  t_stop (seconds) optionally halts the
+    motion, e.g. a press that holds its minimum height."""
 
-    def __init__(self, start, velocity, h=0.01):
-        self.start, self.velocity, self.h = start, velocity, h
+    def __init__(self, start, velocity, h=0.01, t_stop=None):
+        self.start, self.velocity, self.h, self.t_stop = start, velocity, h, t_stop
 
     def __call__(self, step_index):
-        return self.start + (step_index + 1) * self.h * self.velocity
+        t = (step_index + 1) * self.h
+        if self.t_stop is not None:
+            t = min(t, self.t_stop)
+        return self.start + t * self.velocity
 
 
 def _slab(size, corner, cells=(2, 2, 1), young=1e7):
@@ -179,13 +184,15 @@ def c1_scene(nx=10, ny=10, nz=8, size=0.2, height=0.003, speed=1.0):
     return system, state, params
 
 
-def c4_scene(n=42, radius=0.1, gap=0.001, plate_speed=0.1, h=0.01, layers=None):
+def c4_scene(n=42, radius=0.1, gap=0.001, plate_speed=0.1, h=0.01, layers=None, plate_stop=None):
     """Five squishy-ball proxies compressed by a moving plate.
     layers=None builds solid balls; layers=k keeps the outer k cell layers.
 
     Four shells sit in a 2x2 square on a fixed slab, the fifth in the pocket
     above them; a scripted top plate starts one gap above the top shell and
-    moves down at plate_speed.
+    moves down at plate_speed; with plate_stop (metres) it halts once its
+    underside reaches that height and holds the compression (the press of
+    PAPER.md:596 shrinking the container to a minimum height).
     """
     ball = shell_sphere(n, radius, layers=(n + 1) // 2 if layers is None else layers)
     mat = Material(MaterialModel.COR, 1e4, 0.4)
@@ -201,8 +208,11 @@ def c4_scene(n=42, radius=0.1, gap=0.001, plate_speed=0.1, h=0.01, layers=None):
         bodies.append((transformed(ball, translate=ctr), mat, rho, (0.0, 0.0, 0.0)))
     top = centers[-1][2] + radius + gap
     bodies.append(_pinned_slab((0.6, 0.6, 0.03), (-0.3, -0.3, top), (4, 4, 1), mat.young, rho, edge))
+    stop = None
+    if plate_stop is not None:
+        stop = {len(bodies) - 1: max(0.0, (top - plate_stop) / plate_speed)}
     system, state, offs = merge(bodies, boundary_bodies=[0], scripted={len(bodies) - 1: (0.0, 0.0, -plate_speed)},
-                                h=h)
+                                h=h, scripted_stop=stop)
     params = StepParams(h=h, offset=1e-3, min_iterations=2)
     return system, state, params
 
