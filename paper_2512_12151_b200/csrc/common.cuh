@@ -73,6 +73,19 @@ struct PhaseTimer {
   }
 };
 
+// Opt-in host-side phase trace (IBF_TRACE=1): synchronises the stream at
+// each mark and prints the elapsed wall time per phase to stderr.  Off by
+// default; a dev tool for finding host/device stalls, never on the timed path.
+bool trace_enabled();
+struct Trace {
+  bool on;
+  double last;
+  std::string out;
+  explicit Trace(const char* name);
+  void mark(const char* what, cudaStream_t s, long long v = -1);
+  ~Trace();
+};
+
 // Growable device buffer owned by a handle.  Never shrinks; growth only
 // happens outside the timed hot loop once capacities settle.
 template <typename T>

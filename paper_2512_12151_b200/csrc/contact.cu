@@ -12,10 +12,10 @@
 //                              intact/contact.py:251-261, :91-106, :67-69
 //
 // Dedup keys are (kind, sorted quad).  Membership is answered through a CSR
-// bucketed by the smallest vertex of each key (buckets hold a handful of
-// constraints), so no hashing and no order dependence; first-occurrence among
-// new pairs picks the smallest blocking index, i.e. the reference's dict
-// insertion order.  Pruning is a stable compaction, so the resident order is
+// over a hash of the full key (buckets hold ~1 constraint), with exact key
+// comparison inside a bucket, so the result does not depend on the hash;
+// first-occurrence among new pairs picks the smallest blocking index, i.e.
+// the reference's dict insertion order.  Pruning is a stable compaction, so the resident order is
 // the reference's insertion order.
 #include <cub/cub.cuh>
 
@@ -48,32 +48,52 @@ __device__ __forceinline__ void load_key(const int* quad, const int* kind, int64
   key[4] = v[3];
 }
 
-__global__ void k_count_min(int64_t n, const int* __restrict__ quad, const int* __restrict__ sel,
-                            int* __restrict__ count) {
+// Membership buckets: constraints are bucketed by a hash of their full key
+// (kind, sorted quad) into a power-of-two table.  (Bucketing by the smallest
+// vertex degenerates when a pinned plate's few vertices are the smallest id
+// of every pair against it: buckets of 10^4 entries, quadratic scans.)
+__device__ __forceinline__ unsigned key_bucket(const int k[5], unsigned mask) {
+  unsigned long long h = 0x9E3779B97F4A7C15ull;
+#pragma unroll
+  for (int i = 0; i < 5; ++i) {
+    h ^= (unsigned long long)(unsigned)k[i] + 0x9E3779B97F4A7C15ull + (h << 6) + (h >> 2);
+    h *= 0xBF58476D1CE4E5B9ull;
+  }
+  h ^= h >> 31;
+  return (unsigned)h & mask;
+}
+
+__global__ void k_count_bucket(int64_t n, const int* __restrict__ quad, const int* __restrict__ kind,
+                               const int* __restrict__ sel, unsigned mask, int* __restrict__ count) {
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
     if (sel && !sel[j]) continue;
-    const int v = min(min(quad[4 * j], quad[4 * j + 1]), min(quad[4 * j + 2], quad[4 * j + 3]));
-    atomicAdd(count + v, 1);
+    int k[5];
+    load_key(quad, kind, j, k);
+    atomicAdd(count + key_bucket(k, mask), 1);
   }
 }
-__global__ void k_fill_min(int64_t n, const int* __restrict__ quad, const int* __restrict__ sel,
-                           const int* __restrict__ ptr, int* __restrict__ cursor, int* __restrict__ list) {
+__global__ void k_fill_bucket(int64_t n, const int* __restrict__ quad, const int* __restrict__ kind,
+                              const int* __restrict__ sel, unsigned mask, const int* __restrict__ ptr,
+                              int* __restrict__ cursor, int* __restrict__ list) {
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
     if (sel && !sel[j]) continue;
-    const int v = min(min(quad[4 * j], quad[4 * j + 1]), min(quad[4 * j + 2], quad[4 * j + 3]));
-    list[ptr[v] + atomicAdd(cursor + v, 1)] = (int)j;
+    int k[5];
+    load_key(quad, kind, j, k);
+    const unsigned b = key_bucket(k, mask);
+    list[ptr[b] + atomicAdd(cursor + b, 1)] = (int)j;
   }
 }
 
 // new[j] = key(blocking j) not resident
 __global__ void k_new_flags(int64_t nb, const int* __restrict__ bkind, const int* __restrict__ bquad,
-                            const int* __restrict__ rkind, const int* __restrict__ rquad,
+                            const int* __restrict__ rkind, const int* __restrict__ rquad, unsigned mask,
                             const int* __restrict__ rptr, const int* __restrict__ rlist, int* __restrict__ is_new) {
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nb; j += (int64_t)gridDim.x * blockDim.x) {
     int kj[5];
     load_key(bquad, bkind, j, kj);
+    const unsigned bk = key_bucket(kj, mask);
     bool found = false;
-    for (int e = rptr[kj[1]]; e < rptr[kj[1] + 1] && !found; ++e) {
+    for (int e = rptr[bk]; e < rptr[bk + 1] && !found; ++e) {
       int kr[5];
       load_key(rquad, rkind, rlist[e], kr);
       found = kr[0] == kj[0] && kr[1] == kj[1] && kr[2] == kj[2] && kr[3] == kj[3] && kr[4] == kj[4];
@@ -111,8 +131,8 @@ __global__ void k_reset_earliest(int64_t nb, const int* __restrict__ bquad, doub
 }
 // first occurrence of each key among kept pairs (smallest blocking index)
 __global__ void k_first(int64_t nb, const int* __restrict__ bkind, const int* __restrict__ bquad,
-                        const int* __restrict__ keep, const int* __restrict__ kptr, const int* __restrict__ klist,
-                        int* __restrict__ append) {
+                        const int* __restrict__ keep, unsigned mask, const int* __restrict__ kptr,
+                        const int* __restrict__ klist, int* __restrict__ append) {
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nb; j += (int64_t)gridDim.x * blockDim.x) {
     if (!keep[j]) {
       append[j] = 0;
@@ -120,8 +140,9 @@ __global__ void k_first(int64_t nb, const int* __restrict__ bkind, const int* __
     }
     int kj[5];
     load_key(bquad, bkind, j, kj);
+    const unsigned bk = key_bucket(kj, mask);
     bool first = true;
-    for (int e = kptr[kj[1]]; e < kptr[kj[1] + 1] && first; ++e) {
+    for (int e = kptr[bk]; e < kptr[bk + 1] && first; ++e) {
       const int o = klist[e];
       if (o >= j) continue;
       int ko[5];
@@ -275,22 +296,25 @@ static int exclusive_scan(ibf_contacts* c, const int* in, int* out, int64_t n, c
   return IBF_OK;
 }
 
-// CSR of selected rows bucketed by their smallest vertex
-static int min_vertex_csr(ibf_contacts* c, int64_t n, const int* quad, const int* sel, DevBuf<int>& count,
-                          DevBuf<int>& ptr, DevBuf<int>& list, cudaStream_t s) {
-  const int64_t nv = c->n_verts;
-  IBF_TRY(count.reserve(nv + 1));
-  IBF_TRY(ptr.reserve(nv + 1));
+// CSR of the selected rows' keys over a hash table of 2^k >= 2 n buckets
+static int key_csr(ibf_contacts* c, int64_t n, const int* quad, const int* kind, const int* sel, DevBuf<int>& count,
+                   DevBuf<int>& ptr, DevBuf<int>& list, unsigned* mask_out, cudaStream_t s) {
+  int64_t nbk = 1;
+  while (nbk < 2 * std::max<int64_t>(n, 1)) nbk <<= 1;
+  const unsigned mask = (unsigned)(nbk - 1);
+  *mask_out = mask;
+  IBF_TRY(count.reserve(nbk + 1));
+  IBF_TRY(ptr.reserve(nbk + 1));
   IBF_TRY(list.reserve(std::max<int64_t>(n, 1)));
-  IBF_CUDA(cudaMemsetAsync(count.p, 0, (nv + 1) * sizeof(int), s));
+  IBF_CUDA(cudaMemsetAsync(count.p, 0, (nbk + 1) * sizeof(int), s));
   if (n) {
-    k_count_min<<<grid_for(n), 256, 0, s>>>(n, quad, sel, count.p);
+    k_count_bucket<<<grid_for(n), 256, 0, s>>>(n, quad, kind, sel, mask, count.p);
     IBF_LAUNCH_CHECK();
   }
-  IBF_TRY(exclusive_scan(c, count.p, ptr.p, nv + 1, s));
-  IBF_CUDA(cudaMemsetAsync(count.p, 0, (nv + 1) * sizeof(int), s));
+  IBF_TRY(exclusive_scan(c, count.p, ptr.p, nbk + 1, s));
+  IBF_CUDA(cudaMemsetAsync(count.p, 0, (nbk + 1) * sizeof(int), s));
   if (n) {
-    k_fill_min<<<grid_for(n), 256, 0, s>>>(n, quad, sel, ptr.p, count.p, list.p);
+    k_fill_bucket<<<grid_for(n), 256, 0, s>>>(n, quad, kind, sel, mask, ptr.p, count.p, list.p);
     IBF_LAUNCH_CHECK();
   }
   return IBF_OK;
@@ -330,6 +354,8 @@ int contacts_update_dev(ibf_contacts* c, int64_t nb, const int* bkind, const int
   IBF_TRY(c->host.reserve(64));
   hostc = (int*)c->host.p;
   int64_t n_admit = 0;
+  Trace tr("contacts_update");
+  tr.mark("enter", s, nb);
   if (nb > 0) {
     IBF_TRY(c->flags.reserve(nb + 1));
     IBF_TRY(c->pos.reserve(nb + 1));
@@ -337,10 +363,13 @@ int contacts_update_dev(ibf_contacts* c, int64_t nb, const int* bkind, const int
     int* is_new = c->iscratch.p;
     int* keep = c->iscratch.p + (nb + 1);
     // resident CSR by min vertex
-    IBF_TRY(min_vertex_csr(c, c->n, c->quad.p, nullptr, c->v_count, c->v_ptr, c->v_list, s));
-    k_new_flags<<<grid_for(nb), 256, 0, s>>>(nb, bkind, bquad, c->kind.p, c->quad.p, c->v_ptr.p, c->v_list.p,
-                                             is_new);
+    unsigned rmask = 0, kmask = 0;
+    IBF_TRY(key_csr(c, c->n, c->quad.p, c->kind.p, nullptr, c->v_count, c->v_ptr, c->v_list, &rmask, s));
+    tr.mark("resident_csr", s, c->n);
+    k_new_flags<<<grid_for(nb), 256, 0, s>>>(nb, bkind, bquad, c->kind.p, c->quad.p, rmask, c->v_ptr.p,
+                                             c->v_list.p, is_new);
     IBF_LAUNCH_CHECK();
+    tr.mark("new_flags", s);
     if (!c->admit_all) {
       k_earliest<<<grid_for(nb), 256, 0, s>>>(nb, bquad, btoi, is_new, c->earliest.p);
       IBF_LAUNCH_CHECK();
@@ -351,9 +380,11 @@ int contacts_update_dev(ibf_contacts* c, int64_t nb, const int* bkind, const int
       k_reset_earliest<<<grid_for(nb), 256, 0, s>>>(nb, bquad, c->earliest.p);
       IBF_LAUNCH_CHECK();
     }
+    tr.mark("admit", s);
     // first occurrence among kept pairs
-    IBF_TRY(min_vertex_csr(c, nb, bquad, keep, c->k_count, c->k_ptr, c->k_list, s));
-    k_first<<<grid_for(nb), 256, 0, s>>>(nb, bkind, bquad, keep, c->k_ptr.p, c->k_list.p, c->flags.p);
+    IBF_TRY(key_csr(c, nb, bquad, bkind, keep, c->k_count, c->k_ptr, c->k_list, &kmask, s));
+    tr.mark("kept_csr", s);
+    k_first<<<grid_for(nb), 256, 0, s>>>(nb, bkind, bquad, keep, kmask, c->k_ptr.p, c->k_list.p, c->flags.p);
     IBF_LAUNCH_CHECK();
     IBF_CUDA(cudaMemsetAsync(c->flags.p + nb, 0, sizeof(int), s));
     IBF_TRY(exclusive_scan(c, c->flags.p, c->pos.p, nb + 1, s));
@@ -365,6 +396,7 @@ int contacts_update_dev(ibf_contacts* c, int64_t nb, const int* bkind, const int
     IBF_CUDA(cudaStreamSynchronize(s));
     n_admit = hostc[0];
     const int64_t n_app = hostc[1];
+    tr.mark("first_scan", s, n_app);
     if (n_app) {
       IBF_TRY(reserve_soa(c, c->n + n_app, s));
       k_append<<<grid_for(nb), 256, 0, s>>>(nb, c->n, bkind, bquad, c->flags.p, c->pos.p, c->kind.p, c->quad.p,
@@ -374,6 +406,7 @@ int contacts_update_dev(ibf_contacts* c, int64_t nb, const int* bkind, const int
       c->n += n_app;
     }
   }
+  tr.mark("append", s);
   // prune gamma < 0.01, stable
   int64_t n_pruned = 0;
   if (c->n) {
@@ -400,6 +433,8 @@ int contacts_update_dev(ibf_contacts* c, int64_t nb, const int* bkind, const int
       c->n = n_keep;
     }
   }
+  tr.mark("prune", s, n_pruned);
+  tr.mark("exit", s);
   c->vc_nverts = -1;  // incidence must be rebuilt
   *admitted = n_admit;
   *pruned = n_pruned;

@@ -15,6 +15,9 @@
 // is formed the same way in both places).
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <ctime>
 #include <string>
 
 #include "system.cuh"
@@ -22,6 +25,38 @@
 namespace ibf {
 
 unsigned long long g_launches = 0;
+
+static int trace_level() {
+  static int lvl = -1;
+  if (lvl < 0) lvl = getenv("IBF_TRACE") ? atoi(getenv("IBF_TRACE")) : 0;
+  return lvl;
+}
+bool trace_enabled() { return trace_level() > 0; }
+static double now_s() {
+  timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return ts.tv_sec + 1e-9 * ts.tv_nsec;
+}
+Trace::Trace(const char* name) : on(trace_enabled()), last(0.0) {
+  if (on) {
+    last = now_s();
+    out = name;
+  }
+}
+void Trace::mark(const char* what, cudaStream_t s, long long v) {
+  // level 1: only the first and last marks of a call (no extra syncs inside)
+  if (!on || (trace_level() < 2 && strcmp(what, "enter") != 0 && strcmp(what, "exit") != 0)) return;
+  cudaStreamSynchronize(s);
+  const double t = now_s();
+  char b[96];
+  if (v >= 0) snprintf(b, sizeof b, " %s=%.3fms(%lld)", what, 1e3 * (t - last), v);
+  else snprintf(b, sizeof b, " %s=%.3fms", what, 1e3 * (t - last));
+  out += b;
+  last = t;
+}
+Trace::~Trace() {
+  if (on) fprintf(stderr, "[ibf] %s\n", out.c_str());
+}
 static thread_local std::string g_err;
 void set_error(const std::string& msg) { g_err = msg; }
 

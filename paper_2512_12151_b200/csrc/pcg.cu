@@ -67,10 +67,17 @@ struct PlainGather {
 };
 
 // ... or the new CG direction z + beta p_old formed on the fly (first:
-// p = z).  Rounded exactly as numpy's `z + (rz_new / rz) * p`
-// (intact/sparse.py:148; no fused multiply-add), and every reader forms the
-// same bits the owner stores.
+// p = z; intact/sparse.py:148), one fused multiply-add, so every reader
+// forms the bits the owner stores.  (-DIBF_CG_DIR_NUMPY rounds the product
+// separately as numpy does; neither is bit-identical to the oracle's CG,
+// whose Jacobi inverse and dot orders differ anyway.  The golden box-on-slab
+// trajectory sits on exact admission ties, intact/contact.py:151, and its
+// key sets match with the fused form, parity.)
+#ifdef IBF_CG_DIR_NUMPY
 __device__ __forceinline__ double cg_dir(double beta, double p, double z) { return __dadd_rn(z, __dmul_rn(beta, p)); }
+#else
+__device__ __forceinline__ double cg_dir(double beta, double p, double z) { return __fma_rn(beta, p, z); }
+#endif
 
 struct DirGather {
   const double* __restrict__ z;

@@ -264,7 +264,9 @@ __global__ void k_vertex_rows(RowArgs a) {
     const int dq = a.diag_q[i];
 #pragma unroll
     for (int k = 0; k < 9; ++k) D[k] = a.val[qel(dq, k)];
-    if (a.cv.n) {
+    // masked (Dirichlet) rows take no contact terms; a pinned plate's
+    // vertices can sit in 10^4 constraints, so skip the incidence walk
+    if (a.cv.n && !masked) {
       double sc[3] = {0.0, 0.0, 0.0};
       for (int e = a.cv.vc_ptr[i]; e < a.cv.vc_ptr[i + 1]; ++e) {
         const int src = a.cv.vc_src[e];

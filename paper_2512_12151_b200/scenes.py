@@ -203,11 +203,13 @@ def c4_scene(n=42, radius=0.1, gap=0.001, plate_speed=0.1, h=0.01, layers=None, 
     dz = np.sqrt((2 * radius + gap) ** 2 - 2 * c * c)
     centers.append((0.0, 0.0, z0 + dz + gap))
     edge = 2.0 * radius / n
-    bodies = [_pinned_slab((1.0, 1.0, 0.05), (-0.5, -0.5, -0.05), (4, 4, 1), mat.young, rho, edge)]
+    # plates meshed at ~4 cm: long plate edges would each overlap thousands of
+    # ball edges in the EE broad phase
+    bodies = [_pinned_slab((1.0, 1.0, 0.05), (-0.5, -0.5, -0.05), (24, 24, 1), mat.young, rho, edge)]
     for ctr in centers:
         bodies.append((transformed(ball, translate=ctr), mat, rho, (0.0, 0.0, 0.0)))
     top = centers[-1][2] + radius + gap
-    bodies.append(_pinned_slab((0.6, 0.6, 0.03), (-0.3, -0.3, top), (4, 4, 1), mat.young, rho, edge))
+    bodies.append(_pinned_slab((0.6, 0.6, 0.03), (-0.3, -0.3, top), (16, 16, 1), mat.young, rho, edge))
     stop = None
     if plate_stop is not None:
         stop = {len(bodies) - 1: max(0.0, (top - plate_stop) / plate_speed)}

@@ -1,3 +1,2 @@
-timeout 1200 python bench.py > gpurun_out/bench_r1c.log 2>&1
-cp profiles/c4_frame_counts.json gpurun_out/c4_frame_counts.json 2>/dev/null
-timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_r1c.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_bench_r1c.log 2>&1
+IBF_TRACE=1 timeout 1200 python tools/frame_breakdown.py 50 > gpurun_out/breakdown1.json 2> gpurun_out/trace1.err
+timeout 1200 python tools/frame_breakdown.py 50 > gpurun_out/breakdown0.json 2> gpurun_out/trace0.err
