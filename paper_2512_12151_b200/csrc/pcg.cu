@@ -50,8 +50,17 @@ namespace ibf {
 #define IBF_SPMV_UNROLL 2
 #endif
 constexpr int PCG_THREADS = IBF_PCG_THREADS;
-// shared-memory budget per CTA for the rows' r and the (q, p) carried from A to B
-constexpr int PCG_SMEM_BYTES = 56 * 1024;
+// Shared-memory budget per CTA for carrying the rows' r and (q, p) from A to
+// B on chip.  Off by default: at C4 size the carry needs ~48 KB per CTA, and
+// the SMEM it takes comes out of the unified L1 that the SpMV gathers live
+// in — measured 2x slower per CG iteration (the carry pays off only when the
+// L1 working set is small).  An interleaved (z, p) record layout for the
+// gathers was also measured slower (94 vs 88 us per iteration: the two
+// half-record writes per iteration cost more than the fused gather saves).
+#ifndef IBF_PCG_SMEM_KB
+#define IBF_PCG_SMEM_KB 0
+#endif
+constexpr int PCG_SMEM_BYTES = IBF_PCG_SMEM_KB * 1024;
 
 // ---------------------------------------------------------------- gathers
 
@@ -536,30 +545,34 @@ struct PcgShape {
 };
 
 static PcgShape pcg_shape(int n) {
-  static int blocks_smem = -1, blocks_plain = -1;
-  if (blocks_smem < 0) {
-    cudaFuncSetAttribute(k_pcg, cudaFuncAttributeMaxDynamicSharedMemorySize, PCG_SMEM_BYTES);
+  static int max_b = -1;
+  if (max_b < 0) {
+    if (PCG_SMEM_BYTES > 0)
+      cudaFuncSetAttribute(k_pcg, cudaFuncAttributeMaxDynamicSharedMemorySize, PCG_SMEM_BYTES);
     int nb = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_pcg, PCG_THREADS, PCG_SMEM_BYTES);
-    blocks_smem = nb > 0 ? nb : 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_pcg, PCG_THREADS, 0);
-    blocks_plain = nb > 0 ? nb : 1;
+    max_b = nb > 0 ? nb : 1;
   }
   n = std::max(n, 1);
-  PcgShape sh;
-  for (int use_smem = 1; use_smem >= 0; --use_smem) {
-    const int64_t max_ctas = (int64_t)(use_smem ? blocks_smem : blocks_plain) * sm_count();
-    const int grid = (int)std::min<int64_t>(max_ctas, div_up(n, PCG_THREADS));
+  auto shape_for = [&](int b) {
+    const int grid = (int)std::min<int64_t>((int64_t)b * sm_count(), div_up(n, PCG_THREADS));
     const int rpt = (int)div_up(n, (int64_t)grid * PCG_THREADS);
     const int threads = (int)std::min<int64_t>(PCG_THREADS, 32 * div_up(div_up(n, (int64_t)grid * rpt), 32));
-    sh = PcgShape{grid, threads, rpt, 0};
-    if (!use_smem) break;
-    if (pcg_smem(rpt, threads) <= (size_t)PCG_SMEM_BYTES) {
-      sh.smem_rows = rpt;
-      break;
+    return PcgShape{grid, threads, rpt, 0};
+  };
+  // the on-chip carry when a full wave of CTAs with it stays co-resident
+  for (int b = max_b; b >= 1 && PCG_SMEM_BYTES > 0; --b) {
+    PcgShape sh = shape_for(b);
+    const size_t smem = pcg_smem(sh.rows_per_thread, sh.threads);
+    if (smem > (size_t)PCG_SMEM_BYTES) continue;
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_pcg, sh.threads, smem);
+    if ((int64_t)occ * sm_count() >= sh.grid) {
+      sh.smem_rows = sh.rows_per_thread;
+      return sh;
     }
   }
-  return sh;
+  return shape_for(max_b);
 }
 
 int pcg_solve(const Operator& op, const double* rhs, double* x_out, double rel_tol, int64_t max_iters,

@@ -1,2 +1,3 @@
-IBF_TRACE=1 timeout 1200 python tools/frame_breakdown.py 50 > gpurun_out/breakdown1.json 2> gpurun_out/trace1.err
-timeout 1200 python tools/frame_breakdown.py 50 > gpurun_out/breakdown0.json 2> gpurun_out/trace0.err
+python tools/bench_spmv.py > gpurun_out/spmv_new.json 2> gpurun_out/spmv_new.err
+timeout 1200 python bench.py > gpurun_out/bench_r1d.log 2>&1
+cp profiles/c4_frame_counts.json gpurun_out/c4_frame_counts.json
