@@ -549,6 +549,10 @@ static PcgShape pcg_shape(int n) {
   if (max_b < 0) {
     if (PCG_SMEM_BYTES > 0)
       cudaFuncSetAttribute(k_pcg, cudaFuncAttributeMaxDynamicSharedMemorySize, PCG_SMEM_BYTES);
+#ifdef IBF_PCG_CARVEOUT
+    // unified L1/SMEM split: the gathers want L1, the kernel needs ~1 KB SMEM per CTA
+    cudaFuncSetAttribute(k_pcg, cudaFuncAttributePreferredSharedMemoryCarveout, IBF_PCG_CARVEOUT);
+#endif
     int nb = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_pcg, PCG_THREADS, 0);
     max_b = nb > 0 ? nb : 1;
