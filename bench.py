@@ -347,6 +347,59 @@ def run_ours(args):
         torch.distributed.destroy_process_group()
 
 
+def run_c5(args):
+    """Scene-parallel C5 batch: `--scenes` randomized
+    drops sharded round-robin over the ranks, `--steps` frames each, no
+    collective on the data path (batch.py).  value = scene-frames per second
+    over the whole job (max-over-ranks wall of the timed region)."""
+    import torch
+    ws, rank, local = _dist()
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    else:
+        torch.cuda.set_device(0)
+    from paper_2512_12151_b200 import _lib
+    from paper_2512_12151_b200.batch import run_batch, run_scene
+    for k in range(max(args.warmup, 1)):          # warm the library and allocator
+        run_scene(10_000 + k, 1)
+    L = _lib.lib()
+    seeds = list(range(args.scenes))
+    launches0 = L.ibf_launch_count()
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    res = run_batch(seeds, args.steps)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    launches = L.ibf_launch_count() - launches0
+    if ws > 1:
+        t = torch.tensor([wall], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        wall = float(t[0])
+    if rank == 0:
+        records, _walls = res
+        frames = sum(r.frames for r in records)
+        value = frames / wall
+        line = {"metric": "C5 scene-frames/s (64 randomized NH drops, scene-parallel)", "value": value,
+                "unit": "scene-frames/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": 1e3 * wall / args.steps, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": f"C5: {args.scenes} C1-like drops (seeded jitter), {args.steps} frames each, "
+                                       "round-robin over ranks, no data-path collective",
+                           "parallelism": f"scene-parallel x{ws}"},
+                "newton_per_frame": sum(r.newton for r in records) / max(frames, 1),
+                "aborted": sum(r.aborted for r in records),
+                "e2e": {"value": value, "unit": "scene-frames/s", "h2d_bytes_per_step": None,
+                        "d2h_bytes_per_step": None, "note": "each scene runs through Simulation from host state"},
+                "gpu_launches": int(launches)}
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -358,9 +411,14 @@ def main():
                     help="untimed frames of the press before warm-up (reaches the contact-heavy regime)")
     ap.add_argument("--sample-n", type=int, default=16, help="ball resolution of the CPU baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", default="c4", choices=["c4", "c5"],
+                    help="c4: the headline press scene (default); c5: scene-parallel batch of drops")
+    ap.add_argument("--scenes", type=int, default=64, help="c5: number of scenes in the batch")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
+    elif args.workload == "c5":
+        run_c5(args)
     else:
         run_ours(args)
 

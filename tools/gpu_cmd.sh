@@ -1,3 +1,1 @@
-python tools/bench_spmv.py > gpurun_out/spmv_new.json 2> gpurun_out/spmv_new.err
-timeout 1200 python bench.py > gpurun_out/bench_r1d.log 2>&1
-cp profiles/c4_frame_counts.json gpurun_out/c4_frame_counts.json
+timeout 900 python bench.py --workload c5 --steps 5 --warmup 3 > gpurun_out/bench_c5.log 2>&1
