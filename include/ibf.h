@@ -89,6 +89,21 @@ int ibf_ccd_blocking(ibf_ccd* c, const int32_t** kinds, const int32_t** quads,
 /* Host copy of the last blocking set (BlockingPairs, intact/ccd.py:148-165). */
 int ibf_ccd_get_blocking(ibf_ccd* c, int64_t* kinds, int64_t* quads, double* tois, ibf_stream s);
 
+/* ----------------------------------------------------- penetration monitor */
+/* Static triangle-triangle intersection over the handle's surface triangles
+ * at x: replaces static_intersection_test (intact/intersect.py:125-140).
+ * n_hits = number of intersecting pairs (a < b, shared-vertex pairs
+ * excluded); the first min(cap, n_hits) pairs (ascending) go to pairs_host
+ * (cap,2) when it is not NULL. */
+int ibf_static_intersection(ibf_ccd* c, const double* x, int64_t* n_hits, int64_t* pairs_host, int64_t cap,
+                            ibf_stream s);
+/* Nearest non-adjacent VF/EE pair among those whose boxes come within
+ * `radius` at x: d_host = its distance (INFINITY without candidates),
+ * pair_host (5) = (kind, 4 vertex ids) or -1.  Pairs not tested are farther
+ * than radius apart, so d_host > 0 certifies that no surface primitives touch. */
+int ibf_min_distance(ibf_ccd* c, const double* x, double radius, double* d_host, int64_t* pair_host,
+                     ibf_stream s);
+
 /* ------------------------------------------------------------ active set */
 typedef struct ibf_contacts ibf_contacts;
 

@@ -76,6 +76,28 @@ class CCD:
                                                        _lib.host_ptr(t), _lib.stream()), "ibf_ccd_get_blocking")
         return BlockingPairs(k, q, t)
 
+    def static_intersections(self, x_dev, cap: int = 1 << 16):
+        """(n_hits, pairs (k,2)) of intersecting surface triangles at x
+        (intact/intersect.py:125-140); pairs truncated to `cap`."""
+        nh = C.c_int64()
+        out = np.empty((max(cap, 1), 2), dtype=np.int64)
+        _lib.check(_lib.lib().ibf_static_intersection(self.handle, _lib.dev_ptr(x_dev), C.byref(nh),
+                                                      _lib.host_ptr(out), int(cap), _lib.stream()),
+                   "ibf_static_intersection")
+        k = min(int(nh.value), cap)
+        return int(nh.value), out[:k]
+
+    def min_distance(self, x_dev, radius):
+        """(d, kind, quad) of the nearest non-adjacent VF/EE pair whose boxes
+        come within `radius`; (inf, -1, None) without candidates."""
+        d = C.c_double()
+        pr = np.full(5, -1, dtype=np.int64)
+        _lib.check(_lib.lib().ibf_min_distance(self.handle, _lib.dev_ptr(x_dev), float(radius), C.byref(d),
+                                               _lib.host_ptr(pr), _lib.stream()), "ibf_min_distance")
+        if pr[0] < 0:
+            return float(d.value), -1, None
+        return float(d.value), int(pr[0]), pr[1:].copy()
+
     def candidates(self, x0_dev, x1_dev, min_gap):
         nvf, nee = C.c_int64(), C.c_int64()
         _lib.check(_lib.lib().ibf_ccd_candidates(self.handle, _lib.dev_ptr(x0_dev), _lib.dev_ptr(x1_dev),

@@ -241,6 +241,16 @@ struct TraverseArgs {
 };
 
 __device__ __forceinline__ bool make_quad(const TraverseArgs& a, int qi, int pi, int q[4]) {
+  if (a.kind == 2) {  // triangle-triangle (static intersection test): a < b, no shared vertex
+    if (!(qi < pi)) return false;
+    const int* A = a.qprim + 3 * qi;
+    const int* B = a.tprim + 3 * pi;
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+      if (A[i] == B[0] || A[i] == B[1] || A[i] == B[2]) return false;
+    q[0] = qi; q[1] = pi; q[2] = q[3] = 0;
+    return true;
+  }
   if (a.kind == 0) {
     const int v = a.qprim[qi];
     const int t0 = a.tprim[3 * pi], t1 = a.tprim[3 * pi + 1], t2 = a.tprim[3 * pi + 2];
@@ -395,8 +405,8 @@ static int build_tree(ibf_ccd* c, int64_t n, cudaStream_t s, Tree& t) {
 // prefilter, sort.  Result pairs in c->pairs_sorted[0..count).
 static int broad_pass(ibf_ccd* c, int kind, const double* x0, const double* x1, double min_gap, bool filter,
                       int64_t* count, int64_t* n_candidates, cudaStream_t s) {
-  const int64_t nt = (kind == 0) ? c->nt : c->ne;
-  const int64_t nq = (kind == 0) ? c->nv : c->ne;
+  const int64_t nt = (kind == 1) ? c->ne : c->nt;
+  const int64_t nq = (kind == 0) ? c->nv : ((kind == 1) ? c->ne : c->nt);
   *count = 0;
   *n_candidates = 0;
   if (nt == 0 || nq == 0) return IBF_OK;
@@ -404,7 +414,13 @@ static int broad_pass(ibf_ccd* c, int kind, const double* x0, const double* x1, 
   IBF_TRY(c->box_hi.reserve(3 * nt));
   IBF_TRY(c->qlo.reserve(3 * nq));
   IBF_TRY(c->qhi.reserve(3 * nq));
-  if (kind == 0) {
+  if (kind == 2) {
+    // static triangle boxes (intact/intersect.py:129-131), queried against themselves
+    k_swept_boxes<3><<<grid_for(nt), 256, 0, s>>>(nt, c->tris.p, x0, x1, 0.0, c->box_lo.p, c->box_hi.p);
+    IBF_LAUNCH_CHECK();
+    IBF_CUDA(cudaMemcpyAsync(c->qlo.p, c->box_lo.p, 3 * nt * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    IBF_CUDA(cudaMemcpyAsync(c->qhi.p, c->box_hi.p, 3 * nt * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  } else if (kind == 0) {
     k_swept_boxes<3><<<grid_for(nt), 256, 0, s>>>(nt, c->tris.p, x0, x1, min_gap, c->box_lo.p, c->box_hi.p);
     IBF_LAUNCH_CHECK();
     k_swept_boxes<1><<<grid_for(nq), 256, 0, s>>>(nq, c->verts.p, x0, x1, 0.0, c->qlo.p, c->qhi.p);
@@ -428,8 +444,8 @@ static int broad_pass(ibf_ccd* c, int kind, const double* x0, const double* x1, 
     a.qlo = c->qlo.p;
     a.qhi = c->qhi.p;
     a.kind = kind;
-    a.qprim = (kind == 0) ? c->verts.p : c->edges.p;
-    a.tprim = (kind == 0) ? c->tris.p : c->edges.p;
+    a.qprim = (kind == 0) ? c->verts.p : ((kind == 1) ? c->edges.p : c->tris.p);
+    a.tprim = (kind == 1) ? c->edges.p : c->tris.p;
     a.x0 = x0;
     a.x1 = x1;
     a.min_gap = min_gap;
@@ -659,6 +675,251 @@ extern "C" int ibf_ccd_get_blocking(ibf_ccd* c, int64_t* kinds, int64_t* quads, 
   for (int64_t j = 0; j < n; ++j) {
     kinds[j] = k[j];
     for (int e = 0; e < 4; ++e) quads[4 * j + e] = q[4 * j + e];
+  }
+  return IBF_OK;
+}
+
+// ===================================================== penetration monitor
+// GPU restatement of the reference's validation oracle (intact/intersect.py,
+// SURVEY.md §8(f) f1) plus a nearest-pair monitor: certifies "penetration
+// free" at C4 scale, where the numpy test is a Python loop.
+
+namespace ibf {
+namespace mon {
+
+struct D3 {
+  double x, y, z;
+};
+__device__ __forceinline__ D3 ld(const double* p) { return {p[0], p[1], p[2]}; }
+__device__ __forceinline__ D3 sub(D3 a, D3 b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
+__device__ __forceinline__ double dot(D3 a, D3 b) { return (a.x * b.x + a.y * b.y) + a.z * b.z; }
+__device__ __forceinline__ D3 cross(D3 a, D3 b) {
+  return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
+}
+__device__ __forceinline__ double nrm(D3 a) { return sqrt(dot(a, a)); }
+
+// inclusive segment pq vs triangle abc; coplanar segments miss (intersect.py:21-46)
+__device__ bool segment_hits(D3 p, D3 q, D3 a, D3 b, D3 c) {
+  const double eps = 1e-12;
+  const D3 d = sub(q, p), e1 = sub(b, a), e2 = sub(c, a);
+  const D3 h = cross(d, e2);
+  const double det = dot(e1, h);
+  const double scale = nrm(d) * nrm(e1) * nrm(e2);
+  if (!(fabs(det) > eps * fmax(scale, 1e-300))) return false;
+  const double f = 1.0 / det;
+  const D3 s = sub(p, a);
+  const double u = f * dot(s, h);
+  const D3 qv = cross(s, e1);
+  const double v = f * dot(d, qv);
+  const double t = f * dot(e2, qv);
+  return u >= -eps && v >= -eps && u + v <= 1.0 + eps && t >= -eps && t <= 1.0 + eps;
+}
+
+// all of T2's vertices strictly on one side of T1's plane (intersect.py:95-101)
+__device__ bool one_side(const D3 T1[3], const D3 T2[3]) {
+  const D3 n = cross(sub(T1[1], T1[0]), sub(T1[2], T1[0]));
+  double amax = 0.0;
+  for (int k = 0; k < 3; ++k) amax = fmax(amax, fmax(fabs(T2[k].x), fmax(fabs(T2[k].y), fabs(T2[k].z))));
+  const double tol = 1e-12 * nrm(n) * (1.0 + amax);
+  bool pos = true, neg = true;
+  for (int k = 0; k < 3; ++k) {
+    const double d = dot(sub(T2[k], T1[0]), n);
+    pos = pos && d > tol;
+    neg = neg && d < -tol;
+  }
+  return pos || neg;
+}
+
+__device__ bool coplanar_overlap(const D3 A3[3], const D3 B3[3]) {
+  const D3 n = cross(sub(A3[1], A3[0]), sub(A3[2], A3[0]));
+  const double an[3] = {fabs(n.x), fabs(n.y), fabs(n.z)};
+  const int drop = (an[0] >= an[1] && an[0] >= an[2]) ? 0 : (an[1] >= an[2] ? 1 : 2);
+  double A[3][2], B[3][2];
+  for (int k = 0; k < 3; ++k) {
+    const double va[3] = {A3[k].x, A3[k].y, A3[k].z}, vb[3] = {B3[k].x, B3[k].y, B3[k].z};
+    int m = 0;
+    for (int c = 0; c < 3; ++c)
+      if (c != drop) {
+        A[k][m] = va[c];
+        B[k][m] = vb[c];
+        ++m;
+      }
+  }
+  auto crosses = [](const double* p, const double* q, const double* r, const double* s) {
+    const double d1x = q[0] - p[0], d1y = q[1] - p[1], d2x = s[0] - r[0], d2y = s[1] - r[1];
+    const double den = d1x * d2y - d1y * d2x;
+    if (fabs(den) < 1e-300) return false;
+    const double t = ((r[0] - p[0]) * d2y - (r[1] - p[1]) * d2x) / den;
+    const double u = ((r[0] - p[0]) * d1y - (r[1] - p[1]) * d1x) / den;
+    return -1e-12 <= t && t <= 1.0 + 1e-12 && -1e-12 <= u && u <= 1.0 + 1e-12;
+  };
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j)
+      if (crosses(A[i], A[(i + 1) % 3], B[j], B[(j + 1) % 3])) return true;
+  auto inside = [](const double* pt, double T[3][2]) {
+    double sign = 0.0;
+    for (int k = 0; k < 3; ++k) {
+      const double ex = T[(k + 1) % 3][0] - T[k][0], ey = T[(k + 1) % 3][1] - T[k][1];
+      const double wx = pt[0] - T[k][0], wy = pt[1] - T[k][1];
+      const double cr = ex * wy - ey * wx;
+      if (sign == 0.0) sign = cr;
+      else if (cr * sign < 0.0) return false;
+    }
+    return true;
+  };
+  return inside(A[0], B) || inside(B[0], A);
+}
+
+// intact/intersect.py:85-122 for one pair
+__device__ bool tri_tri(const D3 A[3], const D3 B[3]) {
+  if (one_side(A, B) || one_side(B, A)) return false;
+  for (int i = 0; i < 3; ++i) {
+    if (segment_hits(A[i], A[(i + 1) % 3], B[0], B[1], B[2])) return true;
+    if (segment_hits(B[i], B[(i + 1) % 3], A[0], A[1], A[2])) return true;
+  }
+  const D3 n = cross(sub(A[1], A[0]), sub(A[2], A[0]));
+  const double nn = nrm(n);
+  if (nn < 1e-300) return false;
+  double dmax = 0.0, span = 1.0;
+  for (int k = 0; k < 3; ++k) {
+    dmax = fmax(dmax, fabs(dot(sub(B[k], A[0]), n)) / nn);
+    span = fmax(span, fmax(fmax(fabs(A[k].x), fabs(A[k].y)), fabs(A[k].z)));
+    span = fmax(span, fmax(fmax(fabs(B[k].x), fabs(B[k].y)), fabs(B[k].z)));
+  }
+  return dmax < 1e-9 * span && coplanar_overlap(A, B);
+}
+
+}  // namespace mon
+
+__global__ void k_tri_tri(int64_t n, const unsigned long long* __restrict__ pairs, const int* __restrict__ tris,
+                          const double* __restrict__ x, int* __restrict__ hit) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int a = (int)(pairs[i] >> 32), b = (int)(pairs[i] & 0xffffffffull);
+    mon::D3 A[3], B[3];
+    for (int k = 0; k < 3; ++k) {
+      A[k] = mon::ld(x + 3 * (int64_t)tris[3 * a + k]);
+      B[k] = mon::ld(x + 3 * (int64_t)tris[3 * b + k]);
+    }
+    hit[i] = mon::tri_tri(A, B) ? 1 : 0;
+  }
+}
+
+__global__ void k_hit_write(int64_t n, const unsigned long long* __restrict__ pairs, const int* __restrict__ hit,
+                            const int* __restrict__ pos, int64_t cap, long long* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    if (!hit[i] || pos[i] >= cap) continue;
+    out[2 * (int64_t)pos[i]] = (long long)(pairs[i] >> 32);
+    out[2 * (int64_t)pos[i] + 1] = (long long)(pairs[i] & 0xffffffffull);
+  }
+}
+
+// distances of broad-phase pairs; min via ordered bits (distances >= 0)
+__global__ void k_pair_min_dist(int64_t n, int kind, const unsigned long long* __restrict__ pairs,
+                                const int* __restrict__ qprim, const int* __restrict__ tprim,
+                                const double* __restrict__ x, double* __restrict__ dist, double* __restrict__ dmin) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int qi = (int)(pairs[i] >> 32), pi = (int)(pairs[i] & 0xffffffffull);
+    int q[4];
+    if (kind == 0) {
+      q[0] = qprim[qi]; q[1] = tprim[3 * pi]; q[2] = tprim[3 * pi + 1]; q[3] = tprim[3 * pi + 2];
+    } else {
+      q[0] = qprim[2 * qi]; q[1] = qprim[2 * qi + 1]; q[2] = tprim[2 * pi]; q[3] = tprim[2 * pi + 1];
+    }
+    V3 P[4];
+    for (int k = 0; k < 4; ++k) P[k] = geo::ld3(x + 3 * (int64_t)q[k]);
+    const double d = geo::pair_dist(kind, P);
+    dist[i] = d;
+    if (d == d) atomic_min_nonneg(dmin, d);
+  }
+}
+
+__global__ void k_find_dist(int64_t n, const double* __restrict__ dist, const double* __restrict__ dmin,
+                            unsigned long long* __restrict__ first) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    if (dist[i] == *dmin) atomicMin(first, (unsigned long long)i);
+}
+
+}  // namespace ibf
+
+extern "C" int ibf_static_intersection(ibf_ccd* c, const double* x, int64_t* n_hits, int64_t* pairs_host,
+                                       int64_t cap, ibf_stream st) {
+  cudaStream_t s = (cudaStream_t)st;
+  int64_t cnt = 0, all = 0;
+  *n_hits = 0;
+  IBF_TRY(broad_pass(c, 2, x, x, 0.0, false, &cnt, &all, s));
+  if (!cnt) return IBF_OK;
+  IBF_TRY(c->b_flag.reserve(cnt + 1));
+  IBF_TRY(c->s_pos.reserve(cnt + 1));
+  k_tri_tri<<<grid_for(cnt), 256, 0, s>>>(cnt, c->pairs_sorted.p, c->tris.p, x, c->b_flag.p);
+  IBF_LAUNCH_CHECK();
+  IBF_CUDA(cudaMemsetAsync(c->b_flag.p + cnt, 0, sizeof(int), s));
+  size_t need = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, need, c->b_flag.p, c->s_pos.p, (int)(cnt + 1), s);
+  IBF_TRY(c->cub_tmp.reserve(need + 16));
+  size_t have = c->cub_tmp.cap;
+  IBF_CUDA(cub::DeviceScan::ExclusiveSum(c->cub_tmp.p, have, c->b_flag.p, c->s_pos.p, (int)(cnt + 1), s));
+  int* h = (int*)c->host.p;
+  IBF_CUDA(cudaMemcpyAsync(h, c->s_pos.p + cnt, sizeof(int), cudaMemcpyDeviceToHost, s));
+  IBF_CUDA(cudaStreamSynchronize(s));
+  *n_hits = h[0];
+  if (pairs_host && cap > 0 && h[0] > 0) {
+    const int64_t k = std::min<int64_t>(cap, h[0]);
+    DevBuf<long long> out;
+    IBF_TRY(out.reserve(2 * k));
+    k_hit_write<<<grid_for(cnt), 256, 0, s>>>(cnt, c->pairs_sorted.p, c->b_flag.p, c->s_pos.p, k, out.p);
+    IBF_LAUNCH_CHECK();
+    IBF_CUDA(cudaMemcpyAsync(pairs_host, out.p, 2 * k * sizeof(long long), cudaMemcpyDeviceToHost, s));
+    IBF_CUDA(cudaStreamSynchronize(s));
+  }
+  return IBF_OK;
+}
+
+extern "C" int ibf_min_distance(ibf_ccd* c, const double* x, double radius, double* d_host, int64_t* pair_host,
+                                ibf_stream st) {
+  cudaStream_t s = (cudaStream_t)st;
+  *d_host = INFINITY;
+  if (pair_host)
+    for (int k = 0; k < 5; ++k) pair_host[k] = -1;
+  IBF_TRY(c->dscratch.reserve(8));
+  IBF_TRY(c->counters.reserve(4));
+  for (int kind = 0; kind < 2; ++kind) {
+    int64_t cnt = 0, all = 0;
+    IBF_TRY(broad_pass(c, kind, x, x, radius, false, &cnt, &all, s));
+    if (!cnt) continue;
+    IBF_TRY(c->pair_toi.reserve(cnt));
+    k_set<<<1, 1, 0, s>>>(c->dscratch.p, INFINITY);
+    IBF_LAUNCH_CHECK();
+    const int* qprim = kind == 0 ? c->verts.p : c->edges.p;
+    const int* tprim = kind == 0 ? c->tris.p : c->edges.p;
+    k_pair_min_dist<<<grid_for(cnt), 256, 0, s>>>(cnt, kind, c->pairs_sorted.p, qprim, tprim, x, c->pair_toi.p,
+                                                   c->dscratch.p);
+    IBF_LAUNCH_CHECK();
+    IBF_CUDA(cudaMemsetAsync(c->counters.p + 2, 0xff, sizeof(unsigned long long), s));
+    k_find_dist<<<grid_for(cnt), 256, 0, s>>>(cnt, c->pair_toi.p, c->dscratch.p, c->counters.p + 2);
+    IBF_LAUNCH_CHECK();
+    double dm = INFINITY;
+    unsigned long long idx = ~0ull, pr = 0;
+    IBF_CUDA(cudaMemcpyAsync(&dm, c->dscratch.p, sizeof(double), cudaMemcpyDeviceToHost, s));
+    IBF_CUDA(cudaMemcpyAsync(&idx, c->counters.p + 2, sizeof(idx), cudaMemcpyDeviceToHost, s));
+    IBF_CUDA(cudaStreamSynchronize(s));
+    if (dm < *d_host && idx != ~0ull) {
+      *d_host = dm;
+      IBF_CUDA(cudaMemcpy(&pr, c->pairs_sorted.p + idx, sizeof(pr), cudaMemcpyDeviceToHost));
+      if (pair_host) {
+        const int qi = (int)(pr >> 32), pi = (int)(pr & 0xffffffffull);
+        std::vector<int> qv(3), pv(3);
+        if (kind == 0) {
+          IBF_CUDA(cudaMemcpy(qv.data(), c->verts.p + qi, sizeof(int), cudaMemcpyDeviceToHost));
+          IBF_CUDA(cudaMemcpy(pv.data(), c->tris.p + 3 * pi, 3 * sizeof(int), cudaMemcpyDeviceToHost));
+          pair_host[1] = qv[0]; pair_host[2] = pv[0]; pair_host[3] = pv[1]; pair_host[4] = pv[2];
+        } else {
+          IBF_CUDA(cudaMemcpy(qv.data(), c->edges.p + 2 * qi, 2 * sizeof(int), cudaMemcpyDeviceToHost));
+          IBF_CUDA(cudaMemcpy(pv.data(), c->edges.p + 2 * pi, 2 * sizeof(int), cudaMemcpyDeviceToHost));
+          pair_host[1] = qv[0]; pair_host[2] = qv[1]; pair_host[3] = pv[0]; pair_host[4] = pv[1];
+        }
+        pair_host[0] = kind;
+      }
+    }
   }
   return IBF_OK;
 }

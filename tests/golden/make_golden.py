@@ -2,7 +2,7 @@
 
 Run in the build container (the only place /root/reference exists):
 
-    python tests/golden/make_golden.py
+    python tests/golden/make_golden.py [generator ...]   # default: all
 
 Every output array below comes from calling `intact` functions from
 /root/reference/pkg/src on seeded inputs (seed 20240611, the reference's own
@@ -270,8 +270,40 @@ def gen_activeset(rng):
     save("activeset.npz", **out)
 
 
+def gen_intersect(rng):
+    """static_intersection_test (intact/intersect.py:125-140) on two-body
+    surfaces: interpenetrating, coplanar face contact, separated, jittered."""
+    from intact.intersect import static_intersection_test
+    from intact.primitives import box_mesh, sphere_mesh, transformed
+    out = {}
+    a = box_mesh(3, 3, 3, size=0.1)
+    cases = [transformed(box_mesh(3, 3, 3, size=0.1), translate=(0.04, 0.03, 0.06)),   # interpenetrating
+             transformed(box_mesh(2, 2, 2, size=0.1), translate=(0.0, 0.0, 0.1)),      # coplanar face contact
+             transformed(box_mesh(3, 3, 3, size=0.1), translate=(0.0, 0.0, 0.1001)),   # separated by 1e-4
+             transformed(sphere_mesh(3, radius=0.06), translate=(0.05, 0.05, 0.1))]    # sphere through a face
+    for c, b in enumerate(cases):
+        x = np.vstack([a.rest_positions, b.rest_positions])
+        if c == 3:
+            x = x + rng.uniform(-1e-4, 1e-4, x.shape)
+        tris = np.vstack([a.surface_tris, b.surface_tris + a.n_verts])
+        pairs = static_intersection_test(x, tris)
+        pairs = pairs[np.lexsort((pairs[:, 1], pairs[:, 0]))] if len(pairs) else pairs.reshape(0, 2)
+        out.update({f"x{c}": x, f"tris{c}": tris, f"pairs{c}": pairs.astype(np.int64)})
+    out["n"] = np.array(len(cases))
+    save("intersect.npz", **out)
+
+
+GENERATORS = ["distance", "accd", "broadphase", "elastic", "sparse", "activeset", "trajectory", "intersect"]
+
+
 def main():
+    only = sys.argv[1:] or GENERATORS
     _ref()
+    if only != GENERATORS:
+        for k, name in enumerate(GENERATORS):
+            if name in only:
+                globals()[f"gen_{name}"](np.random.default_rng(SEED + k))
+        return
     gen_distance(np.random.default_rng(SEED))
     gen_accd(np.random.default_rng(SEED + 1))
     gen_broadphase(np.random.default_rng(SEED + 2))
@@ -279,6 +311,7 @@ def main():
     gen_sparse(np.random.default_rng(SEED + 4))
     gen_activeset(np.random.default_rng(SEED + 5))
     gen_trajectory(np.random.default_rng(SEED + 6))
+    gen_intersect(np.random.default_rng(SEED + 7))
 
 
 if __name__ == "__main__":

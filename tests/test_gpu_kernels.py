@@ -250,3 +250,51 @@ def test_refresh_and_dual_sweep_match_oracle(ibf, rng):
     assert w_a == w_o
     st = a.export_state()
     assert np.array_equal(st[2], o.lam) and np.array_equal(st[3], o.gamma) and np.array_equal(st[4], o.s)
+
+
+def test_static_intersection_matches_reference(ibf):
+    """GPU tri-tri test vs the reference's static_intersection_test
+    (golden: interpenetrating, coplanar face contact, separated by 1e-4,
+    jittered sphere through a face) and vs the oracle on a larger random
+    two-body case."""
+    from oracle import intersect as ointersect
+    from paper_2512_12151_b200.intersect import static_intersection_test
+    from paper_2512_12151_b200 import scenes
+    g = golden("intersect.npz")
+    for c in range(int(g["n"])):
+        got = static_intersection_test(g[f"x{c}"], g[f"tris{c}"])
+        assert np.array_equal(got, g[f"pairs{c}"]), c
+    rng = np.random.default_rng(7)
+    a = scenes.box_mesh(8, 8, 6, size=0.2)
+    b = scenes.transformed(scenes.shell_sphere(10, 0.07, layers=2), translate=(0.1, 0.1, 0.17))
+    x = np.vstack([a.rest_positions, b.rest_positions]) + rng.uniform(-1e-4, 1e-4, (a.n_verts + b.n_verts, 3))
+    tris = np.vstack([a.surface_tris, b.surface_tris + a.n_verts])
+    want = ointersect.intersecting_pairs(x, tris)
+    assert len(want) > 0
+    assert np.array_equal(static_intersection_test(x, tris), want)
+
+
+def test_min_distance_monitor_matches_oracle(ibf):
+    """Nearest VF/EE pair within a radius: distance bit-identical to the
+    oracle (same pair_dist arithmetic), on separated boxes and on a random
+    drop scene."""
+    from oracle import intersect as ointersect
+    from paper_2512_12151_b200 import scenes
+    from paper_2512_12151_b200.ccd import CCD
+    from paper_2512_12151_b200.device import to_dev
+    g = golden("intersect.npz")
+    x, tris = g["x2"], g["tris2"]
+    edges = np.unique(np.sort(np.concatenate([tris[:, [0, 1]], tris[:, [1, 2]], tris[:, [2, 0]]]), axis=1), axis=0)
+    verts = np.unique(tris)
+    h = CCD(tris, edges, verts)
+    for radius in (1e-3, 5e-5):
+        d, kind, q = h.min_distance(to_dev(x), radius)
+        do, ko, qo = ointersect.min_distance(x, tris, edges, verts, radius)
+        assert d == do and kind == ko
+    system, state, _ = scenes.c5_scene(3, nx=5, ny=5, nz=4)
+    x = state.x + np.random.default_rng(2).uniform(-1e-3, 1e-3, state.x.shape)
+    h = CCD(system.surface_triangles, system.surface_edges, system.surface_vertices)
+    d, kind, q = h.min_distance(to_dev(x), 0.01)
+    do, ko, qo = ointersect.min_distance(x, system.surface_triangles, system.surface_edges, system.surface_vertices,
+                                         0.01)
+    assert d == do and kind == ko

@@ -156,3 +156,29 @@ def test_newton_lin_single_iteration():
     assert nit == 1
     gr, _ = newton.assemble(xh, x_tilde, masses, [reg], None, 1.0, 1e-3, 0.01)
     assert np.abs(gr).max() < 1e-9
+
+
+def test_intersection_pairs_match_reference():
+    """oracle/intersect.py vs the reference's static_intersection_test on
+    interpenetrating, coplanar-contact, separated and jittered two-body
+    surfaces (tests/golden/intersect.npz)."""
+    from oracle import intersect
+    g = golden("intersect.npz")
+    for c in range(int(g["n"])):
+        got = intersect.intersecting_pairs(g[f"x{c}"], g[f"tris{c}"])
+        assert np.array_equal(got, g[f"pairs{c}"]), c
+
+
+def test_min_distance_monitor_oracle():
+    """Separated boxes 1e-4 apart: the closest VF/EE pair is exactly the gap;
+    with a radius below the gap the inter-body pairs are not tested and the
+    result is an intra-body pair beyond the radius (any untested pair is
+    farther than the radius, so min(d, radius) bounds the true minimum)."""
+    from oracle import intersect
+    g = golden("intersect.npz")
+    x, tris = g["x2"], g["tris2"]
+    edges = np.unique(np.sort(np.concatenate([tris[:, [0, 1]], tris[:, [1, 2]], tris[:, [2, 0]]]), axis=1), axis=0)
+    verts = np.unique(tris)
+    d, kind, q = intersect.min_distance(x, tris, edges, verts, 1e-3)
+    assert d == pytest.approx(1e-4, rel=1e-6)
+    assert intersect.min_distance(x, tris, edges, verts, 5e-5)[0] > 5e-5

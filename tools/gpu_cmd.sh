@@ -1,1 +1,1 @@
-timeout 900 python bench.py --workload c5 --steps 5 --warmup 3 > gpurun_out/bench_c5.log 2>&1
+timeout 1200 python bench.py > gpurun_out/bench_r1e.log 2>&1
