@@ -40,7 +40,7 @@ def _region_blocks(reg, F, memo):
     return vertex_blocks(model, mu, lam, F, rows, vols)
 
 
-def energy(x_hat, x_tilde, masses, regions, batch, mu, offset, h):
+def energy(x_hat, x_tilde, masses, regions, batch, mu, offset, h, friction=None):
     """Incremental potential L(x_hat) (`incremental_energy`, :88-106)."""
     d = x_hat - x_tilde
     total = 0.5 * float(np.sum(masses * np.sum(d * d, axis=1)))
@@ -50,10 +50,12 @@ def energy(x_hat, x_tilde, masses, regions, batch, mu, offset, h):
     total += h * h * el
     if batch is not None and len(batch):
         total += batch.energy(batch.values(x_hat, offset), mu)
+    if friction is not None:
+        total += friction.energy(x_hat)
     return total
 
 
-def assemble(x_hat, x_tilde, masses, regions, batch, mu, offset, h, dbc=None, memo=None):
+def assemble(x_hat, x_tilde, masses, regions, batch, mu, offset, h, dbc=None, memo=None, friction=None):
     """(grad (n,3), SymBlockMatrix H) of the AL objective (`assemble`, :109-156)."""
     memo = {} if memo is None else memo
     n = len(x_hat)
@@ -72,6 +74,10 @@ def assemble(x_hat, x_tilde, masses, regions, batch, mu, offset, h, dbc=None, me
         cv = batch.values(x_hat, offset)
         _scatter(g, batch.quad, batch.grad_terms(cv, mu))
         r, c, b = upper_triplets(batch.quad, batch.hess_grids(mu))
+        R.append(r), C.append(c), B.append(b)
+    if friction is not None and len(friction):
+        _scatter(g, friction.indices, friction.grad_terms(x_hat))
+        r, c, b = upper_triplets(friction.indices, friction.hess_grids(x_hat))
         R.append(r), C.append(c), B.append(b)
     H = SymBlockMatrix(n, np.concatenate(R), np.concatenate(C), np.concatenate(B))
     if dbc is not None and dbc.any():
@@ -97,7 +103,7 @@ def backtrack(x_hat, p, fn, cap=1.0):
 
 
 def subproblem(x_tilde, x, x_hat0, masses, regions, aset, mu, offset, h,
-               cg_tol=1e-4, decay=0.9, dbc=None, memo=None):
+               cg_tol=1e-4, decay=0.9, dbc=None, memo=None, friction=None):
     """Newton loop + one dual sweep (`solve_subproblem`, :178-233).
 
     Returns (x_hat, newton_iters, cg_iters, stalled, worst_violation).
@@ -107,13 +113,13 @@ def subproblem(x_tilde, x, x_hat0, masses, regions, aset, mu, offset, h,
     batch = aset.snapshot()
 
     def fn(y):
-        return energy(y, x_tilde, masses, regions, batch, mu, offset, h)
+        return energy(y, x_tilde, masses, regions, batch, mu, offset, h, friction)
 
     x_hat = x_hat0.copy()
     newton = cg_total = 0
     stalled = False
     for _ in range(NEWTON_CAP):
-        g, H = assemble(x_hat, x_tilde, masses, regions, batch, mu, offset, h, dbc, memo)
+        g, H = assemble(x_hat, x_tilde, masses, regions, batch, mu, offset, h, dbc, memo, friction)
         if not np.any(g):
             break
         p, its, _, _ = pcg(H, -g, cg_tol)

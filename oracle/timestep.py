@@ -77,8 +77,11 @@ class Scene:
 
 def step(x_t, v_t, scene, aset, h, offset, epsilon=1e-3, k_min=1, decay=0.9,
          c_mu=0.1, cg_tol=1e-4, gravity=(0.0, 0.0, -9.81), step_index=0,
-         outer_cap=OUTER_CAP, record_iterates=False, trace=None):
-    """One step (`step`, :242-371), frictionless.
+         outer_cap=OUTER_CAP, record_iterates=False, trace=None, mu_f=0.0, eps_v=1e-3, friction=None,
+         friction_out=None):
+    """One step (`step`, :242-371).  `friction` holds the terms frozen at the
+    end of the previous step; with mu_f > 0 the new terms are appended to the
+    list `friction_out` (`friction_precompute`, :361-370).
 
     Returns (x, v, records, mu, offset) with one record per pass:
     (alpha, beta, n_constraints, newton_iters, cg_iters, wall_ms).
@@ -102,7 +105,7 @@ def step(x_t, v_t, scene, aset, h, offset, epsilon=1e-3, k_min=1, decay=0.9,
         t0 = time.perf_counter()
         x_hat, nit, cgit, _, _ = subproblem(
             x_tilde, x, x_hat, scene.masses, scene.regions, aset, mu, offset, h,
-            cg_tol=cg_tol, decay=decay, dbc=scene.dbc, memo=scene.memo)
+            cg_tol=cg_tol, decay=decay, dbc=scene.dbc, memo=scene.memo, friction=friction)
         if trace is not None:
             rec = {"resident": (aset.kind.copy(), aset.quad.copy(), aset.gamma.copy()),
                    "blocking": (kinds.copy(), quads.copy(), tois.copy())}
@@ -131,6 +134,9 @@ def step(x_t, v_t, scene, aset, h, offset, epsilon=1e-3, k_min=1, decay=0.9,
     if not done:
         raise Aborted(records)
     v = (x - x_t) / h
+    if friction_out is not None and mu_f > 0.0:
+        from .friction import precompute
+        friction_out.append(precompute(x, aset, mu, offset, h, mu_f, eps_v))
     if record_iterates:
         return x, v, records, mu, offset, iterates
     return x, v, records, mu, offset

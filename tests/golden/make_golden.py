@@ -293,7 +293,87 @@ def gen_intersect(rng):
     save("intersect.npz", **out)
 
 
-GENERATORS = ["distance", "accd", "broadphase", "elastic", "sparse", "activeset", "trajectory", "intersect"]
+def gen_friction(rng):
+    """intact/friction.py: mollifier and frames on grids; energy / gradient /
+    Hessian of random frozen terms; and a box sliding on a slab with
+    mu_f = 0.5 (per-step states, active sets and precomputed terms)."""
+    from intact.friction import FrictionTerms, f0, f0_over_y, f0_second, friction_precompute, tangent_basis
+    from intact.contact import ActiveSet
+    from intact.elasticity import Material, MaterialModel
+    from intact.mesh import SimState, compute_rest_data
+    from intact.primitives import box_mesh, transformed
+    from intact.solver import ElasticRegion
+    from intact.stepper import BoundaryCondition, Simulation, StepParams, System
+    out = {}
+    eps = 1e-4
+    y = np.concatenate([np.linspace(0.0, 3 * eps, 61), [1e-20, eps * (1 - 1e-12), eps * (1 + 1e-12)]])
+    out.update(y=y, eps=np.array(eps), f0=f0(y, eps), f0y=f0_over_y(y, eps), f0s=f0_second(y, eps))
+    nrm = rng.standard_normal((200, 3))
+    nrm[:5] = np.eye(3)[[0, 1, 2, 0, 2]] * np.array([[1], [-1], [1], [-2], [3]])
+    nrm /= np.linalg.norm(nrm, axis=1, keepdims=True)
+    out.update(normals=nrm, frames=tangent_basis(nrm))
+    k, n = 50, 40
+    idx = np.array([rng.choice(n, 4, replace=False) for _ in range(k)])
+    w = rng.uniform(-1, 1, (k, 4))
+    nn = rng.standard_normal((k, 3))
+    nn /= np.linalg.norm(nn, axis=1, keepdims=True)
+    terms = FrictionTerms(indices=idx, weights=w, frames=tangent_basis(nn), coeff=rng.uniform(0.1, 2, k),
+                          ref=rng.standard_normal((k, 3)) * 1e-3, eps=eps)
+    xr = rng.standard_normal((n, 3)) * 1e-3
+    xr[idx[:5]] = 0.0     # a few terms at exactly zero slip
+    terms.ref[:5] = 0.0
+    out.update(t_idx=idx, t_w=w, t_frames=terms.frames, t_coeff=terms.coeff, t_ref=terms.ref, t_x=xr,
+               t_energy=np.array(terms.energy(xr)), t_grad=terms.gradient_terms(xr), t_hess=terms.hessian_grids(xr))
+    # sliding box
+    slab = box_mesh(2, 2, 1, size=(0.4, 0.4, 0.05), origin=(-0.2, -0.2, -0.05))
+    cube = transformed(box_mesh(2, 2, 2, size=0.08), translate=(-0.04, -0.04, 0.0012))
+    masses, regions, tris, edges, verts, xs = [], [], [], [], [], []
+    off = 0
+    for mesh, mat in ((slab, Material(MaterialModel.LIN, 1e7, 0.3)), (cube, Material(MaterialModel.SNH, 1e5, 0.3))):
+        rest = compute_rest_data(mesh, 1000.0)
+        regions.append(ElasticRegion(mat, mesh.tets + off, rest.shape_rows, rest.volumes))
+        masses.append(rest.masses)
+        tris.append(mesh.surface_tris + off)
+        edges.append(mesh.surface_edges + off)
+        verts.append(mesh.surface_verts + off)
+        xs.append(mesh.rest_positions)
+        off += mesh.n_verts
+    n_slab = slab.n_verts
+    system = System(np.concatenate(masses), regions, np.vstack(tris), np.vstack(edges), np.concatenate(verts),
+                    [BoundaryCondition(np.arange(n_slab))])
+    x0 = np.vstack(xs)
+    v0 = np.zeros_like(x0)
+    v0[n_slab:] = [0.8, 0.3, -0.4]
+    params = StepParams(h=0.01, offset=1e-3, min_iterations=2, friction_coefficient=0.5, eps_v=1e-3)
+    sim = Simulation(system, params, SimState(x0.copy(), v0.copy()), ActiveSet())
+    out.update(s_xinit=x0, s_vinit=v0, s_masses=system.masses, s_tris=system.surface_triangles,
+               s_edges=system.surface_edges, s_verts=system.surface_vertices, s_n_slab=np.array(n_slab))
+    for i, reg in enumerate(regions):
+        out[f"s_reg{i}_tets"], out[f"s_reg{i}_rows"], out[f"s_reg{i}_vols"] = reg.tets, reg.shape_rows, reg.volumes
+    steps = 5
+    for k_ in range(steps):
+        diag = sim.advance()
+        out[f"s_x{k_}"] = sim.state.x.copy()
+        out[f"s_newton{k_}"] = np.array([r.newton_iters for r in diag.iterations])
+        fr = diag.friction
+        out[f"s_nfr{k_}"] = np.array(0 if fr is None else len(fr))
+        if fr is not None:
+            out.update({f"s_fidx{k_}": fr.indices, f"s_fw{k_}": fr.weights, f"s_ffr{k_}": fr.frames,
+                        f"s_fc{k_}": fr.coeff, f"s_fref{k_}": fr.ref})
+        cons = list(sim.active_set)
+        out[f"s_akind{k_}"] = np.array([int(c.kind) for c in cons], dtype=np.int64)
+        out[f"s_aquad{k_}"] = np.array([c.indices for c in cons], dtype=np.int64).reshape(-1, 4)
+        out[f"s_alam{k_}"] = np.array([c.lam for c in cons])
+        out[f"s_mu{k_}"] = np.array(diag.mu)
+        # identical-input precompute from this step's state and multipliers
+        fr2 = friction_precompute(sim.state.x, sim.active_set, diag.mu, diag.offset, params.h, 0.5, 1e-3)
+        assert (fr2 is None and fr is None) or np.array_equal(fr2.coeff, fr.coeff)
+    out["s_steps"] = np.array(steps)
+    save("friction.npz", **out)
+
+
+GENERATORS = ["distance", "accd", "broadphase", "elastic", "sparse", "activeset", "trajectory", "intersect",
+              "friction"]
 
 
 def main():
@@ -312,6 +392,7 @@ def main():
     gen_activeset(np.random.default_rng(SEED + 5))
     gen_trajectory(np.random.default_rng(SEED + 6))
     gen_intersect(np.random.default_rng(SEED + 7))
+    gen_friction(np.random.default_rng(SEED + 8))
 
 
 if __name__ == "__main__":
