@@ -135,6 +135,25 @@ int ibf_contacts_import(ibf_contacts* c, int64_t n, const int64_t* kind, const i
                         const double* anchor_d, const double* anchor_grad,
                         const double* anchor_x, ibf_stream st);
 
+/* -------------------------------------------------------------- friction */
+typedef struct ibf_friction ibf_friction;
+
+/* FrictionTerms (intact/friction.py:56-100) as a device handle. */
+int ibf_friction_create(ibf_friction** out);
+void ibf_friction_destroy(ibf_friction* f);
+int64_t ibf_friction_size(const ibf_friction* f);
+/* friction_precompute (intact/friction.py:103-151) from an accepted state x
+ * (dev) and the active set's multipliers: one term per constraint with a
+ * positive normal force, active-set order; eps = h * eps_v. */
+int ibf_friction_precompute(ibf_friction* f, const ibf_contacts* c, const double* x, double mu, double offset,
+                            double h, double mu_f, double eps_v, int64_t* n_terms, ibf_stream s);
+/* Host import / export of the terms: quad (K,4), w (K,4), frames (K,3,2),
+ * coeff (K), ref (K,3), eps. */
+int ibf_friction_import(ibf_friction* f, int64_t n, const int64_t* quad, const double* w, const double* frames,
+                        const double* coeff, const double* ref, double eps, ibf_stream s);
+int ibf_friction_export(const ibf_friction* f, int64_t* quad, double* w, double* frames, double* coeff,
+                        double* ref, double* eps, ibf_stream s);
+
 /* --------------------------------------------------------- elastic system */
 typedef struct ibf_system ibf_system;
 
@@ -158,6 +177,10 @@ int ibf_system_pattern(const ibf_system* s, int64_t* n_blocks, int64_t* n_lower)
 int ibf_assemble(ibf_system* s, ibf_contacts* c, const double* x_hat, const double* x_tilde,
                  double mu, double offset, double h, int apply_dbc, double* grad,
                  ibf_stream st);
+/* Friction terms entering subsequent assemble / energy / solve calls on s
+ * (the `friction` argument of intact/solver.py:109-233); NULL removes them. */
+int ibf_system_set_friction(ibf_system* s, ibf_friction* f);
+
 /* y = H x with the last assembled matrix (BlockSparseMatrix.matvec,
  * intact/sparse.py:64-73, contact part applied matrix-free). */
 int ibf_system_matvec(ibf_system* s, const double* x, double* y, ibf_stream st);

@@ -38,6 +38,13 @@ _PROTOS = {
     "ibf_max_step_size": (_int, [_vp, _vp, _vp, _dbl, _dbl, _pdbl, _pi64, _vp]),
     "ibf_ccd_get_blocking": (_int, [_vp, _vp, _vp, _vp, _vp]),
     "ibf_static_intersection": (_int, [_vp, _vp, _pi64, _vp, _i64, _vp]),
+    "ibf_friction_create": (_int, [C.POINTER(_vp)]),
+    "ibf_friction_destroy": (None, [_vp]),
+    "ibf_friction_size": (_i64, [_vp]),
+    "ibf_friction_precompute": (_int, [_vp, _vp, _vp, _dbl, _dbl, _dbl, _dbl, _dbl, _pi64, _vp]),
+    "ibf_friction_import": (_int, [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _dbl, _vp]),
+    "ibf_friction_export": (_int, [_vp, _vp, _vp, _vp, _vp, _vp, _pdbl, _vp]),
+    "ibf_system_set_friction": (_int, [_vp, _vp]),
     "ibf_min_distance": (_int, [_vp, _vp, _dbl, _pdbl, _vp, _vp]),
     "ibf_contacts_create": (_int, [_i64, _int, C.POINTER(_vp)]),
     "ibf_contacts_destroy": (None, [_vp]),

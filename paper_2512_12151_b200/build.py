@@ -18,7 +18,7 @@ CSRC = os.path.join(HERE, "csrc")
 OUT = os.environ.get("IBF_BUILD_OUT", os.path.join(HERE, "libibf.so"))
 BUILD = os.environ.get("IBF_BUILD_DIR", os.path.join(CSRC, "build"))
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-SOURCES = ["pcg.cu", "system.cu", "contact.cu", "ccd.cu", "newton.cu"]
+SOURCES = ["pcg.cu", "system.cu", "contact.cu", "ccd.cu", "newton.cu", "friction.cu"]
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",

@@ -47,6 +47,19 @@ __host__ __device__ __forceinline__ size_t qel(int q, int e) {
   return 9 * (size_t)(q & ~31) + (size_t)(q & 31) + 32 * (size_t)e;
 }
 
+// Matrix-free friction term (intact/friction.py:85-100): per term k the
+// 12x12 clique w w^T (x) Hw_k, Hw_k = coeff T [g2 uu^T + g1 (I - uu^T)] T^T
+// (3x3, symmetric PSD), applied as t_k = Hw_k sum_j w_j p_j, y_i += w t_k.
+struct FrictionView {
+  int n = 0;                          // K terms
+  const int* quad = nullptr;          // (K,4)
+  const double* w = nullptr;          // (K,4) witness weights
+  const double* hw = nullptr;         // (K,9) world-space Hessian
+  const int* vf_ptr = nullptr;        // (N+1) vertex -> term incidences
+  const int* vf_src = nullptr;        // k*4 + slot, ordered by k
+  double* t = nullptr;                // (K,3) workspace
+};
+
 // Block-Jacobi inverse: the diagonal blocks are symmetric, so their inverse
 // is stored as its upper triangle (00, 01, 02, 11, 12, 22) — 48 instead of
 // 72 bytes per vertex streamed by every CG iteration.
@@ -83,6 +96,7 @@ struct Operator {
   const uint8_t* mask = nullptr;      // (n) DBC mask (contact masking) or null
   const double* pinv = nullptr;       // (n,6) inverse diagonal blocks (upper triangle)
   ContactView contact;
+  FrictionView friction;
 };
 
 // Host + device halves of the sliced symmetric pattern (built once).
@@ -146,6 +160,23 @@ struct ibf_contacts {
   ibf::DevBuf<double> dscratch;
   ibf::DevBuf<int> iscratch;
   ibf::DevBuf<double> compact_tmp;            // pruning scratch (8-byte words)
+  ibf::HostScratch host;
+};
+
+// Frozen friction terms (FrictionTerms, intact/friction.py:56-100).
+struct ibf_friction {
+  int64_t n = 0;
+  double eps = 0.0;                 // h * eps_v
+  ibf::DevBuf<int> quad;            // (K,4)
+  ibf::DevBuf<double> w, frames, coeff, ref;   // (K,4), (K,3,2), (K), (K,3)
+  ibf::DevBuf<double> gw, hw, tvec;            // per assembly: (K,3) force, (K,9) Hessian, SpMV workspace
+  ibf::DevBuf<int> vf_ptr, vf_src, v_count, keys, keys2, vals;
+  int64_t vf_nverts = -1;
+  // precompute scratch (per constraint)
+  ibf::DevBuf<int> flags, pos;
+  ibf::DevBuf<double> t_w, t_frames, t_coeff, t_ref;
+  ibf::DevBuf<int> t_quad;
+  ibf::DevBuf<unsigned char> cub_tmp;
   ibf::HostScratch host;
 };
 

@@ -130,6 +130,37 @@ __device__ __forceinline__ void contact_dot(const Operator& op, const Gather& gp
   cv.t[c] = cv.coef[c] * acc;
 }
 
+// friction term k: t_k = Hw_k sum_j w_j p_j over unmasked j
+template <class Gather>
+__device__ __forceinline__ void friction_dot(const Operator& op, const Gather& gp, int k) {
+  const FrictionView& fv = op.friction;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int v = fv.quad[4 * k + j];
+    if (op.mask && op.mask[v]) continue;
+    double x0, x1, x2;
+    gp.get(v, x0, x1, x2);
+    const double w = fv.w[4 * k + j];
+    a0 += w * x0;
+    a1 += w * x1;
+    a2 += w * x2;
+  }
+  const double* H = fv.hw + 9 * (size_t)k;
+  double* t = fv.t + 3 * (size_t)k;
+  t[0] = H[0] * a0 + H[1] * a1 + H[2] * a2;
+  t[1] = H[3] * a0 + H[4] * a1 + H[5] * a2;
+  t[2] = H[6] * a0 + H[7] * a1 + H[8] * a2;
+}
+
+// the matrix-free terms' per-term dots (contact and friction) over this CTA's share
+template <class Gather>
+__device__ __forceinline__ void term_dots(const Operator& op, const Gather& gp) {
+  const int S = gridDim.x * blockDim.x;
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < op.contact.n; c += S) contact_dot(op, gp, c);
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < op.friction.n; k += S) friction_dot(op, gp, k);
+}
+
 // one upper block: a_r += (b[3r] x0 + b[3r+1] x1) + b[3r+2] x2
 __device__ __forceinline__ void acc_upper(const double b[9], double x0, double x1, double x2, double& a0, double& a1,
                                           double& a2) {
@@ -235,15 +266,24 @@ __device__ __forceinline__ void row_product(const Operator& op, const Gather& gp
       a2 += t * g[2];
     }
   }
+  if (op.friction.n && !(op.mask && op.mask[i])) {
+    const FrictionView& fv = op.friction;
+    for (int e = fv.vf_ptr[i]; e < fv.vf_ptr[i + 1]; ++e) {
+      const int src = fv.vf_src[e];
+      const double w = fv.w[src];
+      const double* t = fv.t + 3 * (size_t)(src >> 2);
+      a0 += w * t[0];
+      a1 += w * t[1];
+      a2 += w * t[2];
+    }
+  }
   y[0] = a0;
   y[1] = a1;
   y[2] = a2;
 }
 
 __global__ void k_contact_dot(Operator op, const double* __restrict__ p) {
-  const PlainGather gp{p};
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < op.contact.n; c += gridDim.x * blockDim.x)
-    contact_dot(op, gp, c);
+  term_dots(op, PlainGather{p});
 }
 
 __global__ void __launch_bounds__(256, 2) k_spmv(Operator op, const double* __restrict__ p, double* __restrict__ y) {
@@ -259,8 +299,8 @@ __global__ void __launch_bounds__(256, 2) k_spmv(Operator op, const double* __re
 
 int spmv(const Operator& op, const double* x, double* y, cudaStream_t s) {
   if (op.n == 0) return IBF_OK;
-  if (op.contact.n) {
-    k_contact_dot<<<(int)div_up(op.contact.n, 256), 256, 0, s>>>(op, x);
+  if (op.contact.n || op.friction.n) {
+    k_contact_dot<<<(int)div_up(std::max(op.contact.n, op.friction.n), 256), 256, 0, s>>>(op, x);
     IBF_LAUNCH_CHECK();
   }
   // two CTAs per SM sweep the rows in ascending order: a small in-flight
@@ -387,8 +427,8 @@ __global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
       const DirGather gd{a.z, a.p[pb ^ 1], beta, first};
       double* pk = a.p[pb];
       // ---- A: contact dots on p_k, then q = H p_k, pAp
-      if (op.contact.n) {
-        for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < op.contact.n; c += S) contact_dot(op, gd, c);
+      if (op.contact.n || op.friction.n) {
+        term_dots(op, gd);
         grid.sync();
       }
       double acc = 0.0;
@@ -484,8 +524,8 @@ __global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
       if (it % 250 == 0) {
         // restart from the true residual r = b - H x
         const PlainGather gx{Xb(cur)};
-        if (op.contact.n) {
-          for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < op.contact.n; c += S) contact_dot(op, gx, c);
+        if (op.contact.n || op.friction.n) {
+          term_dots(op, gx);
           grid.sync();
         }
         acc_rz = 0.0;

@@ -237,6 +237,8 @@ struct RowArgs {
   const double* val;
   ContactView cv;
   const double* coef_g;  // contact gradient coefficients (C)
+  FrictionView fv;
+  const double* fr_gw;   // friction world forces (K,3)
   double* grad;
   double* pinv;
   int* flags;
@@ -287,6 +289,25 @@ __global__ void k_vertex_rows(RowArgs a) {
 #pragma unroll
       for (int c = 0; c < 3; ++c) g[c] += sc[c];
     }
+    if (a.fv.n && !masked) {
+      // friction: g += w_slot F_k; D += w_slot^2 Hw_k (intact/friction.py:79-100)
+      double sf[3] = {0.0, 0.0, 0.0};
+      for (int e = a.fv.vf_ptr[i]; e < a.fv.vf_ptr[i + 1]; ++e) {
+        const int src = a.fv.vf_src[e];
+        const int k = src >> 2;
+        const double wv = a.fv.w[src];
+        const double* F = a.fr_gw + 3 * (size_t)k;
+        const double* Hk = a.fv.hw + 9 * (size_t)k;
+        sf[0] += wv * F[0];
+        sf[1] += wv * F[1];
+        sf[2] += wv * F[2];
+        const double w2 = wv * wv;
+#pragma unroll
+        for (int q = 0; q < 9; ++q) D[q] += w2 * Hk[q];
+      }
+#pragma unroll
+      for (int c = 0; c < 3; ++c) g[c] += sf[c];
+    }
     if (masked) g[0] = g[1] = g[2] = 0.0;
 #pragma unroll
     for (int c = 0; c < 3; ++c) a.grad[3 * i + c] = g[c];
@@ -318,9 +339,21 @@ struct EnergyArgs {
   const double* clam;
   const double* cgam;
   double mu, offset;
-  int bv, bt, bc;
-  double* part;           // (bv+bt+bc) * MAXT
+  int bv, bt, bc, bf;
+  // friction terms (K)
+  int64_t nf;
+  const int* fquad;
+  const double* fw;
+  const double* ffr;
+  const double* fcoeff;
+  const double* fref;
+  double feps;
+  double* part;           // (bv+bt+bc+bf) * MAXT
 };
+
+__device__ __forceinline__ double fr_f0e(double y, double eps) {
+  return y >= eps ? y : -(y * y * y) / (3.0 * eps * eps) + y * y / eps + eps / 3.0;
+}
 
 __device__ __forceinline__ double trial_r(const EnergyArgs& a, int j) {
   return a.r0 ? __dmul_rn(*a.r0, a.rs[j]) : a.rs[j];
@@ -380,6 +413,26 @@ __global__ void __launch_bounds__(256) k_energy(EnergyArgs a) {
         acc[j] += el::psi(rg.model, rg.mu, rg.lam, F) * vol;
       }
     }
+  } else if (b >= a.bv + a.bt + a.bc) {
+    // friction: sum coeff f0(|T^T (sum w y - ref)|) (intact/friction.py:75-77)
+    const int bb = b - a.bv - a.bt - a.bc;
+    for (int64_t k = bb * (int64_t)blockDim.x + threadIdx.x; k < a.nf; k += (int64_t)a.bf * blockDim.x) {
+      const double* F = a.ffr + 6 * k;
+#pragma unroll 1
+      for (int j = 0; j < MAXT; ++j) {
+        if (j >= a.T) break;
+        double rel[3] = {0.0, 0.0, 0.0};
+        for (int e = 0; e < 4; ++e) {
+          const int64_t v = a.fquad[4 * k + e];
+          const double wv = a.fw[4 * k + e];
+          for (int c = 0; c < 3; ++c) rel[c] += wv * trial_coord(a, rj[j], 3 * v + c);
+        }
+        for (int c = 0; c < 3; ++c) rel[c] -= a.fref[3 * k + c];
+        const double u0 = F[0] * rel[0] + F[2] * rel[1] + F[4] * rel[2];
+        const double u1 = F[1] * rel[0] + F[3] * rel[1] + F[5] * rel[2];
+        acc[j] += a.fcoeff[k] * fr_f0e(sqrt(u0 * u0 + u1 * u1), a.feps);
+      }
+    }
   } else {
     const int bb = b - a.bv - a.bt;
     for (int64_t c = bb * (int64_t)blockDim.x + threadIdx.x; c < a.nc; c += (int64_t)a.bc * blockDim.x) {
@@ -409,20 +462,23 @@ __global__ void __launch_bounds__(256) k_energy(EnergyArgs a) {
   }
 }
 
-__global__ void k_energy_final(const double* __restrict__ part, int T, int bv, int bt, int bc, double h2,
+__global__ void k_energy_final(const double* __restrict__ part, int T, int bv, int bt, int bc, int bf, double h2,
                                double* __restrict__ out) {
-  // one warp per trial
+  // one warp per trial: ((inertia + h^2 elastic) + AL) + friction, the
+  // reference's accumulation order (intact/solver.py:98-106)
   const int j = threadIdx.x >> 5;
   if (j >= T) return;
   const int lane = threadIdx.x & 31;
-  double si = 0.0, se = 0.0, sa = 0.0;
+  double si = 0.0, se = 0.0, sa = 0.0, sf = 0.0;
   for (int k = lane; k < bv; k += 32) si += part[(size_t)k * MAXT + j];
   for (int k = lane; k < bt; k += 32) se += part[(size_t)(bv + k) * MAXT + j];
   for (int k = lane; k < bc; k += 32) sa += part[(size_t)(bv + bt + k) * MAXT + j];
+  for (int k = lane; k < bf; k += 32) sf += part[(size_t)(bv + bt + bc + k) * MAXT + j];
   si = warp_sum(si);
   se = warp_sum(se);
   sa = warp_sum(sa);
-  if (lane == 0) out[j] = (0.5 * si + h2 * se) + sa;
+  sf = warp_sum(sf);
+  if (lane == 0) out[j] = ((0.5 * si + h2 * se) + sa) + sf;
 }
 
 // ------------------------------------------------------------ inversion cap
@@ -595,13 +651,23 @@ int system_assemble(ibf_system* s, ibf_contacts* c, const double* x_hat, const d
     cv = contact_view(c);
     coef_g = c->coef_g.p;
   }
+  FrictionView fv;
+  const double* fr_gw = nullptr;
+  ibf_friction* fr = (s->friction && s->friction->n) ? s->friction : nullptr;
+  if (fr) {
+    IBF_TRY(friction_build_incidence(fr, s->n, st));
+    IBF_TRY(friction_prepare(fr, x_hat, st));
+    fv = friction_view(fr);
+    fr_gw = fr->gw.p;
+  }
   RowArgs r{s->n, x_hat, x_tilde, s->masses.p, mask, s->vt_ptr.p, s->vt_src.p, s->elem_grad.p,
-            s->pat.diag_q.p, s->pat.val.p, cv, coef_g, grad, s->pinv.p, s->flags.p};
+            s->pat.diag_q.p, s->pat.val.p, cv, coef_g, fv, fr_gw, grad, s->pinv.p, s->flags.p};
   if (s->n) {
     k_vertex_rows<<<(int)std::min<int64_t>(div_up(s->n, 256), 148LL * 32), 256, 0, st>>>(r);
     IBF_LAUNCH_CHECK();
   }
   s->assembled_contacts = (c && c->n) ? c : nullptr;
+  s->assembled_friction = fr != nullptr;
   s->assembled_dbc = mask != nullptr;
   return IBF_OK;
 }
@@ -642,11 +708,22 @@ int system_energy_launch(ibf_system* s, ibf_contacts* c, const double* x_hat, co
   a.bv = (int)std::max<int64_t>(1, std::min<int64_t>(div_up(s->n, 256), 148 * 2));
   a.bt = (int)std::max<int64_t>(1, std::min<int64_t>(div_up(s->m, 256), 148 * 8));
   a.bc = (int)std::max<int64_t>(1, std::min<int64_t>(div_up(a.nc, 256), 148 * 2));
-  IBF_TRY(s->epart.reserve((size_t)(a.bv + a.bt + a.bc) * MAXT));
+  ibf_friction* fr = (s->friction && s->friction->n) ? s->friction : nullptr;
+  a.nf = fr ? fr->n : 0;
+  a.bf = fr ? (int)std::max<int64_t>(1, std::min<int64_t>(div_up(a.nf, 256), 148)) : 0;
+  if (fr) {
+    a.fquad = fr->quad.p;
+    a.fw = fr->w.p;
+    a.ffr = fr->frames.p;
+    a.fcoeff = fr->coeff.p;
+    a.fref = fr->ref.p;
+    a.feps = fr->eps;
+  }
+  IBF_TRY(s->epart.reserve((size_t)(a.bv + a.bt + a.bc + a.bf) * MAXT));
   a.part = s->epart.p;
-  k_energy<<<a.bv + a.bt + a.bc, 256, 0, st>>>(a);
+  k_energy<<<a.bv + a.bt + a.bc + a.bf, 256, 0, st>>>(a);
   IBF_LAUNCH_CHECK();
-  k_energy_final<<<1, 32 * MAXT, 0, st>>>(s->epart.p, n_r, a.bv, a.bt, a.bc, h * h, out_dev);
+  k_energy_final<<<1, 32 * MAXT, 0, st>>>(s->epart.p, n_r, a.bv, a.bt, a.bc, a.bf, h * h, out_dev);
   IBF_LAUNCH_CHECK();
   return IBF_OK;
 }
@@ -670,6 +747,7 @@ ibf::Operator ibf_system::op() const {
   o.pinv = pinv.p;
   o.mask = assembled_dbc ? dbc.p : nullptr;
   if (assembled_contacts) o.contact = ibf::contact_view(assembled_contacts);
+  if (assembled_friction && friction) o.friction = ibf::friction_view(friction);
   return o;
 }
 
@@ -899,7 +977,12 @@ extern "C" int ibf_stiffness_diagonal_max(ibf_system* s, const double* x, double
     *out_host = 1.0;
     return IBF_OK;
   }
-  IBF_TRY(system_assemble(s, nullptr, x, x, 1.0, 1.0, h, false, s->vec_a.p, false, stream));
+  // contact- and friction-free system (intact/stepper.py:197)
+  ibf_friction* keep_friction = s->friction;
+  s->friction = nullptr;
+  const int st_asm = system_assemble(s, nullptr, x, x, 1.0, 1.0, h, false, s->vec_a.p, false, stream);
+  s->friction = keep_friction;
+  IBF_TRY(st_asm);
   k_fill<<<1, 1, 0, stream>>>(s->dscal.p + 8, 0.0, 1);
   k_diag_max<<<(int)std::min<int64_t>(div_up(s->n, 256), 148 * 4), 256, 0, stream>>>(s->n, s->pat.diag_q.p,
                                                                                        s->pat.val.p, s->dscal.p + 8);

@@ -37,6 +37,8 @@ struct ibf_system {
   long long pcg_iters = 0;       // CG iterations since the last stats reset
   long long contact_terms = 0;   // sum over PCG launches of C (matrix-free contact)
   ibf_contacts* assembled_contacts = nullptr;  // contact term of the last assembly
+  ibf_friction* friction = nullptr;            // frozen friction terms (ibf_system_set_friction)
+  bool assembled_friction = false;
   bool assembled_dbc = false;
   ibf::Operator op() const;
 };
@@ -46,6 +48,11 @@ namespace ibf {
 int contact_prepare(ibf_contacts* c, const double* x_hat, double mu, double offset, cudaStream_t s);
 int contact_build_incidence(ibf_contacts* c, int64_t n_verts, cudaStream_t s);
 ContactView contact_view(ibf_contacts* c);
+
+// friction.cu
+int friction_build_incidence(ibf_friction* f, int64_t n_verts, cudaStream_t s);
+int friction_prepare(ibf_friction* f, const double* x_hat, cudaStream_t s);
+FrictionView friction_view(ibf_friction* f);
 
 // system.cu
 int system_assemble(ibf_system* s, ibf_contacts* c, const double* x_hat, const double* x_tilde, double mu,

@@ -52,6 +52,7 @@ class DeviceSystem:
     """Device-resident elastic system (masses, regions, DBC mask)."""
 
     def __init__(self, masses, regions, dbc_mask=None):
+        self._friction = None
         masses = np.ascontiguousarray(masses, dtype=np.float64)
         n = len(masses)
         self.n = n
@@ -95,6 +96,14 @@ class DeviceSystem:
                                                    float(cg_tol), float(decay), _lib.host_ptr(res), _lib.stream()),
                    "solve_subproblem")
         return int(res[0]), int(res[1]), bool(res[2]), float(res[3])
+
+    def set_friction(self, friction):
+        """Frozen friction terms for the following assemble / energy / solve
+        calls (None removes them); keeps a reference to the handle."""
+        from .friction import as_device
+        self._friction = as_device(friction)
+        h = self._friction.handle if self._friction is not None and len(self._friction) else None
+        _lib.check(_lib.lib().ibf_system_set_friction(self.handle, h), "ibf_system_set_friction")
 
     def stiffness_diagonal_max(self, x, h) -> float:
         out = C.c_double()
@@ -194,24 +203,26 @@ class AssembledMatrix:
 
 
 def assemble(x_hat, x_tilde, masses, regions, batch, mu, offset, h, dbc_mask=None, friction=None):
-    """(grad (n,3), H) of the AL objective at x_hat (intact/solver.py:109-156)."""
-    if friction is not None and len(friction):
-        raise NotImplementedError("friction terms are not on the device path yet")
+    """(grad (n,3), H) of the AL objective at x_hat (intact/solver.py:109-156).
+    H keeps the friction terms it was assembled with (matrix-free)."""
     dev = device_system(masses, regions, dbc_mask)
     aset = _batch_set(batch, dev.n)
     xd, xt = to_dev(x_hat), to_dev(x_tilde)
     g = empty((dev.n, 3))
+    dev.set_friction(friction)
     dev.assemble(aset, xd, xt, mu, offset, h, dbc_mask is not None and np.any(dbc_mask), g)
-    return to_host(g), AssembledMatrix(dev, aset)
+    return to_host(g), AssembledMatrix(dev, (aset, dev._friction))
 
 
 def incremental_energy(x_hat, x_tilde, masses, regions, batch, mu, offset, h, friction=None) -> float:
     """L(x_hat) (intact/solver.py:88-106)."""
-    if friction is not None and len(friction):
-        raise NotImplementedError("friction terms are not on the device path yet")
     dev = device_system(masses, regions, None)
     aset = _batch_set(batch, dev.n)
-    return float(dev.energy(aset, to_dev(x_hat), to_dev(x_tilde), mu, offset, h)[0])
+    dev.set_friction(friction)
+    try:
+        return float(dev.energy(aset, to_dev(x_hat), to_dev(x_tilde), mu, offset, h)[0])
+    finally:
+        dev.set_friction(None)
 
 
 def line_search(x_hat, p, energy_fn, safe_cap: float = 1.0) -> tuple[float, bool]:
@@ -234,9 +245,11 @@ def solve_subproblem(x_tilde, x, x_hat0, masses, regions, active_set: ActiveSet,
                      decay=0.9, dbc_mask=None, friction=None) -> SubproblemResult:
     """Newton loop (cap 64, exit on full step) plus one dual sweep
     (intact/solver.py:178-233), run by libibf on the device."""
-    if friction is not None and len(friction):
-        raise NotImplementedError("friction terms are not on the device path yet")
     dev = device_system(masses, regions, dbc_mask)
     xt, xd, xh = to_dev(x_tilde), to_dev(x), to_dev(x_hat0)
-    nit, cgit, stalled, worst = dev.solve_subproblem(active_set, xt, xd, xh, mu, offset, h, cg_tol, decay)
+    dev.set_friction(friction)
+    try:
+        nit, cgit, stalled, worst = dev.solve_subproblem(active_set, xt, xd, xh, mu, offset, h, cg_tol, decay)
+    finally:
+        dev.set_friction(None)
     return SubproblemResult(to_host(xh), nit, cgit, stalled, worst)

@@ -344,3 +344,89 @@ def test_contact_heavy_subproblem_parity(pkg, n, layers, frames):
     dc = 2.0 * np.sqrt(3.0) * np.abs(xg - xo).max()
     assert np.abs(sg[2] - o.lam).max() <= mu * dc + 1e-12 * np.abs(o.lam).max()
     assert abs(w - wo) <= dc + 1e-12 * abs(wo)
+
+
+def _fr_system(pkg, g):
+    from paper_2512_12151_b200 import ElasticRegion, Material, MaterialModel, System
+    from paper_2512_12151_b200.stepper import BoundaryCondition
+    regions = [ElasticRegion(Material(MaterialModel.LIN, 1e7, 0.3), g["s_reg0_tets"], g["s_reg0_rows"],
+                             g["s_reg0_vols"]),
+               ElasticRegion(Material(MaterialModel.SNH, 1e5, 0.3), g["s_reg1_tets"], g["s_reg1_rows"],
+                             g["s_reg1_vols"])]
+    return System(g["s_masses"], regions, g["s_tris"], g["s_edges"], g["s_verts"],
+                  [BoundaryCondition(np.arange(int(g["s_n_slab"])))])
+
+
+def test_friction_precompute_matches_reference(pkg):
+    """friction_precompute on the device from the reference's accepted states
+    and multipliers (intact/friction.py:103-151): same terms in the same
+    order, witness weights bit-identical."""
+    from paper_2512_12151_b200.contact import ActiveSet
+    from paper_2512_12151_b200.friction import friction_precompute
+    g = golden("friction.npz")
+    for k in range(int(g["s_steps"])):
+        kinds, quads, lam = g[f"s_akind{k}"], g[f"s_aquad{k}"], g[f"s_alam{k}"]
+        n = len(kinds)
+        aset = ActiveSet()
+        aset.ensure(len(g["s_masses"]))
+        aset.import_state(kinds, quads, lam, np.ones(n), np.zeros(n), np.zeros(n), np.zeros((n, 4, 3)),
+                          np.zeros((n, 4, 3)))
+        ft = friction_precompute(g[f"s_x{k}"], aset, float(g[f"s_mu{k}"]), 1e-3, 0.01, 0.5, 1e-3)
+        nf = int(g[f"s_nfr{k}"])
+        assert (0 if ft is None else len(ft)) == nf
+        if nf:
+            assert np.array_equal(ft.indices, g[f"s_fidx{k}"])
+            assert np.array_equal(ft.weights, g[f"s_fw{k}"])
+            np.testing.assert_allclose(ft.frames, g[f"s_ffr{k}"], rtol=0, atol=1e-14)
+            np.testing.assert_allclose(ft.coeff, g[f"s_fc{k}"], rtol=1e-12)
+            np.testing.assert_allclose(ft.ref, g[f"s_fref{k}"], rtol=1e-13, atol=1e-16)
+            assert ft.eps == pytest.approx(1e-5)
+
+
+def test_assemble_and_energy_with_friction(pkg, rng):
+    """Friction terms in the gradient, the (matrix-free) Hessian and the
+    incremental energy vs the oracle (FP64, 1e-9 / 1e-12 relative)."""
+    from oracle import friction as ofriction
+    from paper_2512_12151_b200.solver import assemble, incremental_energy
+    g = golden("friction.npz")
+    system = _fr_system(pkg, g)
+    k = 2
+    fo = ofriction.FrictionSet(g[f"s_fidx{k}"], g[f"s_fw{k}"], g[f"s_ffr{k}"], g[f"s_fc{k}"], g[f"s_fref{k}"], 1e-5)
+    x = g[f"s_x{k}"]
+    x_tilde = x + 1e-4 * rng.standard_normal(x.shape)
+    x_hat = x + 1e-4 * rng.standard_normal(x.shape)        # slips across the eps = 1e-5 kink
+    n_slab = int(g["s_n_slab"])
+    x_hat[:n_slab] = x[:n_slab]
+    dbc = system.dbc_mask
+    mu_l, lam_l = material.lame(1e7, 0.3)
+    mu_s, lam_s = material.lame(1e5, 0.3)
+    oregions = [("lin", mu_l, lam_l, g["s_reg0_tets"], g["s_reg0_rows"], g["s_reg0_vols"]),
+                ("snh", mu_s, lam_s, g["s_reg1_tets"], g["s_reg1_rows"], g["s_reg1_vols"])]
+    go, Ho = newton.assemble(x_hat, x_tilde, system.masses, oregions, None, 1.0, 1e-3, 0.01, dbc, friction=fo)
+    gg, Hg = assemble(x_hat, x_tilde, system.masses, system.regions, None, 1.0, 1e-3, 0.01, dbc, friction=fo)
+    assert np.abs(gg - go).max() <= 1e-9 * np.abs(go).max()
+    for _ in range(3):
+        p = rng.standard_normal(x.shape)
+        yo, yg = Ho.matvec(p), Hg.matvec(p)
+        assert np.abs(yg - yo).max() <= 1e-9 * np.abs(yo).max()
+    eo = newton.energy(x_hat, x_tilde, system.masses, oregions, None, 1.0, 1e-3, 0.01, friction=fo)
+    eg = incremental_energy(x_hat, x_tilde, system.masses, system.regions, None, 1.0, 1e-3, 0.01, friction=fo)
+    assert eg == pytest.approx(eo, rel=1e-12)
+
+
+def test_sliding_box_with_friction_matches_reference(pkg):
+    """Five steps of the box sliding on the slab with mu_f = 0.5 through
+    Simulation (friction threaded step to step): positions within 1e-5
+    relative of the reference, same number of friction terms per step."""
+    from paper_2512_12151_b200 import Simulation, StepParams
+    from paper_2512_12151_b200.mesh import SimState
+    g = golden("friction.npz")
+    system = _fr_system(pkg, g)
+    params = StepParams(h=0.01, offset=1e-3, min_iterations=2, friction_coefficient=0.5, eps_v=1e-3)
+    sim = Simulation(system, params, SimState(g["s_xinit"].copy(), g["s_vinit"].copy()))
+    scale = np.abs(g["s_xinit"]).max()
+    for k in range(int(g["s_steps"])):
+        d = sim.advance()
+        assert np.abs(sim.state.x - g[f"s_x{k}"]).max() <= 1e-5 * scale, k
+        assert (0 if d.friction is None else len(d.friction)) == int(g[f"s_nfr{k}"]), k
+        assert np.array_equal(np.array([r.newton_iters for r in d.iterations]), g[f"s_newton{k}"])

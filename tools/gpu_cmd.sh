@@ -1,1 +1,1 @@
-timeout 1200 python bench.py > gpurun_out/bench_r1e.log 2>&1
+timeout 900 python -m pytest tests -m gpu -q 2>&1 | tail -15 > gpurun_out/pytest_gpu3.log
