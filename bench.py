@@ -308,7 +308,9 @@ def run_ours(args):
     traffic = None
     try:
         with open(NCU_SUMMARY) as f:
-            traffic = json.load(f).get("pcg_dram_bytes_per_launch")
+            # dram__bytes_read.sum + dram__bytes_write.sum per CG iteration of
+            # k_pcg from the committed ncu capture (profiles/ncu_summary.json)
+            traffic = json.load(f)["k_pcg"]["dram_bytes_per_cg_iter"]
     except Exception:
         pass
     phases = {"assembly_ms": stats[0] / args.steps, "pcg_ms": stats[2] / args.steps,
@@ -330,7 +332,7 @@ def run_ours(args):
             "peak_constraints": int(max(n_constraints)), "phases_ms": phases,
             "roofline": {"kernel": "k_pcg (symmetric BSR SpMV + block-Jacobi vector phase)", "bound": "hbm",
                          "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "peak_source": peak_kind, "traffic": traffic,
+                         "peak_source": peak_kind, "traffic": traffic, "traffic_unit": "bytes per CG iteration",
                          "bytes_per_cg_iter": spmv_bytes + 288.0 * n},
             "spmv_GBps": achieved,
             "e2e": {"value": e2e, "unit": "ms/frame", "h2d_bytes_per_step": 2 * 24 * n,
