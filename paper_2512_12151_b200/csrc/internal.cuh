@@ -120,6 +120,9 @@ struct SellPattern {
 struct PcgWork {
   DevBuf<double> r, z, p, hp, X, part, info;
   HostScratch host;
+  DevBuf<unsigned long long> prof;   // IBF_PCG_PROFILE builds only
+  DevBuf<int> counter;               // dynamic phase-A chunk counters
+  DevBuf<double> part_chunk;         // dynamic phase-A per-chunk partials
   int grid = 0;
   int n_alloc = -1;
 };

@@ -31,6 +31,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <numeric>
 #include <vector>
 
@@ -48,6 +49,12 @@ namespace ibf {
 #endif
 #ifndef IBF_SPMV_UNROLL
 #define IBF_SPMV_UNROLL 2
+#endif
+// Dynamic chunk scheduling of phase A (IBF_PCG_DYNAMIC=1) balances the
+// per-CTA work but its per-chunk partial sum adds a 1.8k-element reduction
+// after the barrier: measured 95 vs 90 us per iteration, so it is off.
+#ifndef IBF_PCG_DYNAMIC
+#define IBF_PCG_DYNAMIC 0
 #endif
 constexpr int PCG_THREADS = IBF_PCG_THREADS;
 // Shared-memory budget per CTA for carrying the rows' r and (q, p) from A to
@@ -346,6 +353,10 @@ struct PcgArgs {
   double* info;     // (iterations, converged, rel_res)
   double tol;
   int64_t max_iters;
+  unsigned long long* prof;  // IBF_PCG_PROFILE builds: per-CTA phase nanoseconds (G,6)
+  int* counter;         // dynamic phase A: chunk counters (2, alternating iterations)
+  double* part_chunk;   // dynamic phase A: per-chunk p.q partials
+  int n_chunks;         // dynamic phase A: chunks of blockDim rows (0: static mapping)
   int rows_per_thread;  // ceil(n / (grid * block))
   int smem_rows;        // rows_per_thread if (q, p) live in shared memory, else 0
 };
@@ -369,7 +380,26 @@ __device__ __forceinline__ void put_partials(double* part, int slot, double v, d
   if (threadIdx.x == 0) part[(size_t)slot * gridDim.x + blockIdx.x] = v;
 }
 
+#ifndef IBF_PCG_PROFILE
+#define IBF_PCG_PROFILE 0
+#endif
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// phase timers of a profiling build: [0] term dots + barrier, [1] A work,
+// [2] A barrier + reduction, [3] B work, [4] B barrier + reduction, [5] iterations
+#define PCG_PT(slot)                                   \
+  if (IBF_PCG_PROFILE && threadIdx.x == 0) {           \
+    const unsigned long long t_ = gtimer();            \
+    prof[slot] += t_ - t_last;                         \
+    t_last = t_;                                       \
+  }
+
 __global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
+  unsigned long long prof[6] = {0, 0, 0, 0, 0, 0};
+  unsigned long long t_last = IBF_PCG_PROFILE ? gtimer() : 0;
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double dyn[];
   __shared__ double red[32];
@@ -408,6 +438,7 @@ __global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
   }
   put_partials(a.part, 0, acc_b, red);
   put_partials(a.part, 1, acc_rz, red);
+  if (a.n_chunks && blockIdx.x == 0 && threadIdx.x == 0) a.counter[0] = a.counter[1] = 0;
   grid.sync();
   const double bnorm = sqrt(grid_total(a.part, 0, bc));
   double rz = grid_total(a.part, 1, bc);
@@ -426,41 +457,88 @@ __global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
     for (int64_t it = 1; it <= a.max_iters; ++it) {
       const DirGather gd{a.z, a.p[pb ^ 1], beta, first};
       double* pk = a.p[pb];
+      PCG_PT(5)
       // ---- A: contact dots on p_k, then q = H p_k, pAp
       if (op.contact.n || op.friction.n) {
         term_dots(op, gd);
         grid.sync();
       }
-      double acc = 0.0;
-      for (int k = 0, i = row0; k < R; ++k, i += S) {
-        if (i >= n) break;
-        double v[3], pv[3];
-        row_product(op, gd, i, v);
-        const double* Z = a.z + 3 * (size_t)i;
-        if (first) {
-          pv[0] = Z[0]; pv[1] = Z[1]; pv[2] = Z[2];
-        } else {
-          const double* P = gd.pold + 3 * (size_t)i;
-          pv[0] = cg_dir(beta, P[0], Z[0]);
-          pv[1] = cg_dir(beta, P[1], Z[1]);
-          pv[2] = cg_dir(beta, P[2], Z[2]);
-        }
-        double* pki = pk + 3 * (size_t)i;
-        pki[0] = pv[0]; pki[1] = pv[1]; pki[2] = pv[2];
-        if (in_smem) {
-          for (int c = 0; c < 3; ++c) {
-            sq[slot(k, c)] = v[c];
-            sp[slot(k, c)] = pv[c];
+      PCG_PT(0)
+      double pap;
+      if (a.n_chunks) {
+        // Dynamic row chunks (blockDim rows each, handed out in ascending
+        // order, so the sweep keeps its L2 locality): per-CTA speed differs
+        // by up to 2x (die / L2-slice locality), and a static split makes
+        // every CTA wait for the slowest at the barrier.  Each chunk's p.q
+        // partial goes to its own slot, summed in chunk order, so the result
+        // does not depend on which CTA took which chunk.
+        if (blockIdx.x == 0 && threadIdx.x == 0) a.counter[(it + 1) & 1] = 0;
+        __shared__ int chunk_sh;
+        while (true) {
+          if (threadIdx.x == 0) chunk_sh = atomicAdd(a.counter + (it & 1), 1);
+          __syncthreads();
+          const int ch = chunk_sh;
+          __syncthreads();
+          if (ch >= a.n_chunks) break;
+          const int i = ch * blockDim.x + threadIdx.x;
+          double accc = 0.0;
+          if (i < n) {
+            double v[3], pv[3];
+            row_product(op, gd, i, v);
+            gd.get(i, pv[0], pv[1], pv[2]);
+            double* pki = pk + 3 * (size_t)i;
+            pki[0] = pv[0]; pki[1] = pv[1]; pki[2] = pv[2];
+            double* qi = a.hp + 3 * (size_t)i;
+            qi[0] = v[0]; qi[1] = v[1]; qi[2] = v[2];
+            accc = pv[0] * v[0] + pv[1] * v[1] + pv[2] * v[2];
           }
-        } else {
-          double* qi = a.hp + 3 * (size_t)i;
-          qi[0] = v[0]; qi[1] = v[1]; qi[2] = v[2];
+          accc = block_sum(accc, red);
+          if (threadIdx.x == 0) a.part_chunk[ch] = accc;
         }
-        acc += pv[0] * v[0] + pv[1] * v[1] + pv[2] * v[2];
+        PCG_PT(1)
+        grid.sync();
+        if (threadIdx.x < 32) {
+          const double v = warp_sum_array(a.part_chunk, a.n_chunks);
+          if (threadIdx.x == 0) bc[0] = v;
+        }
+        __syncthreads();
+        pap = bc[0];
+        __syncthreads();
+        PCG_PT(2)
+      } else {
+        double acc = 0.0;
+        for (int k = 0, i = row0; k < R; ++k, i += S) {
+          if (i >= n) break;
+          double v[3], pv[3];
+          row_product(op, gd, i, v);
+          const double* Z = a.z + 3 * (size_t)i;
+          if (first) {
+            pv[0] = Z[0]; pv[1] = Z[1]; pv[2] = Z[2];
+          } else {
+            const double* P = gd.pold + 3 * (size_t)i;
+            pv[0] = cg_dir(beta, P[0], Z[0]);
+            pv[1] = cg_dir(beta, P[1], Z[1]);
+            pv[2] = cg_dir(beta, P[2], Z[2]);
+          }
+          double* pki = pk + 3 * (size_t)i;
+          pki[0] = pv[0]; pki[1] = pv[1]; pki[2] = pv[2];
+          if (in_smem) {
+            for (int c = 0; c < 3; ++c) {
+              sq[slot(k, c)] = v[c];
+              sp[slot(k, c)] = pv[c];
+            }
+          } else {
+            double* qi = a.hp + 3 * (size_t)i;
+            qi[0] = v[0]; qi[1] = v[1]; qi[2] = v[2];
+          }
+          acc += pv[0] * v[0] + pv[1] * v[1] + pv[2] * v[2];
+        }
+        PCG_PT(1)
+        put_partials(a.part, 2, acc, red);
+        grid.sync();
+        pap = grid_total(a.part, 2, bc);
+        PCG_PT(2)
       }
-      put_partials(a.part, 2, acc, red);
-      grid.sync();
-      const double pap = grid_total(a.part, 2, bc);
       if (pap <= 0.0) {
         // lost positive definiteness along p: keep the best iterate
         result = best;
@@ -504,10 +582,12 @@ __global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
         zi[0] = zv[0]; zi[1] = zv[1]; zi[2] = zv[2];
         acc_rz += rv[0] * zv[0] + rv[1] * zv[1] + rv[2] * zv[2];
       }
+      PCG_PT(3)
       put_partials(a.part, 0, acc_rr, red);
       put_partials(a.part, 1, acc_rz, red);
       grid.sync();
       const double res = sqrt(grid_total(a.part, 0, bc));
+      PCG_PT(4)
       cur = nxt;
       if (res < best_res) {
         best_res = res;
@@ -567,6 +647,8 @@ __global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
   const double* xr = Xb(result);
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < 3LL * n; k += S)
     a.x_out[k] = (bnorm == 0.0) ? 0.0 : xr[k];
+  if (IBF_PCG_PROFILE && threadIdx.x == 0 && a.prof)
+    for (int k = 0; k < 6; ++k) a.prof[6 * blockIdx.x + k] = prof[k];
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     a.info[0] = (double)iters;
     a.info[1] = conv ? 1.0 : 0.0;
@@ -649,10 +731,42 @@ int pcg_solve(const Operator& op, const double* rhs, double* x_out, double rel_t
   a.max_iters = max_iters;
   a.rows_per_thread = sh.rows_per_thread;
   a.smem_rows = sh.smem_rows;
+  a.n_chunks = 0;
+  a.counter = nullptr;
+  a.part_chunk = nullptr;
+  if (IBF_PCG_DYNAMIC && !sh.smem_rows) {
+    a.n_chunks = (int)div_up(std::max(n, 1), sh.threads);
+    IBF_TRY(w.counter.reserve(2));
+    IBF_TRY(w.part_chunk.reserve(a.n_chunks));
+    a.counter = w.counter.p;
+    a.part_chunk = w.part_chunk.p;
+  }
+  a.prof = nullptr;
+  if (IBF_PCG_PROFILE) {
+    IBF_TRY(w.prof.reserve(6 * (size_t)sh.grid));
+    a.prof = w.prof.p;
+  }
   const size_t smem = sh.smem_rows ? pcg_smem(sh.smem_rows, sh.threads) : 0;
   void* args[] = {&a};
   IBF_CUDA(cudaLaunchCooperativeKernel((void*)k_pcg, sh.grid, sh.threads, args, smem, s));
   ++g_launches;
+  if (IBF_PCG_PROFILE) {
+    std::vector<unsigned long long> h(6 * (size_t)sh.grid);
+    IBF_CUDA(cudaMemcpyAsync(h.data(), w.prof.p, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    IBF_CUDA(cudaStreamSynchronize(s));
+    double mean[6] = {0}, mx[6] = {0}, mn[6] = {1e30, 1e30, 1e30, 1e30, 1e30, 1e30};
+    for (int b = 0; b < sh.grid; ++b)
+      for (int k = 0; k < 6; ++k) {
+        const double v = 1e-3 * (double)h[6 * b + k];
+        mean[k] += v / sh.grid;
+        mx[k] = std::max(mx[k], v);
+        mn[k] = std::min(mn[k], v);
+      }
+    fprintf(stderr, "[ibf] pcg phases us (mean/min/max over CTAs): dots %.1f/%.1f/%.1f  A %.1f/%.1f/%.1f  "
+                    "Abar %.1f/%.1f/%.1f  B %.1f/%.1f/%.1f  Bbar %.1f/%.1f/%.1f  loop %.1f/%.1f/%.1f\n",
+            mean[0], mn[0], mx[0], mean[1], mn[1], mx[1], mean[2], mn[2], mx[2], mean[3], mn[3], mx[3], mean[4],
+            mn[4], mx[4], mean[5], mn[5], mx[5]);
+  }
   return IBF_OK;
 }
 
