@@ -389,7 +389,7 @@ def run_c5(args):
         torch.distributed.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    res = run_batch(seeds, args.steps)
+    res = run_batch(seeds, args.steps, concurrency=args.concurrency)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
     launches = L.ibf_launch_count() - launches0
@@ -407,8 +407,9 @@ def run_c5(args):
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": f"C5: {args.scenes} C1-like drops (seeded jitter), {args.steps} frames each, "
                                        "round-robin over ranks, no data-path collective",
-                           "parallelism": f"scene-parallel x{ws}"},
+                           "parallelism": f"scene-parallel x{ws}, {args.concurrency} scenes in flight per GPU"},
                 "newton_per_frame": sum(r.newton for r in records) / max(frames, 1),
+                "state_checksum": sum(r.checksum for r in records),
                 "aborted": sum(r.aborted for r in records),
                 "e2e": {"value": value, "unit": "scene-frames/s", "h2d_bytes_per_step": None,
                         "d2h_bytes_per_step": None, "note": "each scene runs through Simulation from host state"},
@@ -432,6 +433,8 @@ def main():
     ap.add_argument("--workload", default="c4", choices=["c4", "c5"],
                     help="c4: the headline press scene (default); c5: scene-parallel batch of drops")
     ap.add_argument("--scenes", type=int, default=64, help="c5: number of scenes in the batch")
+    ap.add_argument("--concurrency", type=int, default=8,
+                    help="c5: scenes in flight per GPU (host threads, one CUDA stream each)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

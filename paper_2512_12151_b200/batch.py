@@ -64,21 +64,45 @@ def run_scene(seed: int, frames: int, make_scene: Optional[Callable] = None) -> 
     return SceneRecord(seed, 0, frames, passes, newton, cg, start.elapsed_time(end), float(x.sum()), aborted)
 
 
-def run_batch(seeds: Sequence[int], frames: int, runner: Optional[Callable] = None, group=None):
-    """Run this rank's shard of `seeds`; rank 0 returns every record sorted
-    by seed, other ranks return None.  Without an initialised process group
-    the whole batch runs here."""
+def _run_concurrent(seeds, frames, runner, concurrency):
+    """Scenes of one GPU on `concurrency` host threads, each with its own CUDA
+    stream: small scenes are latency-bound (a few
+    hundred launches and a host sync per Newton iteration), so several in
+    flight fill the GPU.  The native calls release the GIL (ctypes), handles
+    are per scene, and the library's shared counters are atomic."""
+    import threading
+    from concurrent.futures import ThreadPoolExecutor
+    import torch
+    local = threading.local()
+
+    def work(seed):
+        if not hasattr(local, "stream"):
+            local.stream = torch.cuda.Stream()
+        with torch.cuda.stream(local.stream):
+            return runner(seed, frames)
+
+    with ThreadPoolExecutor(max_workers=concurrency) as ex:
+        return list(ex.map(work, seeds))
+
+
+def run_batch(seeds: Sequence[int], frames: int, runner: Optional[Callable] = None, group=None,
+              concurrency: int = 1):
+    """Run this rank's shard of `seeds` (`concurrency` scenes in flight per
+    GPU); rank 0 returns every record sorted by seed, other ranks return
+    None.  Without an initialised process group the whole batch runs here."""
     import torch.distributed as dist
     runner = runner or run_scene
     dist_on = dist.is_available() and dist.is_initialized()
     rank = dist.get_rank(group) if dist_on else 0
     world = dist.get_world_size(group) if dist_on else 1
     t0 = time.perf_counter()
-    mine = []
-    for seed in shard(seeds, rank, world):
-        rec = runner(seed, frames)
+    mine_seeds = shard(seeds, rank, world)
+    if concurrency > 1:
+        mine = _run_concurrent(mine_seeds, frames, runner, concurrency)
+    else:
+        mine = [runner(seed, frames) for seed in mine_seeds]
+    for rec in mine:
         rec.rank = rank
-        mine.append(rec)
     wall = time.perf_counter() - t0
     if not dist_on:
         return sorted(mine, key=lambda r: r.seed), [wall]

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <string>
 #include <vector>
 
@@ -30,8 +31,9 @@ void set_error(const std::string& msg);
   } while (0)
 
 // every kernel launch of the library is followed by IBF_LAUNCH_CHECK, which
-// also counts it (ibf_launch_count) for the bench's gpu_launches claim
-extern unsigned long long g_launches;
+// also counts it (ibf_launch_count) for the bench's gpu_launches claim;
+// atomic, since independent scenes may step concurrently on separate streams
+extern std::atomic<unsigned long long> g_launches;
 #define IBF_LAUNCH_CHECK()        \
   do {                            \
     ++::ibf::g_launches;          \

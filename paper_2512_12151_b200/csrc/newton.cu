@@ -24,7 +24,7 @@
 
 namespace ibf {
 
-unsigned long long g_launches = 0;
+std::atomic<unsigned long long> g_launches{0};
 
 static int trace_level() {
   static int lvl = -1;
@@ -353,7 +353,7 @@ extern "C" int ibf_vec_sub(int64_t n, const double* a, const double* b, double* 
   return IBF_OK;
 }
 
-extern "C" unsigned long long ibf_launch_count(void) { return ibf::g_launches; }
+extern "C" unsigned long long ibf_launch_count(void) { return ibf::g_launches.load(); }
 
 extern "C" int ibf_system_stats(ibf_system* s, double* out, int reset) {
   s->t_asm.harvest();

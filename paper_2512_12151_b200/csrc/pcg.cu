@@ -667,7 +667,8 @@ struct PcgShape {
 };
 
 static PcgShape pcg_shape(int n) {
-  static int max_b = -1;
+  static std::atomic<int> max_b_cache{-1};
+  int max_b = max_b_cache.load();
   if (max_b < 0) {
     if (PCG_SMEM_BYTES > 0)
       cudaFuncSetAttribute(k_pcg, cudaFuncAttributeMaxDynamicSharedMemorySize, PCG_SMEM_BYTES);
@@ -678,6 +679,7 @@ static PcgShape pcg_shape(int n) {
     int nb = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_pcg, PCG_THREADS, 0);
     max_b = nb > 0 ? nb : 1;
+    max_b_cache.store(max_b);
   }
   n = std::max(n, 1);
   auto shape_for = [&](int b) {
