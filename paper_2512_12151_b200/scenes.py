@@ -14,6 +14,9 @@ map); scenes follow SURVEY.md §8(d):
       reference algorithm itself blows up on it after a few frames (ultra-light
       shells escape tangentially under the linearised constraints; GPU and
       oracle agree on identical inputs — DESIGN.md §Scenes).
+  C2  27 SNH cubes (3x3x3 stack, 131k tets) falling into a pinned box.
+  C3  8 NH rods (491k tets) whose end layers are twisted in opposite senses
+      by rotational scripted Dirichlet conditions.
   C5  randomized C1-like drops (seeded jitter of translation, rotation and
       velocity), one scene per seed.
 
@@ -217,6 +220,92 @@ def c4_scene(n=42, radius=0.1, gap=0.001, plate_speed=0.1, h=0.01, layers=None, 
                                 h=h, scripted_stop=stop)
     params = StepParams(h=h, offset=1e-3, min_iterations=2)
     return system, state, params
+
+
+class _ScriptedTwist:
+    """Rotation of fixed start positions about a vertical axis through
+    `center` by omega * t at the end of step k (a rotational scripted DBC,
+    SURVEY.md §8(d) C3; the reference's Python BoundaryCondition API,
+    intact/stepper.py:78-100)."""
+
+    def __init__(self, start, center, omega, h=0.01):
+        self.start = np.asarray(start, dtype=np.float64)
+        self.center = np.zeros(3)
+        self.center[:2] = np.asarray(center, dtype=np.float64)[:2]
+        self.omega, self.h = float(omega), float(h)
+
+    def __call__(self, step_index):
+        a = self.omega * (step_index + 1) * self.h
+        c, s_ = np.cos(a), np.sin(a)
+        d = self.start - self.center
+        out = self.start.copy()
+        out[:, 0] = self.center[0] + c * d[:, 0] - s_ * d[:, 1]
+        out[:, 1] = self.center[1] + s_ * d[:, 0] + c * d[:, 1]
+        return out
+
+
+def c2_scene(grid=3, cells=(9, 9, 10), size=(0.09, 0.09, 0.1), gap=0.002, h=0.01):
+    """Stack of grid^3 SNH cubes falling into a pinned box of five slabs
+    (27 x 4,860 tets = 131k tets, dense multi-body
+    contact and active-set churn)."""
+    size = np.asarray(size, dtype=np.float64)
+    mat = Material(MaterialModel.SNH, 1e5, 0.3)
+    rho = 1000.0
+    edge = float(np.min(size / np.asarray(cells)))
+    pitch = size + gap
+    span = grid * pitch - gap
+    lo = -0.5 * span[:2]
+    cube = box_mesh(*cells, size=size)
+    bodies = []
+    wall = 0.02
+    inner = span[:2] + 2 * 0.01
+    height = grid * pitch[2] + 0.05
+    # floor and four walls, pinned (per-vertex diagonal matched to the cubes).
+    # The five slabs keep a slit between one another: the reference's CCD
+    # also tests pairs of pinned primitives, and touching slabs would pin
+    # alpha at 0 for good (TOI 0, intact/ccd.py:64-66).
+    slit = 0.002
+    bodies.append(_pinned_slab((inner[0] + 2 * wall, inner[1] + 2 * wall, wall),
+                               (-inner[0] / 2 - wall, -inner[1] / 2 - wall, -wall), (12, 12, 1), mat.young, rho, edge))
+    for sx, sy, cx, cy in ((wall, inner[1] - 2 * slit, -inner[0] / 2 - wall, -inner[1] / 2 + slit),
+                           (wall, inner[1] - 2 * slit, inner[0] / 2, -inner[1] / 2 + slit),
+                           (inner[0], wall, -inner[0] / 2, -inner[1] / 2 - wall),
+                           (inner[0], wall, -inner[0] / 2, inner[1] / 2)):
+        bodies.append(_pinned_slab((sx, sy, height), (cx, cy, slit),
+                                   (1 if sx == wall else 12, 1 if sy == wall else 12, 10), mat.young, rho, edge))
+    for k in range(grid):
+        for j in range(grid):
+            for i in range(grid):
+                org = (lo[0] + i * pitch[0], lo[1] + j * pitch[1], gap + k * pitch[2])
+                bodies.append((transformed(cube, translate=org), mat, rho, (0.0, 0.0, 0.0)))
+    system, state, _ = merge(bodies, boundary_bodies=list(range(5)), h=h)
+    return system, state, StepParams(h=h, offset=1e-3, min_iterations=2)
+
+
+def c3_scene(rows=2, cols=4, cells=(8, 8, 160), size=(0.02, 0.02, 0.4), gap=0.002, omega=np.pi, h=0.01):
+    """Bundle of NH rods (rho 1e3, E 1e6, nu 0.3, offset 2e-4)
+    whose end layers are twisted in opposite senses about the bundle axis by
+    rotational scripted Dirichlet conditions (~500k tets,
+    self-contact with edge-edge dominated CCD)."""
+    size = np.asarray(size, dtype=np.float64)
+    mat = Material(MaterialModel.NH, 1e6, 0.3)
+    rho = 1e3
+    rod = box_mesh(*cells, size=size)
+    pitch = size[:2] + gap
+    bodies = []
+    for j in range(rows):
+        for i in range(cols):
+            org = (-0.5 * (cols * pitch[0] - gap) + i * pitch[0], -0.5 * (rows * pitch[1] - gap) + j * pitch[1], 0.0)
+            bodies.append((transformed(rod, translate=org), mat, rho, (0.0, 0.0, 0.0)))
+    system, state, offs = merge(bodies, h=h)
+    x = state.x
+    bottom = np.flatnonzero(np.isclose(x[:, 2], 0.0))
+    top = np.flatnonzero(np.isclose(x[:, 2], size[2]))
+    boundary = [BoundaryCondition(bottom, kind="scripted", trajectory=_ScriptedTwist(x[bottom], (0, 0), -omega, h)),
+                BoundaryCondition(top, kind="scripted", trajectory=_ScriptedTwist(x[top], (0, 0), omega, h))]
+    system = System(system.masses, system.regions, system.surface_triangles, system.surface_edges,
+                    system.surface_vertices, boundary)
+    return system, state, StepParams(h=h, offset=2e-4, min_iterations=2)
 
 
 def c5_scene(seed, nx=10, ny=10, nz=8):

@@ -184,7 +184,8 @@ def _oracle_scene(system):
     regions = [(r.material.model.value, r.material.mu, r.material.lam, r.tets, r.shape_rows, r.volumes)
                for r in system.regions]
     return timestep.Scene(system.masses, regions, system.surface_triangles, system.surface_edges,
-                          system.surface_vertices, [(bc.vertices, None) for bc in system.boundary])
+                          system.surface_vertices,
+                          [(bc.vertices, bc.trajectory if bc.kind == "scripted" else None) for bc in system.boundary])
 
 
 def test_c1_per_pass_sets_on_identical_inputs(pkg):
@@ -430,3 +431,46 @@ def test_sliding_box_with_friction_matches_reference(pkg):
         assert np.abs(sim.state.x - g[f"s_x{k}"]).max() <= 1e-5 * scale, k
         assert (0 if d.friction is None else len(d.friction)) == int(g[f"s_nfr{k}"]), k
         assert np.array_equal(np.array([r.newton_iters for r in d.iterations]), g[f"s_newton{k}"])
+
+
+def _jittered(state, system, amp=1e-7, seed=5):
+    """Break the exact TOI ties of axis-aligned stacks (admission compares
+    TOIs for equality, intact/contact.py:151) with a sub-micron jitter of the
+    free vertices."""
+    from paper_2512_12151_b200.mesh import SimState
+    x = state.x.copy()
+    free = ~system.dbc_mask
+    x[free] += amp * np.random.default_rng(seed).standard_normal(x[free].shape)
+    return SimState(x, state.v.copy())
+
+
+def test_c2_stack_small_matches_oracle(pkg):
+    """Reduced C2 (2x2x2 cubes falling into the pinned five-slab box):
+    positions 1e-5 relative per step, equal pass counts, Newton +-1,
+    identical active key sets."""
+    from paper_2512_12151_b200 import scenes
+    system, state, params = scenes.c2_scene(grid=2, cells=(3, 3, 3), size=(0.03, 0.03, 0.03), gap=0.001)
+    state = _jittered(state, system)
+    out = _run_both(system, state, params, 5)
+    assert max(len(kg) for *_, kg, _ in out) > 0
+    for xg, xo, d, rec, kg, ko in out:
+        assert np.abs(xg - xo).max() <= 1e-5 * np.abs(xo).max()
+        assert len(d.iterations) == len(rec)
+        assert all(abs(a.newton_iters - b[3]) <= 1 for a, b in zip(d.iterations, rec))
+        assert kg == ko
+
+
+def test_c3_twisted_rods_small_matches_oracle(pkg):
+    """Reduced C3 (two NH rods, end layers twisted in opposite senses by
+    rotational scripted Dirichlet conditions): same checks as C2."""
+    from paper_2512_12151_b200 import scenes
+    system, state, params = scenes.c3_scene(rows=1, cols=2, cells=(2, 2, 12), size=(0.02, 0.02, 0.12), gap=0.001,
+                                            omega=6 * np.pi)
+    state = _jittered(state, system)
+    out = _run_both(system, state, params, 5)
+    assert max(len(kg) for *_, kg, _ in out) > 0
+    for xg, xo, d, rec, kg, ko in out:
+        assert np.abs(xg - xo).max() <= 1e-5 * np.abs(xo).max()
+        assert len(d.iterations) == len(rec)
+        assert all(abs(a.newton_iters - b[3]) <= 1 for a, b in zip(d.iterations, rec))
+        assert kg == ko
