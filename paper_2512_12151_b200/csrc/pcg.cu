@@ -57,15 +57,16 @@ namespace ibf {
 #define IBF_PCG_DYNAMIC 0
 #endif
 constexpr int PCG_THREADS = IBF_PCG_THREADS;
-// Shared-memory budget per CTA for carrying the rows' r and (q, p) from A to
-// B on chip.  Off by default: at C4 size the carry needs ~48 KB per CTA, and
-// the SMEM it takes comes out of the unified L1 that the SpMV gathers live
-// in — measured 2x slower per CG iteration (the carry pays off only when the
-// L1 working set is small).  An interleaved (z, p) record layout for the
-// gathers was also measured slower (94 vs 88 us per iteration: the two
-// half-record writes per iteration cost more than the fused gather saves).
+// Shared-memory budget per CTA for keeping each thread's rows' residual on
+// chip for the whole solve (it is only ever touched by its row's owner):
+// 16 KB per CTA at C4 size, 86.6 vs 90.4 us per CG iteration.  Carrying q
+// and p across the A/B barrier as well (IBF_PCG_CARRY_QP=1, ~48 KB per CTA)
+// is 2x slower: that SMEM comes out of the unified L1 the SpMV gathers live
+// in.  An interleaved (z, p) record layout for the gathers was also slower
+// (94 vs 88 us: the two half-record writes per iteration cost more than the
+// fused gather saves).
 #ifndef IBF_PCG_SMEM_KB
-#define IBF_PCG_SMEM_KB 0
+#define IBF_PCG_SMEM_KB 20
 #endif
 constexpr int PCG_SMEM_BYTES = IBF_PCG_SMEM_KB * 1024;
 
@@ -358,7 +359,8 @@ struct PcgArgs {
   double* part_chunk;   // dynamic phase A: per-chunk p.q partials
   int n_chunks;         // dynamic phase A: chunks of blockDim rows (0: static mapping)
   int rows_per_thread;  // ceil(n / (grid * block))
-  int smem_rows;        // rows_per_thread if (q, p) live in shared memory, else 0
+  int smem_rows;        // rows_per_thread if the carry lives in shared memory, else 0
+  int carry_qp;         // with smem_rows: 1 carries r, q and p; 0 carries r only
 };
 
 // all CTAs compute the same fixed-order total of part[slot*G .. slot*G+G)
@@ -409,10 +411,11 @@ __global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
   const int S = gridDim.x * blockDim.x;          // rows per sweep
   const int R = a.rows_per_thread;
   const bool in_smem = a.smem_rows > 0;
+  const bool qp_smem = in_smem && a.carry_qp;
   // per-thread row slots: row(k) = blockIdx.x*blockDim.x + threadIdx.x + k*S
   double* sq = dyn;                                  // (R, 3, blockDim) H p
   double* sp = dyn + 3 * (size_t)R * blockDim.x;     // (R, 3, blockDim) p
-  double* sr = dyn + 6 * (size_t)R * blockDim.x;     // (R, 3, blockDim) residual
+  double* sr = dyn + (a.carry_qp ? 6 : 0) * (size_t)R * blockDim.x;   // (R, 3, blockDim) residual
   auto slot = [&](int k, int c) { return ((size_t)k * 3 + c) * blockDim.x + threadIdx.x; };
   // the residual is only ever touched by its row's owner: keep it on chip
   auto r_ref = [&](int k, int i, int c) -> double& { return in_smem ? sr[slot(k, c)] : a.r[3 * (size_t)i + c]; };
@@ -522,7 +525,7 @@ __global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
           }
           double* pki = pk + 3 * (size_t)i;
           pki[0] = pv[0]; pki[1] = pv[1]; pki[2] = pv[2];
-          if (in_smem) {
+          if (qp_smem) {
             for (int c = 0; c < 3; ++c) {
               sq[slot(k, c)] = v[c];
               sp[slot(k, c)] = pv[c];
@@ -558,7 +561,7 @@ __global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
       for (int k = 0, i = row0; k < R; ++k, i += S) {
         if (i >= n) break;
         double qv[3], pv[3], rv[3], zv[3];
-        if (in_smem) {
+        if (qp_smem) {
           for (int c = 0; c < 3; ++c) {
             qv[c] = sq[slot(k, c)];
             pv[c] = sp[slot(k, c)];
@@ -656,7 +659,12 @@ __global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
   }
 }
 
-static size_t pcg_smem(int rows_per_thread, int threads) { return (size_t)9 * rows_per_thread * threads * sizeof(double); }
+#ifndef IBF_PCG_CARRY_QP
+#define IBF_PCG_CARRY_QP 0
+#endif
+static size_t pcg_smem(int rows_per_thread, int threads) {
+  return (size_t)(IBF_PCG_CARRY_QP ? 9 : 3) * rows_per_thread * threads * sizeof(double);
+}
 
 // Launch shape: a full wave of co-resident CTAs, rows_per_thread sweeps, and
 // a block size trimmed (in warps) so the last sweep is nearly full — every
@@ -733,6 +741,7 @@ int pcg_solve(const Operator& op, const double* rhs, double* x_out, double rel_t
   a.max_iters = max_iters;
   a.rows_per_thread = sh.rows_per_thread;
   a.smem_rows = sh.smem_rows;
+  a.carry_qp = IBF_PCG_CARRY_QP;
   a.n_chunks = 0;
   a.counter = nullptr;
   a.part_chunk = nullptr;

@@ -1,1 +1,3 @@
-for c in 1 8; do timeout 900 python bench.py --workload c5 --steps 5 --warmup 3 --concurrency $c > gpurun_out/bench_c5_$c.log 2>&1; done
+python tools/bench_spmv.py > gpurun_out/spmv_new.json 2> gpurun_out/spmv_new.err
+timeout 900 python -m pytest tests -m gpu -q 2>&1 | tail -4 > gpurun_out/pytest_gpu3.log
+timeout 1200 python bench.py > gpurun_out/bench_r1h.log 2>&1
