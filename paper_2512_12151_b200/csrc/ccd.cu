@@ -405,6 +405,8 @@ static int build_tree(ibf_ccd* c, int64_t n, cudaStream_t s, Tree& t) {
 // prefilter, sort.  Result pairs in c->pairs_sorted[0..count).
 static int broad_pass(ibf_ccd* c, int kind, const double* x0, const double* x1, double min_gap, bool filter,
                       int64_t* count, int64_t* n_candidates, cudaStream_t s) {
+  Trace tr(kind == 0 ? "broad_pass VF" : (kind == 1 ? "broad_pass EE" : "broad_pass TT"));
+  tr.mark("enter", s);
   const int64_t nt = (kind == 1) ? c->ne : c->nt;
   const int64_t nq = (kind == 0) ? c->nv : ((kind == 1) ? c->ne : c->nt);
   *count = 0;
@@ -431,8 +433,10 @@ static int broad_pass(ibf_ccd* c, int kind, const double* x0, const double* x1, 
     IBF_CUDA(cudaMemcpyAsync(c->qlo.p, c->box_lo.p, 3 * nt * sizeof(double), cudaMemcpyDeviceToDevice, s));
     IBF_CUDA(cudaMemcpyAsync(c->qhi.p, c->box_hi.p, 3 * nt * sizeof(double), cudaMemcpyDeviceToDevice, s));
   }
+  tr.mark("boxes", s, nt);
   Tree tree;
   IBF_TRY(build_tree(c, nt, s, tree));
+  tr.mark("tree", s);
   IBF_TRY(c->counters.reserve(4));
   IBF_TRY(c->host.reserve(64));
   if (c->pairs.cap < 4096) IBF_TRY(c->pairs.reserve(1 << 16));
@@ -469,6 +473,7 @@ static int broad_pass(ibf_ccd* c, int kind, const double* x0, const double* x1, 
     }
     IBF_TRY(c->pairs.reserve((size_t)h[0]));
   }
+  tr.mark("traverse", s, *n_candidates);
   const int64_t cnt = *count;
   IBF_TRY(c->pairs_sorted.reserve(std::max<int64_t>(cnt, 1)));
   if (cnt) {
@@ -478,6 +483,8 @@ static int broad_pass(ibf_ccd* c, int kind, const double* x0, const double* x1, 
     size_t have = c->cub_tmp.cap;
     IBF_CUDA(cub::DeviceRadixSort::SortKeys(c->cub_tmp.p, have, c->pairs.p, c->pairs_sorted.p, (int)cnt, 0, 64, s));
   }
+  tr.mark("sort", s, cnt);
+  tr.mark("exit", s);
   return IBF_OK;
 }
 
