@@ -321,7 +321,10 @@ def run_ours(args):
               "energy": stats[6] / args.steps}
     line = {"metric": METRIC, "value": value, "unit": "ms/frame", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": value, "higher_is_better": False, "scaling": "weak",
-            "vs_baseline": round(5367.0 / value, 3) if value > 0 else None,
+            # value / the paper's 5,367 ms/frame (RTX 4090, FP64, the authors' own mesh;
+            # this is the solid-ball proxy of the same 2.2M-tet press scene)
+            "vs_baseline": round(value / 5367.0, 4) if value > 0 else None,
+            "vs_baseline_note": "value / 5367 ms/frame (paper Table 1, RTX 4090); lower is better; proxy scene",
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": workload(args), "system": f"{sum(len(r.tets) for r in system.regions)} tets, "
                                                             f"{n} vertices incl. the two pinned plates",
