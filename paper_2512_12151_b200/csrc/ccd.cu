@@ -237,6 +237,9 @@ struct TraverseArgs {
   int filter;          // 1: keep only pairs that can block (TOI 0 or needs advancement)
   unsigned long long* out;
   unsigned long long cap;
+  // self-queries (EE, tri-tri): visit the queries in the tree's Morton order
+  // (its sorted keys), so a warp's 32 traversals follow nearly the same path
+  const unsigned long long* qorder;
   unsigned long long* counters;  // [0] emitted, [1] all candidates
 };
 
@@ -268,7 +271,8 @@ __device__ __forceinline__ bool make_quad(const TraverseArgs& a, int qi, int pi,
 
 __global__ void __launch_bounds__(128) k_traverse(TraverseArgs a) {
   unsigned long long n_cand = 0;
-  for (int64_t qi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; qi < a.nq; qi += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < a.nq; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t qi = a.qorder ? (int64_t)(a.qorder[t] & 0xffffffffull) : t;
     const double ql[3] = {a.qlo[3 * qi], a.qlo[3 * qi + 1], a.qlo[3 * qi + 2]};
     const double qh[3] = {a.qhi[3 * qi], a.qhi[3 * qi + 1], a.qhi[3 * qi + 2]};
     // LBVH depth is bounded by the 64 key bits, so depth+1 entries suffice
@@ -444,6 +448,7 @@ static int broad_pass(ibf_ccd* c, int kind, const double* x0, const double* x1, 
     IBF_CUDA(cudaMemsetAsync(c->counters.p, 0, 2 * sizeof(unsigned long long), s));
     TraverseArgs a;
     a.tree = tree;
+    a.qorder = (kind == 0) ? nullptr : tree.keys;
     a.nq = nq;
     a.qlo = c->qlo.p;
     a.qhi = c->qhi.p;
