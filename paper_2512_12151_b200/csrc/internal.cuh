@@ -91,6 +91,7 @@ struct Operator {
   const int* slice_ptr = nullptr;     // (S+1) storage block offset per slice
   const int* col = nullptr;           // (nq) column of each storage block
   const double* val = nullptr;        // 9 (nq + 32) entries, qel layout
+  size_t val_bytes = 0;
   const int* low_ptr = nullptr;       // (S+1) lower-entry offset per slice
   const int2* low = nullptr;          // (nlq) (storage block, source row)
   const uint8_t* mask = nullptr;      // (n) DBC mask (contact masking) or null

@@ -209,12 +209,15 @@ extern "C" int ibf_solve_subproblem(ibf_system* s, ibf_contacts* c, const double
   double* hd = (double*)s->host.p;      // hd[0..7] energies, hd[8] r0, hd[9..11] pcg info
   int* hi = (int*)(hd + 16);            // hi[0] nonfinite, hi[1] grad nonzero
   ibf_contacts* cc = (c && c->n) ? c : nullptr;
+  Trace tr("solve_subproblem");
+  tr.mark("enter", stream, cc ? cc->n : 0);
   if (cc) {
     IBF_TRY(c->iscratch.reserve(2));
     IBF_CUDA(cudaMemsetAsync(c->iscratch.p, 0, sizeof(int), stream));
     IBF_TRY(contacts_refresh(c, x, c->iscratch.p, stream));
     IBF_TRY(contact_build_incidence(c, n, stream));
   }
+  tr.mark("refresh+incidence", stream);
   int newton = 0;
   int64_t cg_total = 0;
   bool stalled = false;
@@ -225,11 +228,13 @@ extern "C" int ibf_solve_subproblem(ibf_system* s, ibf_contacts* c, const double
     s->t_asm.begin(stream);
     IBF_TRY(system_assemble(s, cc, x_hat, x_tilde, mu, offset, h, true, grad, true, stream));
     s->t_asm.end(stream);
+    tr.mark("assemble", stream);
     k_neg<<<grid_for(n3), 256, 0, stream>>>(n3, grad, rhs);
     IBF_LAUNCH_CHECK();
     s->t_pcg.begin(stream);
     IBF_TRY(pcg_solve(s->op(), rhs, p, cg_tol, 10 * n, s->work, stream));
     s->t_pcg.end(stream);
+    tr.mark("pcg", stream);
     k_dot_part<<<dot_parts, 256, 0, stream>>>(n3, grad, p, dpart);
     IBF_LAUNCH_CHECK();
     k_descent_fix<<<grid_for(n), 256, 0, stream>>>(n, dpart, dot_parts, grad, s->pinv.p, p);
@@ -249,6 +254,7 @@ extern "C" int ibf_solve_subproblem(ibf_system* s, ibf_contacts* c, const double
     IBF_CUDA(cudaMemcpyAsync(hd + 9, s->work.info.p, 3 * sizeof(double), cudaMemcpyDeviceToHost, stream));
     IBF_CUDA(cudaMemcpyAsync(hi, s->flags.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, stream));
     IBF_CUDA(cudaStreamSynchronize(stream));
+    tr.mark("safeguard+cap+energy+sync", stream);
     if (hi[0]) {
       set_error("elastic energy is not finite at the evaluation point");
       return IBF_ERR_NONFINITE;
@@ -325,6 +331,7 @@ extern "C" int ibf_solve_subproblem(ibf_system* s, ibf_contacts* c, const double
     }
   }
   if (capped) stalled = true;
+  tr.mark("linesearch+step", stream);
   double w = 0.0;
   if (cc) {
     IBF_TRY(contacts_dual(c, x_hat, offset, mu, decay, worst, stream));
@@ -332,6 +339,8 @@ extern "C" int ibf_solve_subproblem(ibf_system* s, ibf_contacts* c, const double
     IBF_CUDA(cudaStreamSynchronize(stream));
     w = hd[0];
   }
+  tr.mark("dual", stream);
+  tr.mark("exit", stream);
   result_host[0] = newton;
   result_host[1] = (double)cg_total;
   result_host[2] = stalled ? 1.0 : 0.0;
