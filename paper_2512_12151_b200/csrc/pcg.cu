@@ -202,8 +202,13 @@ __device__ __forceinline__ void row_product(const Operator& op, const Gather& gp
     const int* C = op.col + q0 + lane;
     int k = 0;
     if (IBF_SPMV_UNROLL >= 2) {
+      // column indices are loaded one slot pair ahead, so the p gathers of a
+      // pair never wait on an index load (the chain per pair is one level)
+      int n0 = w > 0 ? __ldg(C) : 0, n1 = w > 1 ? __ldg(C + 32) : 0;
       for (; k + 2 <= w; k += 2) {
-        const int j0 = __ldg(C + 32 * k), j1 = __ldg(C + 32 * k + 32);
+        const int j0 = n0, j1 = n1;
+        if (k + 2 < w) n0 = __ldg(C + 32 * (k + 2));
+        if (k + 3 < w) n1 = __ldg(C + 32 * (k + 3));
         const double* B = V + 288 * (size_t)k;
         double b[9], c[9];
 #pragma unroll
@@ -234,8 +239,11 @@ __device__ __forceinline__ void row_product(const Operator& op, const Gather& gp
     const int2* L = op.low + l0 + lane;
     int t = 0;
     if (IBF_SPMV_UNROLL >= 2) {
+      int2 n0 = w > 0 ? __ldg(L) : make_int2(0, 0), n1 = w > 1 ? __ldg(L + 32) : make_int2(0, 0);
       for (; t + 2 <= w; t += 2) {
-        const int2 e0 = __ldg(L + 32 * t), e1 = __ldg(L + 32 * t + 32);
+        const int2 e0 = n0, e1 = n1;
+        if (t + 2 < w) n0 = __ldg(L + 32 * (t + 2));
+        if (t + 3 < w) n1 = __ldg(L + 32 * (t + 3));
         const double* B0 = op.val + qel(e0.x, 0);
         const double* B1 = op.val + qel(e1.x, 0);
         double b[9], c[9];
