@@ -51,9 +51,10 @@ namespace ibf {
 #ifndef IBF_SPMV_UNROLL
 #define IBF_SPMV_UNROLL 2
 #endif
-// Dynamic chunk scheduling of phase A (IBF_PCG_DYNAMIC=1) balances the
-// per-CTA work but its per-chunk partial sum adds a 1.8k-element reduction
-// after the barrier: measured 95 vs 90 us per iteration, so it is off.
+// Dynamic chunk scheduling of phase A (IBF_PCG_DYNAMIC=1): measured equal to
+// the static split (86.3 vs 86.4 us per iteration).  The per-CTA spread of
+// phase A (44-77 us) persists with it: a chunk is one row per thread, and a
+// row's dependent-load latency (~20 us under load) is the scheduling grain.
 #ifndef IBF_PCG_DYNAMIC
 #define IBF_PCG_DYNAMIC 0
 #endif
@@ -509,13 +510,13 @@ __global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
         }
         PCG_PT(1)
         grid.sync();
-        if (threadIdx.x < 32) {
-          const double v = warp_sum_array(a.part_chunk, a.n_chunks);
-          if (threadIdx.x == 0) bc[0] = v;
+        {
+          // whole-CTA fixed-order sum of the chunk partials (strided, then
+          // the block tree): identical in every CTA, ~8 loads per thread
+          double v = 0.0;
+          for (int c = threadIdx.x; c < a.n_chunks; c += blockDim.x) v += a.part_chunk[c];
+          pap = block_sum(v, red);
         }
-        __syncthreads();
-        pap = bc[0];
-        __syncthreads();
         PCG_PT(2)
       } else {
         double acc = 0.0;
