@@ -429,12 +429,22 @@ __global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
   auto slot = [&](int k, int c) { return ((size_t)k * 3 + c) * blockDim.x + threadIdx.x; };
   // the residual is only ever touched by its row's owner: keep it on chip
   auto r_ref = [&](int k, int i, int c) -> double& { return in_smem ? sr[slot(k, c)] : a.r[3 * (size_t)i + c]; };
-  const int row0 = blockIdx.x * blockDim.x + threadIdx.x;
+  // Row of this thread in sweep k.  Full sweeps give each CTA a contiguous
+  // block of blockDim rows; the last, partial sweep is dealt out by 32-row
+  // slices round-robin over the CTAs (slice = warp * G + CTA), so every CTA
+  // (and SM) gets the same share of it instead of the low CTAs taking it all
+  // (a ~10 % per-SM imbalance at C4 size otherwise).
+  auto row_of = [&](int k) {
+    if (k < R - 1) return k * S + blockIdx.x * blockDim.x + threadIdx.x;
+    const int slice = (threadIdx.x >> 5) * gridDim.x + blockIdx.x;
+    return (R - 1) * S + 32 * slice + (threadIdx.x & 31);
+  };
   auto Xb = [&](int k) { return a.X + (size_t)k * 3 * n; };
 
   // ---- r = b, z = P^-1 r, x = 0
   double acc_b = 0.0, acc_rz = 0.0;
-  for (int k = 0, i = row0; k < R; ++k, i += S) {
+  for (int k = 0; k < R; ++k) {
+    const int i = row_of(k);
     if (i >= n) break;
     const double r0 = a.rhs[3 * (size_t)i], r1 = a.rhs[3 * (size_t)i + 1], r2 = a.rhs[3 * (size_t)i + 2];
     double zv[3];
@@ -520,7 +530,8 @@ __global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
         PCG_PT(2)
       } else {
         double acc = 0.0;
-        for (int k = 0, i = row0; k < R; ++k, i += S) {
+        for (int k = 0; k < R; ++k) {
+          const int i = row_of(k);
           if (i >= n) break;
           double v[3], pv[3];
           row_product(op, gd, i, v);
@@ -568,7 +579,8 @@ __global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
       double* xn = Xb(nxt);
       double acc_rr = 0.0;
       acc_rz = 0.0;
-      for (int k = 0, i = row0; k < R; ++k, i += S) {
+      for (int k = 0; k < R; ++k) {
+        const int i = row_of(k);
         if (i >= n) break;
         double qv[3], pv[3], rv[3], zv[3];
         if (qp_smem) {
@@ -622,7 +634,8 @@ __global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
           grid.sync();
         }
         acc_rz = 0.0;
-        for (int k = 0, i = row0; k < R; ++k, i += S) {
+        for (int k = 0; k < R; ++k) {
+          const int i = row_of(k);
           if (i >= n) break;
           double v[3], zv[3];
           row_product(op, gx, i, v);
@@ -703,8 +716,7 @@ static PcgShape pcg_shape(int n) {
   auto shape_for = [&](int b) {
     const int grid = (int)std::min<int64_t>((int64_t)b * sm_count(), div_up(n, PCG_THREADS));
     const int rpt = (int)div_up(n, (int64_t)grid * PCG_THREADS);
-    const int threads = (int)std::min<int64_t>(PCG_THREADS, 32 * div_up(div_up(n, (int64_t)grid * rpt), 32));
-    return PcgShape{grid, threads, rpt, 0};
+    return PcgShape{grid, PCG_THREADS, rpt, 0};
   };
   // the on-chip carry when a full wave of CTAs with it stays co-resident
   for (int b = max_b; b >= 1 && PCG_SMEM_BYTES > 0; --b) {
