@@ -87,8 +87,11 @@ struct ElemArgs {
   int* flags;
 };
 
+#ifndef IBF_ELEM_MINB
+#define IBF_ELEM_MINB 1
+#endif
 template <bool HESS>
-__global__ void __launch_bounds__(ELEM_THREADS) k_elem(ElemArgs a) {
+__global__ void __launch_bounds__(ELEM_THREADS, IBF_ELEM_MINB) k_elem(ElemArgs a) {
   __shared__ double stage[ELEM_THREADS / 32][384];
   __shared__ RegionDev sreg[MAX_SMEM_REGIONS];
   const bool use_smem = a.nreg <= MAX_SMEM_REGIONS;

@@ -24,6 +24,17 @@ e1.record(); torch.cuda.synchronize()
 t_spmv = e0.elapsed_time(e1) / R
 b = dev.spmv_bytes()
 out = {"N": N, "blocks": dev.n_blocks, "spmv_ms": t_spmv, "spmv_GBps": b / t_spmv / 1e6, "spmv_bytes": b}
+for _ in range(3): dev.assemble(None, x, xt, 1.0, 1e-3, 0.01, True, g)
+torch.cuda.synchronize()
+e0.record()
+for _ in range(10): dev.assemble(None, x, xt, 1.0, 1e-3, 0.01, True, g)
+e1.record(); torch.cuda.synchronize()
+out["assemble_ms"] = e0.elapsed_time(e1) / 10
+rs = np.ones(2)
+e0.record()
+for _ in range(10): dev.energy(None, x, xt, 1.0, 1e-3, 0.01, p=g, rs=(1.0, 0.5))
+e1.record(); torch.cuda.synchronize()
+out["energy2_ms"] = e0.elapsed_time(e1) / 10
 rhs = -g
 xo = empty((N, 3))
 dev.pcg(rhs, xo, 1e-30, 20)
