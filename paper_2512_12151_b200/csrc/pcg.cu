@@ -315,8 +315,132 @@ __global__ void __launch_bounds__(256, 2) k_spmv(Operator op, const double* __re
   }
 }
 
+// ------------------------------------------------ TMA-staged upper stream
+// Each warp owns one 32-row slice at a time.  Its upper slots are one
+// contiguous range (w x 2304 bytes, 16-byte aligned), so lane 0 streams them
+// into the warp's shared-memory stages with 1D bulk async copies
+// (cp.async.bulk ... mbarrier::complete_tx), two slots per stage, two stages:
+// the copy engine moves the next pair while the lanes consume the current
+// one from SMEM (conflict-free: entry e of slot k for lane l at
+// stage[(k*9 + e)*32 + l]).  The p gathers and the transposed part stay LDG.
+constexpr int TMA_WARPS = 4;                   // 128 threads, 36.9 KB of stages
+constexpr int TMA_STAGE_DOUBLES = 2 * 288;     // two slots of a slice
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+__global__ void __launch_bounds__(TMA_WARPS * 32, 1) k_spmv_tma(Operator op, const double* __restrict__ p,
+                                                              double* __restrict__ y) {
+  __shared__ __align__(128) double stage[TMA_WARPS][2][TMA_STAGE_DOUBLES];
+  __shared__ __align__(8) unsigned long long bar[TMA_WARPS][2];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    mbar_init(&bar[warp][0], 1);
+    mbar_init(&bar[warp][1], 1);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncwarp();
+  unsigned phase[2] = {0, 0};
+  const PlainGather gp{p};
+  const int n_slices = (op.n + 31) >> 5;
+  for (int sl = blockIdx.x * TMA_WARPS + warp; sl < n_slices; sl += gridDim.x * TMA_WARPS) {
+    const int i = 32 * sl + lane;
+    const int q0 = __ldg(op.slice_ptr + sl), w = (__ldg(op.slice_ptr + sl + 1) - q0) >> 5;
+    const double* V = op.val + 9 * (size_t)q0;
+    const int* C = op.col + q0 + lane;
+    const int npairs = (w + 1) >> 1;
+    auto issue = [&](int pr, int st) {
+      if (lane == 0) {
+        const int slots = min(2, w - 2 * pr);
+        const unsigned bytes = (unsigned)(slots * 288 * sizeof(double));
+        mbar_expect_tx(&bar[warp][st], bytes);
+        bulk_g2s(stage[warp][st], V + 576 * (size_t)pr, bytes, &bar[warp][st]);
+      }
+    };
+    if (npairs > 0) issue(0, 0);
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    for (int pr = 0; pr < npairs; ++pr) {
+      const int st = pr & 1;
+      // every lane has finished reading stage st^1 (pair pr-1) before it is refilled
+      __syncwarp();
+      if (pr + 1 < npairs) issue(pr + 1, st ^ 1);
+      const int k = 2 * pr;
+      const int j0 = __ldg(C + 32 * k);
+      const int j1 = (k + 1 < w) ? __ldg(C + 32 * k + 32) : i;
+      double x0, x1, x2, z0 = 0.0, z1 = 0.0, z2 = 0.0;
+      gp.get(j0, x0, x1, x2);
+      if (k + 1 < w) gp.get(j1, z0, z1, z2);
+      mbar_wait(&bar[warp][st], phase[st]);
+      phase[st] ^= 1;
+      const double* S0 = stage[warp][st] + lane;
+      double b[9];
+#pragma unroll
+      for (int e = 0; e < 9; ++e) b[e] = S0[32 * e];
+      acc_upper(b, x0, x1, x2, a0, a1, a2);
+      if (k + 1 < w) {
+#pragma unroll
+        for (int e = 0; e < 9; ++e) b[e] = S0[288 + 32 * e];
+        acc_upper(b, z0, z1, z2, a0, a1, a2);
+      }
+    }
+    __syncwarp();
+    if (i < op.n) {
+      // transposed part and contact/friction as in row_product
+      const int l0 = __ldg(op.low_ptr + sl), lw = (__ldg(op.low_ptr + sl + 1) - l0) >> 5;
+      const int2* L = op.low + l0 + lane;
+      for (int t = 0; t < lw; ++t) {
+        const int2 le = __ldg(L + 32 * t);
+        const double* B = op.val + qel(le.x, 0);
+        double b[9];
+#pragma unroll
+        for (int e = 0; e < 9; ++e) b[e] = __ldg(B + 32 * e);
+        double x0, x1, x2;
+        gp.get(le.y, x0, x1, x2);
+        acc_lower(b, x0, x1, x2, a0, a1, a2);
+      }
+      y[3 * (size_t)i] = a0;
+      y[3 * (size_t)i + 1] = a1;
+      y[3 * (size_t)i + 2] = a2;
+    }
+  }
+}
+
 int spmv(const Operator& op, const double* x, double* y, cudaStream_t s) {
   if (op.n == 0) return IBF_OK;
+  static int tma = -1;
+  if (tma < 0) tma = getenv("IBF_SPMV_TMA") ? atoi(getenv("IBF_SPMV_TMA")) : 0;
+  if (tma && !op.contact.n && !op.friction.n) {
+    // experimental (measured): TMA-staged upper stream
+    const int grid = (int)std::min<int64_t>(div_up(op.n, 32 * TMA_WARPS), (int64_t)tma * sm_count());
+    k_spmv_tma<<<grid, 32 * TMA_WARPS, 0, s>>>(op, x, y);
+    IBF_LAUNCH_CHECK();
+    return IBF_OK;
+  }
   if (op.contact.n || op.friction.n) {
     k_contact_dot<<<(int)div_up(std::max(op.contact.n, op.friction.n), 256), 256, 0, s>>>(op, x);
     IBF_LAUNCH_CHECK();
