@@ -297,7 +297,15 @@ __global__ void __launch_bounds__(128) k_traverse(TraverseArgs a) {
           emit = geo::accd_class(a.kind, X0, X1, a.min_gap) != 1;
         }
         if (emit) {
-          const unsigned long long slot = atomicAdd(a.counters, 1ull);
+          // warp-aggregated append: the lanes emitting at this point take
+          // consecutive slots with one atomic for the group
+          const unsigned grp = __activemask();
+          const int lane = threadIdx.x & 31;
+          const int leader = __ffs(grp) - 1;
+          unsigned long long base = 0;
+          if (lane == leader) base = atomicAdd(a.counters, (unsigned long long)__popc(grp));
+          base = __shfl_sync(grp, base, leader);
+          const unsigned long long slot = base + __popc(grp & ((1u << lane) - 1u));
           if (slot < a.cap) a.out[slot] = ((unsigned long long)qi << 32) | (unsigned long long)pi;
         }
       } else {
