@@ -1,0 +1,30 @@
+"""Dev tool: the whole C4 press (plate 0.5 m/s to 5 cm, then hold), F frames,
+per-frame device ms / Newton / CG / constraints, for a whole-run average
+comparable to the paper's per-scene average."""
+import sys, os, json
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import bench
+from paper_2512_12151_b200 import scenes
+from paper_2512_12151_b200.contact import ActiveSet
+from paper_2512_12151_b200.device import to_dev
+from paper_2512_12151_b200.stepper import step_device
+frames = int(sys.argv[1]) if len(sys.argv) > 1 else 100
+system, state, params = scenes.c4_scene(n=42, plate_speed=bench.PLATE_SPEED, plate_stop=bench.PLATE_STOP)
+aset = ActiveSet(); aset.ensure(system.n_vertices)
+x, v = to_dev(state.x), to_dev(state.v)
+rows = []
+for k in range(frames):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    x, v, d = step_device(x, v, system, aset, params, step_index=k)
+    e1.record(); torch.cuda.synchronize()
+    rows.append({"frame": k, "ms": e0.elapsed_time(e1), "passes": len(d.iterations),
+                 "newton": sum(r.newton_iters for r in d.iterations), "cg": sum(r.cg_iters for r in d.iterations),
+                 "constraints": len(aset)})
+    print(json.dumps(rows[-1]), flush=True)
+ms = np.array([r["ms"] for r in rows])
+print(json.dumps({"frames": frames, "mean_ms": float(ms.mean()), "max_ms": float(ms.max()),
+                  "mean_newton": float(np.mean([r["newton"] for r in rows])),
+                  "mean_cg_per_solve": float(sum(r["cg"] for r in rows) / max(sum(r["newton"] for r in rows), 1)),
+                  "peak_constraints": max(r["constraints"] for r in rows), "rows": rows}))
