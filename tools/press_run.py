@@ -10,6 +10,7 @@ from paper_2512_12151_b200.contact import ActiveSet
 from paper_2512_12151_b200.device import to_dev
 from paper_2512_12151_b200.stepper import step_device
 frames = int(sys.argv[1]) if len(sys.argv) > 1 else 100
+first_logged = int(sys.argv[2]) if len(sys.argv) > 2 else 0
 system, state, params = scenes.c4_scene(n=42, plate_speed=bench.PLATE_SPEED, plate_stop=bench.PLATE_STOP)
 aset = ActiveSet(); aset.ensure(system.n_vertices)
 x, v = to_dev(state.x), to_dev(state.v)
@@ -21,8 +22,11 @@ for k in range(frames):
     e1.record(); torch.cuda.synchronize()
     rows.append({"frame": k, "ms": e0.elapsed_time(e1), "passes": len(d.iterations),
                  "newton": sum(r.newton_iters for r in d.iterations), "cg": sum(r.cg_iters for r in d.iterations),
-                 "constraints": len(aset)})
-    print(json.dumps(rows[-1]), flush=True)
+                 "constraints": len(aset), "triggers": d.adaptive_triggers, "mu": d.mu, "offset": d.offset,
+                 "min_alpha": min(r.alpha for r in d.iterations),
+                 "alpha_lt_1e-4": sum(r.alpha < 1e-4 for r in d.iterations)})
+    if k >= first_logged:
+        print(json.dumps(rows[-1]), flush=True)
 ms = np.array([r["ms"] for r in rows])
 print(json.dumps({"frames": frames, "mean_ms": float(ms.mean()), "max_ms": float(ms.max()),
                   "mean_newton": float(np.mean([r["newton"] for r in rows])),
