@@ -37,7 +37,8 @@ typedef enum {
     IBF_ERR_CUDA = 2,
     IBF_ERR_OOM = 3,
     IBF_ERR_NONFINITE = 4,   /* NonFiniteEnergyError, intact/solver.py:35 */
-    IBF_ERR_NO_DEVICE = 5
+    IBF_ERR_NO_DEVICE = 5,
+    IBF_ERR_IO = 6           /* file could not be written: OSError */
 } ibf_status;
 
 /* material models — MaterialModel, intact/elasticity.py:31-35 */
@@ -103,6 +104,26 @@ int ibf_static_intersection(ibf_ccd* c, const double* x, int64_t* n_hits, int64_
  * than radius apart, so d_host > 0 certifies that no surface primitives touch. */
 int ibf_min_distance(ibf_ccd* c, const double* x, double radius, double* d_host, int64_t* pair_host,
                      ibf_stream s);
+
+/* ------------------------------------------------------ scene build / export */
+typedef struct ibf_surface ibf_surface;
+
+/* Boundary surface of a tet mesh: replaces extract_surface_arrays
+ * (intact/mesh.py:106-124).  tets: (m,4) int64 dev, ids in [0, 2^31).
+ * Counts come back at once; ibf_surface_get copies tris (n_tris,3) in the
+ * tets' face order and winding, edges (n_edges,2) unique sorted, verts
+ * (n_verts) unique ascending (int64, host or dev pointers, NULL skips).
+ * n_nonmanifold = edges shared by > 2 boundary faces (the reference's warning). */
+int ibf_surface_extract(int64_t m, const int64_t* tets, ibf_surface** out, int64_t* n_tris,
+                        int64_t* n_edges, int64_t* n_verts, int64_t* n_nonmanifold, ibf_stream s);
+int ibf_surface_get(const ibf_surface* h, int64_t* tris, int64_t* edges, int64_t* verts, ibf_stream s);
+void ibf_surface_destroy(ibf_surface* h);
+
+/* OBJ frame: replaces export_frame (intact/io_utils.py:35-43).  Host
+ * pointers; byte-identical file (repr coordinates, compacted 1-based faces).
+ * n_threads <= 0 uses every hardware thread.  Needs no GPU. */
+int ibf_export_obj(const char* path, const double* positions, int64_t n_positions, const int64_t* tris,
+                   int64_t n_tris, int n_threads);
 
 /* ------------------------------------------------------------ active set */
 typedef struct ibf_contacts ibf_contacts;

@@ -15,7 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 # IBF_LIB selects another build of the same ABI (A/B timing of kernel variants)
 LIB_PATH = os.environ.get("IBF_LIB") or os.path.join(HERE, "libibf.so")
 
-IBF_OK, IBF_ERR_BAD_ARG, IBF_ERR_CUDA, IBF_ERR_OOM, IBF_ERR_NONFINITE, IBF_ERR_NO_DEVICE = range(6)
+IBF_OK, IBF_ERR_BAD_ARG, IBF_ERR_CUDA, IBF_ERR_OOM, IBF_ERR_NONFINITE, IBF_ERR_NO_DEVICE, IBF_ERR_IO = range(7)
 MODELS = {"snh": 0, "nh": 1, "cor": 2, "lin": 3}
 
 _vp = C.c_void_p
@@ -38,6 +38,10 @@ _PROTOS = {
     "ibf_max_step_size": (_int, [_vp, _vp, _vp, _dbl, _dbl, _pdbl, _pi64, _vp]),
     "ibf_ccd_get_blocking": (_int, [_vp, _vp, _vp, _vp, _vp]),
     "ibf_static_intersection": (_int, [_vp, _vp, _pi64, _vp, _i64, _vp]),
+    "ibf_surface_extract": (_int, [_i64, _vp, C.POINTER(_vp), _pi64, _pi64, _pi64, _pi64, _vp]),
+    "ibf_surface_get": (_int, [_vp, _vp, _vp, _vp, _vp]),
+    "ibf_surface_destroy": (None, [_vp]),
+    "ibf_export_obj": (_int, [C.c_char_p, _vp, _i64, _vp, _i64, _int]),
     "ibf_friction_create": (_int, [C.POINTER(_vp)]),
     "ibf_friction_destroy": (None, [_vp]),
     "ibf_friction_size": (_i64, [_vp]),
@@ -120,6 +124,8 @@ def check(status, what=""):
         raise NonFiniteEnergyError(msg)
     if status == IBF_ERR_BAD_ARG:
         raise ValueError(f"{what}: {msg}")
+    if status == IBF_ERR_IO:
+        raise OSError(f"{what}: {msg}")
     raise IbfError(f"{what}: status {status}: {msg}")
 
 

@@ -18,7 +18,7 @@ CSRC = os.path.join(HERE, "csrc")
 OUT = os.environ.get("IBF_BUILD_OUT", os.path.join(HERE, "libibf.so"))
 BUILD = os.environ.get("IBF_BUILD_DIR", os.path.join(CSRC, "build"))
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-SOURCES = ["pcg.cu", "system.cu", "contact.cu", "ccd.cu", "newton.cu", "friction.cu"]
+SOURCES = ["pcg.cu", "system.cu", "contact.cu", "ccd.cu", "newton.cu", "friction.cu", "surface.cu", "export.cpp"]
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
@@ -28,7 +28,7 @@ FLAGS = [
 
 
 def _compile(src, verbose):
-    obj = os.path.join(BUILD, src.replace(".cu", ".o"))
+    obj = os.path.join(BUILD, os.path.splitext(src)[0] + ".o")
     cmd = [NVCC, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
@@ -43,7 +43,7 @@ def _stale():
         return True
     t = os.path.getmtime(OUT)
     for f in os.listdir(CSRC):
-        if f.endswith((".cu", ".cuh")) and os.path.getmtime(os.path.join(CSRC, f)) > t:
+        if f.endswith((".cu", ".cuh", ".cpp")) and os.path.getmtime(os.path.join(CSRC, f)) > t:
             return True
     hdr = os.path.join(os.path.dirname(HERE), "include", "ibf.h")
     return os.path.exists(hdr) and os.path.getmtime(hdr) > t

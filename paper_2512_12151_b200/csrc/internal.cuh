@@ -43,7 +43,16 @@ struct ContactView {
 // per-row list of (storage block, source row) entries stored the same way.
 // Padding blocks are zero with col = own row; padding lower entries point at
 // a zero block past the last slice.
+//
+// IBF_BLOCK_AOS builds (experiment) keep each block's 9 entries contiguous
+// instead: val[9 q + e].
+#ifndef IBF_BLOCK_AOS
+#define IBF_BLOCK_AOS 0
+#endif
+constexpr int QEL_ES = IBF_BLOCK_AOS ? 1 : 32;   // stride between entries of a block
+constexpr int QEL_LS = IBF_BLOCK_AOS ? 9 : 1;    // stride between lanes of a slice
 __host__ __device__ __forceinline__ size_t qel(int q, int e) {
+  if (IBF_BLOCK_AOS) return 9 * (size_t)q + e;
   return 9 * (size_t)(q & ~31) + (size_t)(q & 31) + 32 * (size_t)e;
 }
 

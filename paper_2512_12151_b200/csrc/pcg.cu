@@ -199,7 +199,7 @@ __device__ __forceinline__ void row_product(const Operator& op, const Gather& gp
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
   {
     const int q0 = __ldg(op.slice_ptr + s), w = (__ldg(op.slice_ptr + s + 1) - q0) >> 5;
-    const double* V = op.val + 9 * (size_t)q0 + lane;
+    const double* V = op.val + 9 * (size_t)q0 + QEL_LS * lane;
     const int* C = op.col + q0 + lane;
     int k = 0;
     if (IBF_SPMV_UNROLL >= 2) {
@@ -214,8 +214,8 @@ __device__ __forceinline__ void row_product(const Operator& op, const Gather& gp
         double b[9], c[9];
 #pragma unroll
         for (int e = 0; e < 9; ++e) {
-          b[e] = __ldg(B + 32 * e);
-          c[e] = __ldg(B + 288 + 32 * e);
+          b[e] = __ldg(B + QEL_ES * e);
+          c[e] = __ldg(B + 288 + QEL_ES * e);
         }
         double x0, x1, x2, y0, y1, y2;
         gp.get(j0, x0, x1, x2);
@@ -229,7 +229,7 @@ __device__ __forceinline__ void row_product(const Operator& op, const Gather& gp
       const double* B = V + 288 * (size_t)k;
       double b[9];
 #pragma unroll
-      for (int e = 0; e < 9; ++e) b[e] = __ldg(B + 32 * e);
+      for (int e = 0; e < 9; ++e) b[e] = __ldg(B + QEL_ES * e);
       double x0, x1, x2;
       gp.get(j, x0, x1, x2);
       acc_upper(b, x0, x1, x2, a0, a1, a2);
@@ -250,8 +250,8 @@ __device__ __forceinline__ void row_product(const Operator& op, const Gather& gp
         double b[9], c[9];
 #pragma unroll
         for (int e = 0; e < 9; ++e) {
-          b[e] = __ldg(B0 + 32 * e);
-          c[e] = __ldg(B1 + 32 * e);
+          b[e] = __ldg(B0 + QEL_ES * e);
+          c[e] = __ldg(B1 + QEL_ES * e);
         }
         double x0, x1, x2, y0, y1, y2;
         gp.get(e0.y, x0, x1, x2);
@@ -265,7 +265,7 @@ __device__ __forceinline__ void row_product(const Operator& op, const Gather& gp
       const double* B = op.val + qel(le.x, 0);
       double b[9];
 #pragma unroll
-      for (int e = 0; e < 9; ++e) b[e] = __ldg(B + 32 * e);
+      for (int e = 0; e < 9; ++e) b[e] = __ldg(B + QEL_ES * e);
       double x0, x1, x2;
       gp.get(le.y, x0, x1, x2);
       acc_lower(b, x0, x1, x2, a0, a1, a2);
@@ -397,14 +397,14 @@ __global__ void __launch_bounds__(TMA_WARPS * 32, 1) k_spmv_tma(Operator op, con
       if (k + 1 < w) gp.get(j1, z0, z1, z2);
       mbar_wait(&bar[warp][st], phase[st]);
       phase[st] ^= 1;
-      const double* S0 = stage[warp][st] + lane;
+      const double* S0 = stage[warp][st] + QEL_LS * lane;
       double b[9];
 #pragma unroll
-      for (int e = 0; e < 9; ++e) b[e] = S0[32 * e];
+      for (int e = 0; e < 9; ++e) b[e] = S0[QEL_ES * e];
       acc_upper(b, x0, x1, x2, a0, a1, a2);
       if (k + 1 < w) {
 #pragma unroll
-        for (int e = 0; e < 9; ++e) b[e] = S0[288 + 32 * e];
+        for (int e = 0; e < 9; ++e) b[e] = S0[288 + QEL_ES * e];
         acc_upper(b, z0, z1, z2, a0, a1, a2);
       }
     }
@@ -418,7 +418,7 @@ __global__ void __launch_bounds__(TMA_WARPS * 32, 1) k_spmv_tma(Operator op, con
         const double* B = op.val + qel(le.x, 0);
         double b[9];
 #pragma unroll
-        for (int e = 0; e < 9; ++e) b[e] = __ldg(B + 32 * e);
+        for (int e = 0; e < 9; ++e) b[e] = __ldg(B + QEL_ES * e);
         double x0, x1, x2;
         gp.get(le.y, x0, x1, x2);
         acc_lower(b, x0, x1, x2, a0, a1, a2);

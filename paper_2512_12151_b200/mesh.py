@@ -80,6 +80,44 @@ def surface_of(tets):
     return bnd, edges, np.unique(bnd)
 
 
+def extract_surface_arrays(tets):
+    """Boundary faces, their unique sorted edges and vertices, computed on
+    the device (csrc/surface.cu): drop-in for intact/mesh.py:106-124 with
+    bit-identical outputs.  `tets` is (m,4) int64, numpy or a CUDA tensor;
+    the results are numpy int64 arrays.  Needs the GPU (no host fallback;
+    `surface_of` is the host preprocessing path of build_tet_mesh)."""
+    import ctypes as C
+    from . import _lib
+    from .device import require_cuda
+    torch = require_cuda()
+    if isinstance(tets, torch.Tensor):
+        td = tets.to(device="cuda", dtype=torch.int64).contiguous()
+    else:
+        td = torch.from_numpy(np.ascontiguousarray(tets, dtype=np.int64).reshape(-1, 4)).cuda()
+    h = C.c_void_p()
+    nt, ne, nv, nbad = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
+    _lib.check(_lib.lib().ibf_surface_extract(td.shape[0] if td.numel() else 0, _lib.dev_ptr(td), C.byref(h),
+                                              C.byref(nt), C.byref(ne), C.byref(nv), C.byref(nbad), _lib.stream()),
+               "ibf_surface_extract")
+    try:
+        tris = np.empty((nt.value, 3), dtype=np.int64)
+        edges = np.empty((ne.value, 2), dtype=np.int64)
+        verts = np.empty(nv.value, dtype=np.int64)
+        _lib.check(_lib.lib().ibf_surface_get(h, _lib.host_ptr(tris), _lib.host_ptr(edges), _lib.host_ptr(verts),
+                                              _lib.stream()), "ibf_surface_get")
+    finally:
+        _lib.lib().ibf_surface_destroy(h)
+    if nbad.value:
+        log.warning("non-manifold surface: %d edge(s) shared by >2 boundary faces", nbad.value)
+    return tris, edges, verts
+
+
+def extract_surface(mesh: TetMesh):
+    """(surface_tris, surface_edges, surface_verts) recomputed on the device
+    (intact/mesh.py:127-129)."""
+    return extract_surface_arrays(mesh.tets)
+
+
 def build_tet_mesh(positions, tets) -> TetMesh:
     """Validate, re-orient negative tets, extract the surface."""
     positions = np.ascontiguousarray(positions, dtype=np.float64)

@@ -372,8 +372,55 @@ def gen_friction(rng):
     save("friction.npz", **out)
 
 
+def _surface_meshes(rng):
+    """Tet sets for surface extraction: a box, a sphere, two bodies in one
+    index space, a random ragged subset (holes, non-manifold edges), one tet,
+    and tets in shuffled order."""
+    from intact.primitives import box_mesh, sphere_mesh
+    box = box_mesh(4, 3, 5, size=0.1)
+    sph = sphere_mesh(4, radius=0.3)
+    two = np.vstack([box.tets, sph.tets + box.n_verts])
+    sub = box.tets[rng.random(len(box.tets)) < 0.55]
+    shuffled = box.tets[rng.permutation(len(box.tets))]
+    return [box.tets, sph.tets, two, sub, box.tets[:1], shuffled]
+
+
+def gen_sceneio(rng):
+    """extract_surface_arrays (intact/mesh.py:106-124) on several tet sets, and
+    the exact bytes export_frame (intact/io_utils.py:35-43) writes, with
+    coordinates covering repr's layouts (tiny, huge, integral, negative zero)."""
+    import tempfile
+    from intact.io_utils import export_frame
+    from intact.mesh import extract_surface_arrays
+    from intact.primitives import box_mesh
+    out = {}
+    meshes = _surface_meshes(rng)
+    for c, tets in enumerate(meshes):
+        tris, edges, verts = extract_surface_arrays(tets)
+        out.update({f"tets{c}": tets, f"tris{c}": tris, f"edges{c}": edges, f"verts{c}": verts})
+    out["n_meshes"] = np.array(len(meshes))
+    box = box_mesh(3, 2, 2, size=0.1)
+    x = box.rest_positions + rng.standard_normal(box.rest_positions.shape) * 1e-3
+    special = [0.0, -0.0, 1.0, -2.0, 1e-5, 1e-4, 0.0001234, 123456789012345.6, 1e16, 1e15, 2.5e-300, -1.7e308,
+               0.1, 1 / 3, 5e-324, 1e22, 9007199254740993.0, 1.5]
+    x[:len(special) // 3 * 3].flat[:len(special)] = special[:len(special) // 3 * 3]
+    x = x.reshape(-1, 3)
+    x[-6:] *= 10.0 ** rng.integers(-12, 18, (6, 1))
+    with tempfile.TemporaryDirectory() as d:
+        path = os.path.join(d, "frame.obj")
+        export_frame(x, box.surface_tris, path)
+        with open(path, "rb") as f:
+            data = f.read()
+        export_frame(x, np.zeros((0, 3), np.int64), path)
+        with open(path, "rb") as f:
+            empty = f.read()
+    out.update({"obj_x": x, "obj_tris": box.surface_tris, "obj_bytes": np.frombuffer(data, np.uint8),
+                "obj_empty_bytes": np.frombuffer(empty, np.uint8)})
+    save("sceneio.npz", **out)
+
+
 GENERATORS = ["distance", "accd", "broadphase", "elastic", "sparse", "activeset", "trajectory", "intersect",
-              "friction"]
+              "friction", "sceneio"]
 
 
 def main():
@@ -393,6 +440,7 @@ def main():
     gen_trajectory(np.random.default_rng(SEED + 6))
     gen_intersect(np.random.default_rng(SEED + 7))
     gen_friction(np.random.default_rng(SEED + 8))
+    gen_sceneio(np.random.default_rng(SEED + 9))
 
 
 if __name__ == "__main__":
