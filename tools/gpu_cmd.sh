@@ -1,1 +1,1 @@
-timeout 2700 python tools/press_run.py 106 94 > gpurun_out/press_run2.log 2>&1
+timeout 900 python tools/surface_timing.py > gpurun_out/surface_timing.log 2>&1
