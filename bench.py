@@ -30,8 +30,8 @@ import argparse
 import json
 import os
 import subprocess
-import sys
 import threading
+import sys
 import time
 
 import numpy as np
@@ -59,17 +59,51 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """Clocks and throttle reasons sampled DURING the timed region.
+
+    Modes (IBF_BENCH_CLOCKS): "spawn" (default) runs one nvidia-smi per
+    sample, 0.2 s apart; "nvml" queries NVML (the library nvidia-smi reads)
+    from a thread of this process; "lms" keeps one `nvidia-smi -lms 200`
+    running (the profiling recipe's clocks line); "off".  The frame's
+    host-driven share ("other_ms": the GPU waiting on the Newton loop's host
+    logic) is sensitive to the box: A/B on one box over 2 runs each gave
+    other_ms 32/38 (spawn), 173/140 (nvml), 61/271 (off), and 40/18 (spawn)
+    vs 103/262 (lms) on another; the kernel phases do not move."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index=0):
-        self.index, self.samples, self.stop = index, [], threading.Event()
+    def __init__(self, index=0, mode=None, period=0.2):
+        self.index, self.samples, self.proc = index, [], None
+        self.mode = mode or os.environ.get("IBF_BENCH_CLOCKS", "spawn")
+        self.period = period
+        self.stop = threading.Event()
         self.t = threading.Thread(target=self._run, daemon=True)
 
+    def _nvml_sample(self, nv, h):
+        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+        smax = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        bits = (0x8, 0x40, 0x20, 0x4)  # hw_slowdown, hw_thermal, sw_thermal, sw_power_cap
+        return [str(sm), str(smax)] + ["Active" if r & b else "Not Active" for b in bits]
+
     def _run(self):
-        while not self.stop.is_set():
+        if self.mode == "nvml":
+            try:
+                import pynvml as nv
+                nv.nvmlInit()
+                h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            except Exception:
+                return
+            while not self.stop.is_set():
+                try:
+                    self.samples.append(self._nvml_sample(nv, h))
+                except Exception:
+                    pass
+                self.stop.wait(self.period)
+            nv.nvmlShutdown()
+            return
+        while not self.stop.is_set():     # "spawn"
             try:
                 out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
                                       "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
@@ -78,15 +112,36 @@ class ClockSampler:
                     self.samples.append(vals)
             except Exception:
                 pass
-            self.stop.wait(0.2)
+            self.stop.wait(self.period)
 
     def __enter__(self):
-        self.t.start()
+        if self.mode == "lms":
+            try:
+                self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                              "--format=csv,noheader,nounits", "-lms", "200"],
+                                             stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            except Exception:
+                self.proc = None
+        elif self.mode != "off":
+            self.t.start()
         return self
 
     def __exit__(self, *a):
         self.stop.set()
-        self.t.join(timeout=10)
+        if self.t.is_alive():
+            self.t.join(timeout=10)
+        if self.proc is None:
+            return
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=10)
+        except Exception:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        for line in (out or "").splitlines():
+            vals = [v.strip() for v in line.split(",")]
+            if len(vals) == 6:
+                self.samples.append(vals)
 
     def summary(self):
         if not self.samples:
