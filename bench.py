@@ -305,7 +305,7 @@ def run_ours(args):
     v_dev = torch.empty_like(v)
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
     newton = cg = passes = 0
-    n_constraints = []
+    n_constraints, pass_ms = [], []
     cert = []
     mon_launches = 0
     launches0 = L.ibf_launch_count()
@@ -339,6 +339,7 @@ def run_ours(args):
             cg += sum(r.cg_iters for r in diag.iterations)
             passes += len(diag.iterations)
             n_constraints.append(max(r.n_constraints for r in diag.iterations))
+            pass_ms.append(max(r.wall_ms for r in diag.iterations))
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
     launches = L.ibf_launch_count() - launches0 - mon_launches
@@ -395,7 +396,8 @@ def run_ours(args):
             "spmv_GBps": achieved,
             "e2e": {"value": e2e, "unit": "ms/frame", "h2d_bytes_per_step": 2 * 24 * n,
                     "d2h_bytes_per_step": 2 * 24 * n},
-            "gpu_launches": int(launches), "wall_s": wall, "setup_s": setup_s,
+            "gpu_launches": int(launches), "frames_ms": [round(t, 1) for t in frame_ms],
+            "slowest_pass_wall_ms": [round(t, 1) for t in pass_ms], "wall_s": wall, "setup_s": setup_s,
             "penetration_free": {"frames_checked": len(cert),
                                  "min_distance": min(c[0] for c in cert) if cert else None,
                                  "intersecting_triangle_pairs": max(c[1] for c in cert) if cert else None,

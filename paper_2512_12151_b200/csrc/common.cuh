@@ -90,6 +90,22 @@ struct Trace {
 
 // Growable device buffer owned by a handle.  Never shrinks; growth only
 // happens outside the timed hot loop once capacities settle.
+// IBF_ALLOC_LOG=1: report (re)allocations slower than 1 ms (dev aid)
+bool alloc_log();
+double wall_now();
+void alloc_report(const char* what, size_t bytes, double t0);
+
+// Device memory of the handles' growable buffers comes from the device's
+// stream-ordered pool, with the release threshold raised so freed blocks stay
+// mapped for reuse.  Plain cudaMalloc / cudaFree inside the Newton loop (a
+// buffer outgrowing its capacity mid-press) measured 2-800 ms per call on the
+// B200 boxes, stalling the whole frame; the pool path is microseconds.
+// Semantics are kept: dev_free waits for the device like cudaFree, and
+// dev_alloc returns memory usable on any stream.
+int dev_alloc(void** p, size_t bytes);
+void dev_free(void* p);
+
+// Growable device buffer owned by a handle.  Never shrinks.
 template <typename T>
 struct DevBuf {
   T* p = nullptr;
@@ -97,26 +113,30 @@ struct DevBuf {
   int reserve(size_t n) {
     if (n <= cap) return IBF_OK;
     size_t want = n + n / 4 + 64;
-    if (p) cudaFree(p);
+    const double t0 = alloc_log() ? wall_now() : 0.0;
+    if (p) dev_free(p);
     p = nullptr;
     cap = 0;
-    IBF_CUDA(cudaMalloc(&p, want * sizeof(T)));
+    IBF_TRY(dev_alloc((void**)&p, want * sizeof(T)));
     cap = want;
+    if (t0 > 0.0) alloc_report("reserve", want * sizeof(T), t0);
     return IBF_OK;
   }
   // grow preserving contents (stream-ordered copy)
   int grow_keep(size_t n, size_t used, cudaStream_t s) {
     if (n <= cap) return IBF_OK;
     size_t want = n + n / 2 + 64;
+    const double t0 = alloc_log() ? wall_now() : 0.0;
     T* q = nullptr;
-    IBF_CUDA(cudaMalloc(&q, want * sizeof(T)));
+    IBF_TRY(dev_alloc((void**)&q, want * sizeof(T)));
     if (p && used) IBF_CUDA(cudaMemcpyAsync(q, p, used * sizeof(T), cudaMemcpyDeviceToDevice, s));
     if (p) {
       IBF_CUDA(cudaStreamSynchronize(s));
-      cudaFree(p);
+      dev_free(p);
     }
     p = q;
     cap = want;
+    if (t0 > 0.0) alloc_report("grow_keep", want * sizeof(T), t0);
     return IBF_OK;
   }
   int upload(const T* host, size_t n, cudaStream_t s = 0) {
@@ -125,7 +145,7 @@ struct DevBuf {
     return IBF_OK;
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p) dev_free(p);
     p = nullptr;
     cap = 0;
   }

@@ -32,6 +32,44 @@ static int trace_level() {
   return lvl;
 }
 bool trace_enabled() { return trace_level() > 0; }
+bool alloc_log() {
+  static int on = -1;
+  if (on < 0) on = getenv("IBF_ALLOC_LOG") ? atoi(getenv("IBF_ALLOC_LOG")) : 0;
+  return on > 0;
+}
+double wall_now() {
+  timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return ts.tv_sec + 1e-9 * ts.tv_nsec;
+}
+int dev_alloc(void** p, size_t bytes) {
+  static std::atomic<unsigned> pools_ready{0};   // bit per device
+  int dev = 0;
+  IBF_CUDA(cudaGetDevice(&dev));
+  if (dev < 32 && !(pools_ready.load() & (1u << dev))) {
+    cudaMemPool_t pool;
+    IBF_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+    uint64_t keep = UINT64_MAX;
+    IBF_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    pools_ready.fetch_or(1u << dev);
+  }
+  // legacy default stream: ordered after prior work on blocking streams; the
+  // sync makes the block usable from any (non-blocking) stream at once
+  IBF_CUDA(cudaMallocAsync(p, bytes, 0));
+  IBF_CUDA(cudaStreamSynchronize(0));
+  return IBF_OK;
+}
+
+void dev_free(void* p) {
+  // the old buffer may still be read by queued kernels on any stream
+  cudaDeviceSynchronize();
+  cudaFreeAsync(p, 0);
+}
+
+void alloc_report(const char* what, size_t bytes, double t0) {
+  const double ms = 1e3 * (wall_now() - t0);
+  if (ms > 1.0) fprintf(stderr, "[ibf] slow %s: %.1f ms for %zu bytes\n", what, ms, bytes);
+}
 static double now_s() {
   timespec ts;
   clock_gettime(CLOCK_MONOTONIC, &ts);
