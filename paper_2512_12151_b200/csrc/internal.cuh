@@ -133,6 +133,7 @@ struct PcgWork {
   DevBuf<unsigned long long> prof;   // IBF_PCG_PROFILE builds only
   DevBuf<int> counter;               // dynamic phase-A chunk counters
   DevBuf<double> part_chunk;         // dynamic phase-A per-chunk partials
+  DevBuf<unsigned> ready;            // term-dot ready counter
   int grid = 0;
   int n_alloc = -1;
 };

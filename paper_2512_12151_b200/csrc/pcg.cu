@@ -71,6 +71,10 @@ constexpr int PCG_THREADS = IBF_PCG_THREADS;
 #define IBF_PCG_SMEM_KB 20
 #endif
 constexpr int PCG_SMEM_BYTES = IBF_PCG_SMEM_KB * 1024;
+// matrix-free term dots behind a ready counter instead of a grid barrier
+#ifndef IBF_PCG_READY
+#define IBF_PCG_READY 1
+#endif
 
 // ---------------------------------------------------------------- gathers
 
@@ -123,6 +127,20 @@ struct DirGather {
 // ---------------------------------------------------------------- SpMV pieces
 
 // t_c = coef_c * sum_slot g_c[slot] . p[v(slot)], masked columns excluded.
+// Ready counter for the term dots (k_pcg): each CTA that computes term dots
+// adds 1 to a global counter once all its dots are stored, and a row that
+// touches terms waits once, just before its term loop, until the counter
+// reaches this iteration's target — a barrier only for the rows that need
+// it, at the end of their SpMV work, instead of a grid barrier before it.
+__device__ __forceinline__ void wait_count(const unsigned* p, unsigned target) {
+  unsigned x;
+  while (true) {
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(x) : "l"(p) : "memory");
+    if ((int)(x - target) >= 0) break;
+    __nanosleep(32);
+  }
+}
+
 template <class Gather>
 __device__ __forceinline__ void contact_dot(const Operator& op, const Gather& gp, int c) {
   const ContactView& cv = op.contact;
@@ -163,13 +181,39 @@ __device__ __forceinline__ void friction_dot(const Operator& op, const Gather& g
   t[2] = H[6] * a0 + H[7] * a1 + H[8] * a2;
 }
 
-// the matrix-free terms' per-term dots (contact and friction) over this CTA's share
+// the matrix-free terms' per-term dots (contact and friction) over this thread's share
 template <class Gather>
 __device__ __forceinline__ void term_dots(const Operator& op, const Gather& gp) {
   const int S = gridDim.x * blockDim.x;
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < op.contact.n; c += S) contact_dot(op, gp, c);
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < op.friction.n; k += S) friction_dot(op, gp, k);
 }
+
+// Where row_product reads the terms' dots: after a grid barrier ...
+struct StoredTerms {
+  __device__ __forceinline__ void ready() const {}
+  __device__ __forceinline__ double contact(const ContactView& cv, int c) const { return cv.t[c]; }
+  __device__ __forceinline__ void friction(const FrictionView& fv, int k, double t[3]) const {
+    const double* T = fv.t + 3 * (size_t)k;
+    t[0] = T[0];
+    t[1] = T[1];
+    t[2] = T[2];
+  }
+};
+// ... or after this row's wait on the ready counter (L2 reads: another SM
+// wrote them after this one's L1 may have cached the previous iteration's)
+struct CountedTerms {
+  const unsigned* counter;
+  unsigned target;
+  __device__ __forceinline__ void ready() const { wait_count(counter, target); }
+  __device__ __forceinline__ double contact(const ContactView& cv, int c) const { return __ldcg(cv.t + c); }
+  __device__ __forceinline__ void friction(const FrictionView& fv, int k, double t[3]) const {
+    const double* T = fv.t + 3 * (size_t)k;
+    t[0] = __ldcg(T);
+    t[1] = __ldcg(T + 1);
+    t[2] = __ldcg(T + 2);
+  }
+};
 
 // one upper block: a_r += (b[3r] x0 + b[3r+1] x1) + b[3r+2] x2
 __device__ __forceinline__ void acc_upper(const double b[9], double x0, double x1, double x2, double& a0, double& a1,
@@ -193,8 +237,9 @@ __device__ __forceinline__ void acc_lower(const double b[9], double x0, double x
 // row's blocks in storage order.  Two slots are in flight per iteration
 // (18 matrix entries, 2 indices, 6 p entries): the product is latency-bound
 // otherwise.
-template <class Gather>
-__device__ __forceinline__ void row_product(const Operator& op, const Gather& gp, int i, double y[3]) {
+template <class Gather, class Terms = StoredTerms>
+__device__ __forceinline__ void row_product(const Operator& op, const Gather& gp, int i, double y[3],
+                                            const Terms& terms = Terms()) {
   const int s = i >> 5, lane = i & 31;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
   {
@@ -274,10 +319,11 @@ __device__ __forceinline__ void row_product(const Operator& op, const Gather& gp
   if (op.contact.n && !(op.mask && op.mask[i])) {
     const ContactView& cv = op.contact;
     const int e0 = cv.vc_ptr[i], e1 = cv.vc_ptr[i + 1];
+    if (e0 < e1) terms.ready();
     for (int e = e0; e < e1; ++e) {
       const int src = cv.vc_src[e];
       const int c = src >> 2, slot = src & 3;
-      const double t = cv.t[c];
+      const double t = terms.contact(cv, c);
       const double* g = cv.grad + 12 * c + 3 * slot;
       a0 += t * g[0];
       a1 += t * g[1];
@@ -286,10 +332,12 @@ __device__ __forceinline__ void row_product(const Operator& op, const Gather& gp
   }
   if (op.friction.n && !(op.mask && op.mask[i])) {
     const FrictionView& fv = op.friction;
+    if (fv.vf_ptr[i] < fv.vf_ptr[i + 1]) terms.ready();
     for (int e = fv.vf_ptr[i]; e < fv.vf_ptr[i + 1]; ++e) {
       const int src = fv.vf_src[e];
       const double w = fv.w[src];
-      const double* t = fv.t + 3 * (size_t)(src >> 2);
+      double t[3];
+      terms.friction(fv, src >> 2, t);
       a0 += w * t[0];
       a1 += w * t[1];
       a2 += w * t[2];
@@ -495,6 +543,8 @@ struct PcgArgs {
   int rows_per_thread;  // ceil(n / (grid * block))
   int smem_rows;        // rows_per_thread if the carry lives in shared memory, else 0
   int carry_qp;         // with smem_rows: 1 carries r, q and p; 0 carries r only
+  unsigned* ready;      // term-dot ready counter, or null: grid barrier after the dots
+  unsigned n_home;      // CTAs that compute term dots (each adds 1 per iteration)
 };
 
 // all CTAs compute the same fixed-order total of part[slot*G .. slot*G+G)
@@ -605,10 +655,32 @@ __global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
       const DirGather gd{a.z, a.p[pb ^ 1], beta, first};
       double* pk = a.p[pb];
       PCG_PT(5)
-      // ---- A: contact dots on p_k, then q = H p_k, pAp
+      // ---- A: contact dots on p_k, then q = H p_k, pAp.  With the ready
+      // counter, the CTAs holding term dots compute them first and count
+      // themselves in; rows touching terms wait for the count just before
+      // their term loop, instead of every CTA waiting at a grid barrier.
+      const bool counted = a.ready != nullptr;
+      const CountedTerms sterms{a.ready, (unsigned)it * a.n_home};
+      auto product = [&](int i, double v[3]) {
+        if (counted)
+          row_product(op, gd, i, v, sterms);
+        else
+          row_product(op, gd, i, v);
+      };
       if (op.contact.n || op.friction.n) {
-        term_dots(op, gd);
-        grid.sync();
+        if (counted) {
+          if (blockIdx.x < a.n_home) {
+            term_dots(op, gd);
+            __syncthreads();
+            if (threadIdx.x == 0) {
+              __threadfence();
+              atomicAdd(a.ready, 1u);
+            }
+          }
+        } else {
+          term_dots(op, gd);
+          grid.sync();
+        }
       }
       PCG_PT(0)
       double pap;
@@ -631,7 +703,7 @@ __global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
           double accc = 0.0;
           if (i < n) {
             double v[3], pv[3];
-            row_product(op, gd, i, v);
+            product(i, v);
             gd.get(i, pv[0], pv[1], pv[2]);
             double* pki = pk + 3 * (size_t)i;
             pki[0] = pv[0]; pki[1] = pv[1]; pki[2] = pv[2];
@@ -658,7 +730,7 @@ __global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
           const int i = row_of(k);
           if (i >= n) break;
           double v[3], pv[3];
-          row_product(op, gd, i, v);
+          product(i, v);
           const double* Z = a.z + 3 * (size_t)i;
           if (first) {
             pv[0] = Z[0]; pv[1] = Z[1]; pv[2] = Z[2];
@@ -934,6 +1006,14 @@ int pcg_solve(const Operator& op, const double* rhs, double* x_out, double rel_t
     IBF_TRY(w.part_chunk.reserve(a.n_chunks));
     a.counter = w.counter.p;
     a.part_chunk = w.part_chunk.p;
+  }
+  a.ready = nullptr;
+  a.n_home = 0;
+  if (IBF_PCG_READY && (op.contact.n || op.friction.n)) {
+    IBF_TRY(w.ready.reserve(1));
+    IBF_CUDA(cudaMemsetAsync(w.ready.p, 0, sizeof(unsigned), s));
+    a.ready = w.ready.p;
+    a.n_home = (unsigned)std::min<int64_t>(sh.grid, div_up(std::max(op.contact.n, op.friction.n), sh.threads));
   }
   a.prof = nullptr;
   if (IBF_PCG_PROFILE) {
