@@ -71,6 +71,10 @@ constexpr int PCG_THREADS = IBF_PCG_THREADS;
 #define IBF_PCG_SMEM_KB 20
 #endif
 constexpr int PCG_SMEM_BYTES = IBF_PCG_SMEM_KB * 1024;
+// phase B's barrier split around the x update
+#ifndef IBF_PCG_SPLIT_BAR
+#define IBF_PCG_SPLIT_BAR 1
+#endif
 // matrix-free term dots behind a ready counter instead of a grid barrier
 #ifndef IBF_PCG_READY
 #define IBF_PCG_READY 1
@@ -544,6 +548,7 @@ struct PcgArgs {
   int smem_rows;        // rows_per_thread if the carry lives in shared memory, else 0
   int carry_qp;         // with smem_rows: 1 carries r, q and p; 0 carries r only
   unsigned* ready;      // term-dot ready counter, or null: grid barrier after the dots
+  unsigned* bar;        // split-barrier arrival counter (phase B), or null: grid barrier
   unsigned n_home;      // CTAs that compute term dots (each adds 1 per iteration)
 };
 
@@ -646,6 +651,7 @@ __global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
   double rel = 0.0;
   double beta = 0.0;
   bool first = true;   // p_k = z (first iteration and after a restart)
+  unsigned bar_epoch = 0;  // split barriers passed
   int pb = 0;          // p[pb] receives p_k
   if (bnorm == 0.0) {
     conv = true;
@@ -775,6 +781,7 @@ __global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
       double* xn = Xb(nxt);
       double acc_rr = 0.0;
       acc_rz = 0.0;
+      const bool split = a.bar != nullptr && !qp_smem;
       for (int k = 0; k < R; ++k) {
         const int i = row_of(k);
         if (i >= n) break;
@@ -785,14 +792,13 @@ __global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
             pv[c] = sp[slot(k, c)];
           }
         } else {
-          for (int c = 0; c < 3; ++c) {
-            qv[c] = a.hp[3 * (size_t)i + c];
-            pv[c] = pk[3 * (size_t)i + c];
-          }
+          for (int c = 0; c < 3; ++c) qv[c] = a.hp[3 * (size_t)i + c];
+          if (!split)
+            for (int c = 0; c < 3; ++c) pv[c] = pk[3 * (size_t)i + c];
         }
         for (int c = 0; c < 3; ++c) {
           const size_t e = 3 * (size_t)i + c;
-          xn[e] = xc[e] + alpha * pv[c];
+          if (!split) xn[e] = xc[e] + alpha * pv[c];
           double& rr = r_ref(k, i, c);
           rv[c] = rr - alpha * qv[c];
           rr = rv[c];
@@ -806,7 +812,29 @@ __global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
       PCG_PT(3)
       put_partials(a.part, 0, acc_rr, red);
       put_partials(a.part, 1, acc_rz, red);
-      grid.sync();
+      if (split) {
+        // split barrier: arrive, update x (which nothing reads before the
+        // next own-row update, a restart or the end, each behind a full
+        // barrier), then wait — the x stream hides the barrier latency
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          __threadfence();
+          atomicAdd(a.bar, 1u);
+        }
+        for (int k = 0; k < R; ++k) {
+          const int i = row_of(k);
+          if (i >= n) break;
+          for (int c = 0; c < 3; ++c) {
+            const size_t e = 3 * (size_t)i + c;
+            xn[e] = xc[e] + alpha * pk[e];
+          }
+        }
+        ++bar_epoch;
+        if (threadIdx.x == 0) wait_count(a.bar, bar_epoch * gridDim.x);
+        __syncthreads();
+      } else {
+        grid.sync();
+      }
       const double res = sqrt(grid_total(a.part, 0, bc));
       PCG_PT(4)
       cur = nxt;
@@ -824,6 +852,7 @@ __global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
       }
       if (it % 250 == 0) {
         // restart from the true residual r = b - H x
+        if (a.bar) grid.sync();   // x of other rows: updated after the split barrier's arrive
         const PlainGather gx{Xb(cur)};
         if (op.contact.n || op.friction.n) {
           term_dots(op, gx);
@@ -866,6 +895,7 @@ __global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
       rel = best_res / bnorm;
     }
   }
+  if (a.bar) grid.sync();   // the last x update ran after the split barrier's arrive
   const double* xr = Xb(result);
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < 3LL * n; k += S)
     a.x_out[k] = (bnorm == 0.0) ? 0.0 : xr[k];
@@ -1009,9 +1039,10 @@ int pcg_solve(const Operator& op, const double* rhs, double* x_out, double rel_t
   }
   a.ready = nullptr;
   a.n_home = 0;
+  IBF_TRY(w.ready.reserve(2));
+  IBF_CUDA(cudaMemsetAsync(w.ready.p, 0, 2 * sizeof(unsigned), s));
+  a.bar = IBF_PCG_SPLIT_BAR ? w.ready.p + 1 : nullptr;
   if (IBF_PCG_READY && (op.contact.n || op.friction.n)) {
-    IBF_TRY(w.ready.reserve(1));
-    IBF_CUDA(cudaMemsetAsync(w.ready.p, 0, sizeof(unsigned), s));
     a.ready = w.ready.p;
     a.n_home = (unsigned)std::min<int64_t>(sh.grid, div_up(std::max(op.contact.n, op.friction.n), sh.threads));
   }
