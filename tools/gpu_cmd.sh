@@ -1,1 +1,2 @@
-for c in 1 8; do timeout 900 python bench.py --workload c5 --concurrency $c --steps 5 --warmup 3 > gpurun_out/c5_$c.json 2> gpurun_out/c5_$c.err; done
+IBF_LIB=tools/variants/libibf_spread.so timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/sp_tests.log 2>&1
+for v in nospread spread nospread spread; do IBF_LIB=tools/variants/libibf_$v.so timeout 900 python bench.py --steps 5 --warmup 3 --no-cpu-baseline >> gpurun_out/bench_sp_all.jsonl 2> gpurun_out/bench_$v.err; done
