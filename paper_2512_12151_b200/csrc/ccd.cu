@@ -374,42 +374,77 @@ static int grid_for(int64_t n, int threads = 256) {
 }
 
 // Build the LBVH over n primitive boxes (c->box_lo/hi) into c's node arrays.
-static int build_tree(ibf_ccd* c, int64_t n, cudaStream_t s, Tree& t) {
-  const int nparts = (int)std::min<int64_t>(grid_for(n), 148 * 2);
-  IBF_TRY(c->dscratch.reserve(6 * (size_t)nparts + 8));
-  IBF_TRY(c->keys.reserve(n));
-  IBF_TRY(c->keys_sorted.reserve(n));
+// LBVH over the n boxes in c->box_lo/hi (Karras split on sorted Morton keys,
+// bottom-up refit).  cache != null: reuse its topology when it was built for
+// the same n fewer than IBF_CCD_REBUILD calls ago, refitting only — the
+// refit bounds are exact unions of the current leaf boxes, so traversal
+// returns the same overlapping pairs; only the tree's tightness ages.
+#ifndef IBF_CCD_REBUILD
+#define IBF_CCD_REBUILD 16
+#endif
+static int build_tree(ibf_ccd* c, int64_t n, cudaStream_t s, Tree& t, ibf_ccd::TreeCache* cache = nullptr) {
   const int64_t nn = std::max<int64_t>(2 * n - 1, 1);
-  IBF_TRY(c->node_left.reserve(nn));
-  IBF_TRY(c->node_right.reserve(nn));
-  IBF_TRY(c->node_parent.reserve(nn));
-  IBF_TRY(c->node_flag.reserve(nn));
-  IBF_TRY(c->node_lo.reserve(3 * nn));
-  IBF_TRY(c->node_hi.reserve(3 * nn));
-  k_bounds<<<nparts, 256, 0, s>>>(n, c->box_lo.p, c->box_hi.p, c->dscratch.p);
-  IBF_LAUNCH_CHECK();
-  k_morton<<<grid_for(n), 256, 0, s>>>(n, c->box_lo.p, c->box_hi.p, c->dscratch.p, nparts, c->keys.p);
-  IBF_LAUNCH_CHECK();
-  size_t need = 0;
-  cub::DeviceRadixSort::SortKeys(nullptr, need, c->keys.p, c->keys_sorted.p, (int)n, 0, 64, s);
-  IBF_TRY(c->cub_tmp.reserve(need + 16));
-  size_t have = c->cub_tmp.cap;
-  IBF_CUDA(cub::DeviceRadixSort::SortKeys(c->cub_tmp.p, have, c->keys.p, c->keys_sorted.p, (int)n, 0, 64, s));
-  if (n > 1) {
-    k_build<<<grid_for(n - 1), 256, 0, s>>>((int)n, c->keys_sorted.p, c->node_left.p, c->node_right.p,
-                                             c->node_parent.p);
-    IBF_LAUNCH_CHECK();
+  unsigned long long* keys_sorted = c->keys_sorted.p;
+  int *left, *right, *parent, *flag;
+  double *lo, *hi;
+  bool refit_only = false;
+  if (cache) {
+    IBF_TRY(cache->keys_sorted.reserve(n));
+    IBF_TRY(cache->left.reserve(nn));
+    IBF_TRY(cache->right.reserve(nn));
+    IBF_TRY(cache->parent.reserve(nn));
+    IBF_TRY(cache->flag.reserve(nn));
+    IBF_TRY(cache->lo.reserve(3 * nn));
+    IBF_TRY(cache->hi.reserve(3 * nn));
+    refit_only = cache->n == n && cache->uses < IBF_CCD_REBUILD;
+    keys_sorted = cache->keys_sorted.p;
+    left = cache->left.p, right = cache->right.p, parent = cache->parent.p, flag = cache->flag.p;
+    lo = cache->lo.p, hi = cache->hi.p;
+  } else {
+    IBF_TRY(c->keys_sorted.reserve(n));
+    IBF_TRY(c->node_left.reserve(nn));
+    IBF_TRY(c->node_right.reserve(nn));
+    IBF_TRY(c->node_parent.reserve(nn));
+    IBF_TRY(c->node_flag.reserve(nn));
+    IBF_TRY(c->node_lo.reserve(3 * nn));
+    IBF_TRY(c->node_hi.reserve(3 * nn));
+    keys_sorted = c->keys_sorted.p;
+    left = c->node_left.p, right = c->node_right.p, parent = c->node_parent.p, flag = c->node_flag.p;
+    lo = c->node_lo.p, hi = c->node_hi.p;
   }
-  IBF_CUDA(cudaMemsetAsync(c->node_flag.p, 0, nn * sizeof(int), s));
-  k_refit<<<grid_for(n), 256, 0, s>>>((int)n, c->keys_sorted.p, c->box_lo.p, c->box_hi.p, c->node_left.p,
-                                       c->node_right.p, c->node_parent.p, c->node_flag.p, c->node_lo.p, c->node_hi.p);
+  if (!refit_only) {
+    const int nparts = (int)std::min<int64_t>(grid_for(n), 148 * 2);
+    IBF_TRY(c->dscratch.reserve(6 * (size_t)nparts + 8));
+    IBF_TRY(c->keys.reserve(n));
+    k_bounds<<<nparts, 256, 0, s>>>(n, c->box_lo.p, c->box_hi.p, c->dscratch.p);
+    IBF_LAUNCH_CHECK();
+    k_morton<<<grid_for(n), 256, 0, s>>>(n, c->box_lo.p, c->box_hi.p, c->dscratch.p, nparts, c->keys.p);
+    IBF_LAUNCH_CHECK();
+    size_t need = 0;
+    cub::DeviceRadixSort::SortKeys(nullptr, need, c->keys.p, keys_sorted, (int)n, 0, 64, s);
+    IBF_TRY(c->cub_tmp.reserve(need + 16));
+    size_t have = c->cub_tmp.cap;
+    IBF_CUDA(cub::DeviceRadixSort::SortKeys(c->cub_tmp.p, have, c->keys.p, keys_sorted, (int)n, 0, 64, s));
+    if (n > 1) {
+      k_build<<<grid_for(n - 1), 256, 0, s>>>((int)n, keys_sorted, left, right, parent);
+      IBF_LAUNCH_CHECK();
+    }
+    if (cache) {
+      cache->n = n;
+      cache->uses = 0;
+    }
+  }
+  if (cache) ++cache->uses;
+  IBF_CUDA(cudaMemsetAsync(flag, 0, nn * sizeof(int), s));
+  k_refit<<<grid_for(n), 256, 0, s>>>((int)n, keys_sorted, c->box_lo.p, c->box_hi.p, left, right, parent, flag, lo,
+                                       hi);
   IBF_LAUNCH_CHECK();
   t.n = (int)n;
-  t.keys = c->keys_sorted.p;
-  t.left = c->node_left.p;
-  t.right = c->node_right.p;
-  t.lo = c->node_lo.p;
-  t.hi = c->node_hi.p;
+  t.keys = keys_sorted;
+  t.left = left;
+  t.right = right;
+  t.lo = lo;
+  t.hi = hi;
   return IBF_OK;
 }
 
@@ -447,7 +482,7 @@ static int broad_pass(ibf_ccd* c, int kind, const double* x0, const double* x1, 
   }
   tr.mark("boxes", s, nt);
   Tree tree;
-  IBF_TRY(build_tree(c, nt, s, tree));
+  IBF_TRY(build_tree(c, nt, s, tree, (kind < 2 && IBF_CCD_REBUILD > 1) ? &c->tc[kind] : nullptr));
   tr.mark("tree", s);
   IBF_TRY(c->counters.reserve(4));
   IBF_TRY(c->host.reserve(64));

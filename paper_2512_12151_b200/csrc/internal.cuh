@@ -203,6 +203,15 @@ struct ibf_ccd {
   ibf::DevBuf<int> order;                               // sorted primitive order
   ibf::DevBuf<int> node_left, node_right, node_parent, node_flag;
   ibf::DevBuf<double> node_lo, node_hi;
+  // VF (triangle) and EE (edge) trees kept between calls: later calls refit
+  // the cached topology to the new boxes; it is rebuilt every few calls
+  struct TreeCache {
+    ibf::DevBuf<unsigned long long> keys_sorted;
+    ibf::DevBuf<int> left, right, parent, flag;
+    ibf::DevBuf<double> lo, hi;
+    int64_t n = -1;
+    int uses = 0;
+  } tc[2];
   ibf::DevBuf<unsigned char> cub_tmp;
   // candidate / survivor pairs
   ibf::DevBuf<unsigned long long> pairs, pairs_sorted;
