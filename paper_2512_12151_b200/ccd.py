@@ -52,9 +52,12 @@ class CCD:
 
     def __del__(self):
         h = getattr(self, "handle", None)
-        if h and _lib._lib is not None:
-            _lib.lib().ibf_ccd_destroy(h)
-            self.handle = None
+        try:
+            if h and _lib._lib is not None:
+                _lib.lib().ibf_ccd_destroy(h)
+                self.handle = None
+        except (AttributeError, TypeError):
+            pass  # interpreter shutdown: module globals already cleared
 
     def max_step_size(self, x_dev, x_hat_dev, min_gap, cap=1.0):
         """alpha on the host; blocking pairs stay on the device."""

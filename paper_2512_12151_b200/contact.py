@@ -68,9 +68,12 @@ class ActiveSet:
 
     def __del__(self):
         h = getattr(self, "handle", None)
-        if h and _lib._lib is not None:
-            _lib.lib().ibf_contacts_destroy(h)
-            self.handle = None
+        try:
+            if h and _lib._lib is not None:
+                _lib.lib().ibf_contacts_destroy(h)
+                self.handle = None
+        except (AttributeError, TypeError):
+            pass  # interpreter shutdown: module globals already cleared
 
     # -- handle management: the reference's ActiveSet() does not know N
     def ensure(self, n_verts: int):

@@ -29,9 +29,12 @@ class FrictionTerms:
 
     def __del__(self):
         h = getattr(self, "handle", None)
-        if h and _lib._lib is not None:
-            _lib.lib().ibf_friction_destroy(h)
-            self.handle = None
+        try:
+            if h and _lib._lib is not None:
+                _lib.lib().ibf_friction_destroy(h)
+                self.handle = None
+        except (AttributeError, TypeError):
+            pass  # interpreter shutdown: module globals already cleared
 
     def __len__(self) -> int:
         return int(_lib.lib().ibf_friction_size(self.handle))

@@ -83,9 +83,12 @@ class DeviceSystem:
 
     def __del__(self):
         h = getattr(self, "handle", None)
-        if h and _lib._lib is not None:
-            _lib.lib().ibf_system_destroy(h)
-            self.handle = None
+        try:
+            if h and _lib._lib is not None:
+                _lib.lib().ibf_system_destroy(h)
+                self.handle = None
+        except (AttributeError, TypeError):
+            pass  # interpreter shutdown: module globals already cleared
 
     # ---- device-tensor entry points (used by the stepper)
     def solve_subproblem(self, aset: ActiveSet | None, x_tilde, x, x_hat, mu, offset, h, cg_tol, decay):

@@ -57,9 +57,12 @@ class BlockSparseMatrix:
 
     def __del__(self):
         h = getattr(self, "handle", None)
-        if h and _lib._lib is not None:
-            _lib.lib().ibf_bsr_destroy(h)
-            self.handle = None
+        try:
+            if h and _lib._lib is not None:
+                _lib.lib().ibf_bsr_destroy(h)
+                self.handle = None
+        except (AttributeError, TypeError):
+            pass  # interpreter shutdown: module globals already cleared
 
     def _sync_host(self):
         nb = int(_lib.lib().ibf_bsr_size(self.handle))
