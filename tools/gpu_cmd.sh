@@ -1,2 +1,2 @@
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_pcg -c 1 -o gpurun_out/pcg_final python tools/bench_spmv.py > gpurun_out/ncu_final.log 2>&1
-timeout 600 ncu --set full --clock-control none -k regex:k_spmv -c 1 -o gpurun_out/spmv_final python tools/bench_spmv.py >> gpurun_out/ncu_final.log 2>&1
+IBF_LIB=tools/variants/libibf_even.so timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/ev_tests.log 2>&1
+for v in noeven even noeven even; do IBF_LIB=tools/variants/libibf_$v.so timeout 900 python bench.py --steps 5 --warmup 3 --no-cpu-baseline >> gpurun_out/bench_ev_all.jsonl 2> gpurun_out/bench_$v.err; done
