@@ -1,3 +1,5 @@
+"""Dev tool: golden box-on-slab trajectory through Simulation, per step: active-set key
+diffs against the reference's keys and the per-pass (alpha, |C|, Newton) records."""
 import sys, os
 sys.path.insert(0, os.getcwd())
 import numpy as np
