@@ -108,6 +108,31 @@ def test_broadphase_large_random(ibf):
         {(int(k), tuple(q), t) for k, q, t in zip(rk, rq.tolist(), rt)}
 
 
+def test_broadphase_refit_across_calls(ibf):
+    """One CCD handle over 40 calls on a drifting, deforming scene: the VF/EE
+    trees are refit between rebuilds (every 16 calls, csrc/ccd.cu), and every
+    call's candidate set and step limit must still equal brute force."""
+    from paper_2512_12151_b200 import ccd, scenes
+    from paper_2512_12151_b200.device import to_dev
+    mesh = scenes.box_mesh(6, 6, 3, size=(0.3, 0.3, 0.1))
+    rng = np.random.default_rng(11)
+    t, e, v = mesh.surface_tris, mesh.surface_edges, mesh.surface_verts
+    h = ccd.CCD(t, e, v)
+    x = mesh.rest_positions + rng.uniform(-0.003, 0.003, mesh.rest_positions.shape)
+    vel = rng.uniform(-0.01, 0.01, x.shape)
+    gap = 2e-3
+    for k in range(40):
+        x1 = x + vel + rng.uniform(-0.002, 0.002, x.shape)
+        vf, ee = h.candidates(to_dev(x), to_dev(x1), gap)
+        rvf, ree = geometry.candidates(x, x1, t, e, v, gap)
+        assert {tuple(q) for q in vf.tolist()} == {tuple(q) for q in rvf.tolist()}, k
+        assert {tuple(q) for q in ee.tolist()} == {tuple(q) for q in ree.tolist()}, k
+        alpha = h.max_step_size(to_dev(x), to_dev(x1), gap)
+        ra, _, _, _ = geometry.step_limit(x, x1, t, e, v, gap)
+        assert alpha == ra, k
+        x = x + 0.5 * (x1 - x)     # drift: the scene moves between calls
+
+
 def test_bsr_coalesce_matvec_pcg(ibf):
     from paper_2512_12151_b200.sparse import BlockSparseMatrix, clique_contributions, pcg_solve
     g = golden("sparse.npz")
