@@ -25,6 +25,9 @@ for cls, name in [(solver.DeviceSystem, "solve_subproblem"), (solver.DeviceSyste
 F = 20
 L = _lib.lib()
 l0 = L.ibf_launch_count()
+import numpy as np
+st = np.zeros(9)
+L.ibf_system_stats(system.device.handle, _lib.host_ptr(st), 1)
 torch.cuda.synchronize(); t0 = time.perf_counter()
 passes = newton = 0
 for _ in range(F):
@@ -36,4 +39,9 @@ out = {"ms_per_frame": 1e3 * wall / F, "passes_per_frame": passes / F, "newton_p
        "ms_per_frame_by_call": {k: round(1e3 * v / F, 3) for k, v in T.items()},
        "calls_per_frame": {k: v / F for k, v in N.items()}}
 out["unaccounted_ms"] = out["ms_per_frame"] - sum(out["ms_per_frame_by_call"].values())
+L.ibf_system_stats(system.device.handle, _lib.host_ptr(st), 0)
+out["pcg_ms_per_frame"] = st[2] / F
+out["cg_iters_per_frame"] = st[4] / F
+out["us_per_cg_iter"] = 1e3 * st[2] / max(st[4], 1)
+out["n_vertices"] = system.n_vertices
 print(json.dumps(out, indent=1))
