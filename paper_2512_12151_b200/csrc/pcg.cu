@@ -75,6 +75,13 @@ constexpr int PCG_SMEM_BYTES = IBF_PCG_SMEM_KB * 1024;
 #ifndef IBF_PCG_SPLIT_BAR
 #define IBF_PCG_SPLIT_BAR 1
 #endif
+// small systems: lanes per row in phase A
+#ifndef IBF_PCG_LANES
+#define IBF_PCG_LANES 4
+#endif
+#ifndef IBF_PCG_LANES_MAX_N
+#define IBF_PCG_LANES_MAX_N 16384
+#endif
 // matrix-free term dots behind a ready counter instead of a grid barrier
 #ifndef IBF_PCG_READY
 #define IBF_PCG_READY 1
@@ -352,6 +359,76 @@ __device__ __forceinline__ void row_product(const Operator& op, const Gather& gp
   y[2] = a2;
 }
 
+// Row i's product split over L lanes of one warp (lane sub takes slots,
+// lower entries and term incidences sub, sub + L, ...); the caller sums the
+// L partial results with shuffles in a fixed order.  For small systems, where
+// a CG iteration is the latency of one row's chain of block loads.
+template <class Gather, class Terms = StoredTerms>
+__device__ __forceinline__ void row_product_lanes(const Operator& op, const Gather& gp, int i, double y[3], int sub,
+                                                  int L, const Terms& terms = Terms()) {
+  const int s = i >> 5, lane = i & 31;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+  {
+    const int q0 = __ldg(op.slice_ptr + s), w = (__ldg(op.slice_ptr + s + 1) - q0) >> 5;
+    const double* V = op.val + 9 * (size_t)q0 + lane;
+    const int* C = op.col + q0 + lane;
+    for (int k = sub; k < w; k += L) {
+      const int j = __ldg(C + 32 * k);
+      const double* B = V + 288 * (size_t)k;
+      double b[9];
+#pragma unroll
+      for (int e = 0; e < 9; ++e) b[e] = __ldg(B + 32 * e);
+      double x0, x1, x2;
+      gp.get(j, x0, x1, x2);
+      acc_upper(b, x0, x1, x2, a0, a1, a2);
+    }
+  }
+  {
+    const int l0 = __ldg(op.low_ptr + s), w = (__ldg(op.low_ptr + s + 1) - l0) >> 5;
+    const int2* Lw = op.low + l0 + lane;
+    for (int t = sub; t < w; t += L) {
+      const int2 le = __ldg(Lw + 32 * t);
+      const double* B = op.val + qel(le.x, 0);
+      double b[9];
+#pragma unroll
+      for (int e = 0; e < 9; ++e) b[e] = __ldg(B + 32 * e);
+      double x0, x1, x2;
+      gp.get(le.y, x0, x1, x2);
+      acc_lower(b, x0, x1, x2, a0, a1, a2);
+    }
+  }
+  if (op.contact.n && !(op.mask && op.mask[i])) {
+    const ContactView& cv = op.contact;
+    const int e0 = cv.vc_ptr[i], e1 = cv.vc_ptr[i + 1];
+    if (e0 + sub < e1) terms.ready();
+    for (int e = e0 + sub; e < e1; e += L) {
+      const int src = cv.vc_src[e];
+      const int c = src >> 2, slot = src & 3;
+      const double t = terms.contact(cv, c);
+      const double* g = cv.grad + 12 * c + 3 * slot;
+      a0 += t * g[0];
+      a1 += t * g[1];
+      a2 += t * g[2];
+    }
+  }
+  if (op.friction.n && !(op.mask && op.mask[i])) {
+    const FrictionView& fv = op.friction;
+    if (fv.vf_ptr[i] + sub < fv.vf_ptr[i + 1]) terms.ready();
+    for (int e = fv.vf_ptr[i] + sub; e < fv.vf_ptr[i + 1]; e += L) {
+      const int src = fv.vf_src[e];
+      const double w = fv.w[src];
+      double t[3];
+      terms.friction(fv, src >> 2, t);
+      a0 += w * t[0];
+      a1 += w * t[1];
+      a2 += w * t[2];
+    }
+  }
+  y[0] = a0;
+  y[1] = a1;
+  y[2] = a2;
+}
+
 __global__ void k_contact_dot(Operator op, const double* __restrict__ p) {
   term_dots(op, PlainGather{p});
 }
@@ -549,6 +626,7 @@ struct PcgArgs {
   int carry_qp;         // with smem_rows: 1 carries r, q and p; 0 carries r only
   unsigned* ready;      // term-dot ready counter, or null: grid barrier after the dots
   unsigned* bar;        // split-barrier arrival counter (phase B), or null: grid barrier
+  int lanes;            // lanes per row in phase A (1: one thread per row)
   unsigned n_home;      // CTAs that compute term dots (each adds 1 per iteration)
 };
 
@@ -732,7 +810,32 @@ __global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
         PCG_PT(2)
       } else {
         double acc = 0.0;
-        for (int k = 0; k < R; ++k) {
+        if (a.lanes > 1) {
+          // small system: L lanes per row; warp-uniform loop for the shuffles
+          const int L = a.lanes, sub = threadIdx.x & (L - 1);
+          for (int base = (blockIdx.x * blockDim.x + (threadIdx.x & ~31)) / L; base < n; base += S / L) {
+            const int i = base + (threadIdx.x & 31) / L;
+            double v[3] = {0.0, 0.0, 0.0};
+            if (i < n) {
+              if (counted)
+                row_product_lanes(op, gd, i, v, sub, L, sterms);
+              else
+                row_product_lanes(op, gd, i, v, sub, L);
+            }
+            for (int o = 1; o < L; o <<= 1)
+              for (int c = 0; c < 3; ++c) v[c] += __shfl_xor_sync(0xffffffffu, v[c], o);
+            if (i < n && sub == 0) {
+              double pv[3];
+              gd.get(i, pv[0], pv[1], pv[2]);
+              double* pki = pk + 3 * (size_t)i;
+              pki[0] = pv[0]; pki[1] = pv[1]; pki[2] = pv[2];
+              double* qi = a.hp + 3 * (size_t)i;
+              qi[0] = v[0]; qi[1] = v[1]; qi[2] = v[2];
+              acc += pv[0] * v[0] + pv[1] * v[1] + pv[2] * v[2];
+            }
+          }
+        }
+        for (int k = 0; k < R && a.lanes == 1; ++k) {
           const int i = row_of(k);
           if (i >= n) break;
           double v[3], pv[3];
@@ -1007,7 +1110,12 @@ int pcg_solve(const Operator& op, const double* rhs, double* x_out, double rel_t
   IBF_TRY(w.hp.reserve(n3));
   IBF_TRY(w.X.reserve(3 * n3));
   IBF_TRY(w.info.reserve(4));
-  const PcgShape sh = pcg_shape(n);
+  const int lanes = (IBF_PCG_LANES > 1 && !IBF_PCG_CARRY_QP && n <= IBF_PCG_LANES_MAX_N) ? IBF_PCG_LANES : 1;
+  PcgShape sh = pcg_shape(n * lanes);   // grid sized for lanes x rows threads
+  if (lanes > 1) {
+    sh.rows_per_thread = (int)div_up(std::max(n, 1), (int64_t)sh.grid * sh.threads);
+    if (sh.smem_rows) sh.smem_rows = sh.rows_per_thread;
+  }
   IBF_TRY(w.part.reserve(4 * (size_t)sh.grid));
   w.grid = sh.grid;
   PcgArgs a;
@@ -1042,6 +1150,7 @@ int pcg_solve(const Operator& op, const double* rhs, double* x_out, double rel_t
   IBF_TRY(w.ready.reserve(2));
   IBF_CUDA(cudaMemsetAsync(w.ready.p, 0, 2 * sizeof(unsigned), s));
   a.bar = IBF_PCG_SPLIT_BAR ? w.ready.p + 1 : nullptr;
+  a.lanes = lanes;
   if (IBF_PCG_READY && (op.contact.n || op.friction.n)) {
     a.ready = w.ready.p;
     a.n_home = (unsigned)std::min<int64_t>(sh.grid, div_up(std::max(op.contact.n, op.friction.n), sh.threads));
