@@ -116,6 +116,38 @@ def test_pcg_sphere_compression(pkg):
     np.testing.assert_allclose(to_host(pd), po, rtol=1e-6, atol=1e-9 * np.abs(po).max())
 
 
+def test_pcg_large_system_matches_oracle(pkg):
+    """A 19.7k-vertex compressed box: above the small-system threshold, so the
+    solve takes the C4 path (one thread per row, residual carried on chip,
+    split phase-B barrier) — iteration count within 1 of the oracle's and the
+    same solution to 1e-6."""
+    from paper_2512_12151_b200 import ElasticRegion, Material, MaterialModel
+    from paper_2512_12151_b200.mesh import build_tet_mesh, compute_rest_data
+    from paper_2512_12151_b200.scenes import cell_tets, grid_points
+    from paper_2512_12151_b200.solver import DeviceSystem
+    from paper_2512_12151_b200.device import to_dev, empty, to_host
+    n = 26
+    mesh = build_tet_mesh(grid_points(n, n, n, 0.5), cell_tets(n, n, n))
+    assert mesh.n_verts > 16384
+    rest = compute_rest_data(mesh, 1000.0)
+    x = mesh.rest_positions * np.array([1.0, 1.0, 0.8])
+    mu_, lam_ = material.lame(1e5, 0.4)
+    go, Ho = newton.assemble(x, x, rest.masses, [("snh", mu_, lam_, mesh.tets, rest.shape_rows, rest.volumes)],
+                             None, 1.0, 0.0, 0.01)
+    po, its, conv, _ = __import__("oracle.blocksparse", fromlist=["pcg"]).pcg(Ho, -go, 1e-4)
+    reg = ElasticRegion(Material(MaterialModel.SNH, 1e5, 0.4), mesh.tets, rest.shape_rows, rest.volumes)
+    dev = DeviceSystem(rest.masses, [reg])
+    xd = to_dev(x)
+    gd = empty(x.shape)
+    dev.assemble(None, xd, xd, 1.0, 0.0, 0.01, False, gd)
+    assert np.abs(to_host(gd) - go).max() <= 1e-9 * np.abs(go).max()
+    pd = empty(x.shape)
+    it_g, conv_g, _ = dev.pcg(-gd, pd, 1e-4)
+    assert conv and conv_g
+    assert abs(it_g - its) <= 1
+    np.testing.assert_allclose(to_host(pd), po, rtol=1e-6, atol=1e-9 * np.abs(po).max())
+
+
 def test_plane_settle_kkt(pkg):
     """tests/test_solver.py:196-227: converged state one offset above the
     plane, |c| contracts geometrically, lambda = 0.3, DBC rows bit-pinned."""
