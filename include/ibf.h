@@ -209,6 +209,15 @@ int ibf_system_matvec(ibf_system* s, const double* x, double* y, ibf_stream st);
 int ibf_system_export_bsr(ibf_system* s, int64_t* rows, int64_t* cols, double* blocks,
                           ibf_stream st);
 
+/* Explicit upper cliques of the last assembly's matrix-free terms, as the
+ * reference's COO (clique_contributions, intact/sparse.py:17-36, of
+ * ConstraintBatch.hessian_grids, intact/contact.py:139-141, then
+ * FrictionTerms.hessian_grids, intact/friction.py:88-100): 10 blocks per term,
+ * unmasked, uncoalesced.  rows == NULL only returns the count in n_blocks;
+ * otherwise rows, cols (n_blocks) and blocks (n_blocks,3,3) are host arrays. */
+int ibf_system_export_terms(ibf_system* s, int64_t* n_blocks, int64_t* rows, int64_t* cols, double* blocks,
+                            ibf_stream st);
+
 /* pcg_solve on the last assembled matrix (intact/sparse.py:99-150).
  * info_host = (iterations, converged, rel_residual). max_iters <= 0 -> 10 n. */
 int ibf_system_pcg(ibf_system* s, const double* rhs, double* x_out, double rel_tol,
@@ -266,6 +275,18 @@ int64_t ibf_bsr_size(const ibf_bsr* m);
 int ibf_bsr_export(const ibf_bsr* m, int64_t* rows, int64_t* cols, double* blocks, ibf_stream st);
 int ibf_bsr_pcg(ibf_bsr* m, const double* rhs, double* x_out, double rel_tol,
                 int64_t max_iters, double* info_host, ibf_stream st);
+
+/* Launch-shape overrides for every subsequent PCG solve in the process
+ * (tuning and tests; no reference counterpart — pcg_solve has no launch
+ * shape, intact/sparse.py:99-150).  lanes_max_n: systems with at most this
+ * many rows give each row 4 lanes of a warp (default 16384; < 0 restores the
+ * default, 0 forces one thread per row).  max_ctas: cap on the cooperative
+ * grid (0: a full co-resident wave), which raises the row sweeps per thread. */
+int ibf_pcg_tuning(int64_t lanes_max_n, int max_ctas);
+/* Shape of the last PCG launch in the process: out[0..5] = CTAs, threads per
+ * CTA, row sweeps per thread, lanes per row, ready counter used (0/1),
+ * matrix-free terms (contacts + friction). */
+int ibf_pcg_last_shape(int64_t* out);
 
 /* Algorithmic bytes of one symmetric SpMV over the elastic pattern
  * (BASELINE.md §4), for the bench's roofline line. */

@@ -85,6 +85,9 @@ _PROTOS = {
     "ibf_ccd_stats": (_int, [_vp, _vp, _int]),
     "ibf_launch_count": (C.c_ulonglong, []),
     "ibf_bsr_export": (_int, [_vp, _vp, _vp, _vp, _vp]),
+    "ibf_pcg_tuning": (_int, [_i64, _int]),
+    "ibf_pcg_last_shape": (_int, [_vp]),
+    "ibf_system_export_terms": (_int, [_vp, _pi64, _vp, _vp, _vp, _vp]),
 }
 
 _lib = None
@@ -140,3 +143,27 @@ def dev_ptr(t):
 def stream():
     import torch
     return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def pcg_last_shape():
+    """(ctas, threads, sweeps per thread, lanes per row, ready counter, terms)
+    of the last PCG launch."""
+    out = np.zeros(6, dtype=np.int64)
+    check(lib().ibf_pcg_last_shape(host_ptr(out)), "ibf_pcg_last_shape")
+    return tuple(int(v) for v in out)
+
+
+class pcg_tuning:
+    """Context manager over ibf_pcg_tuning: PCG launch-shape overrides for
+    the solves inside the block (lanes_max_n 0 forces one thread per row;
+    max_ctas caps the cooperative grid so each thread sweeps several rows)."""
+
+    def __init__(self, lanes_max_n=-1, max_ctas=0):
+        self.args = (int(lanes_max_n), int(max_ctas))
+
+    def __enter__(self):
+        check(lib().ibf_pcg_tuning(*self.args), "ibf_pcg_tuning")
+        return self
+
+    def __exit__(self, *exc):
+        lib().ibf_pcg_tuning(-1, 0)

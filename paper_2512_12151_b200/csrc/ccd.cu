@@ -542,6 +542,7 @@ using namespace ibf;
 
 extern "C" int ibf_pair_eval(int kind, int64_t n, const double* pts, double* d, double* grad, double* weights,
                              uint8_t* degenerate, ibf_stream s) {
+  ::ibf::StreamScope ibf_scope_((cudaStream_t)s);
   if (kind != 0 && kind != 1) {
     set_error("ibf_pair_eval: kind must be 0 (VF) or 1 (EE)");
     return IBF_ERR_BAD_ARG;
@@ -554,6 +555,7 @@ extern "C" int ibf_pair_eval(int kind, int64_t n, const double* pts, double* d, 
 
 extern "C" int ibf_accd(int kind, int64_t n, const double* x0, const double* x1, double min_gap, double* toi,
                         ibf_stream s) {
+  ::ibf::StreamScope ibf_scope_((cudaStream_t)s);
   if (kind != 0 && kind != 1) {
     set_error("ibf_accd: kind must be 0 (VF) or 1 (EE)");
     return IBF_ERR_BAD_ARG;
@@ -597,6 +599,7 @@ static ibf::DevBuf<int>& cand_store(ibf_ccd* c) { return c->b_pos; }
 
 extern "C" int ibf_ccd_candidates(ibf_ccd* c, const double* x0, const double* x1, double min_gap, int64_t* n_vf,
                                   int64_t* n_ee, ibf_stream st) {
+  ::ibf::StreamScope ibf_scope_((cudaStream_t)st);
   cudaStream_t s = (cudaStream_t)st;
   int64_t cnt_vf = 0, cnt_ee = 0, all = 0;
   IBF_TRY(broad_pass(c, 0, x0, x1, min_gap, false, &cnt_vf, &all, s));
@@ -629,6 +632,7 @@ extern "C" int ibf_ccd_candidates(ibf_ccd* c, const double* x0, const double* x1
 }
 
 extern "C" int ibf_ccd_get_candidates(ibf_ccd* c, int64_t* vf_host, int64_t* ee_host, ibf_stream st) {
+  ::ibf::StreamScope ibf_scope_((cudaStream_t)st);
   cudaStream_t s = (cudaStream_t)st;
   const int64_t tot = c->n_vf + c->n_ee;
   std::vector<int> q(4 * tot);
@@ -641,6 +645,7 @@ extern "C" int ibf_ccd_get_candidates(ibf_ccd* c, int64_t* vf_host, int64_t* ee_
 
 extern "C" int ibf_max_step_size(ibf_ccd* c, const double* x, const double* x_hat, double min_gap, double cap,
                                  double* alpha_host, int64_t* n_blocking_host, ibf_stream st) {
+  ::ibf::StreamScope ibf_scope_((cudaStream_t)st);
   cudaStream_t s = (cudaStream_t)st;
   IBF_TRY(c->dscratch.reserve(8));
   IBF_TRY(c->host.reserve(64));
@@ -719,6 +724,7 @@ extern "C" int ibf_ccd_blocking(ibf_ccd* c, const int32_t** kinds, const int32_t
 }
 
 extern "C" int ibf_ccd_get_blocking(ibf_ccd* c, int64_t* kinds, int64_t* quads, double* tois, ibf_stream st) {
+  ::ibf::StreamScope ibf_scope_((cudaStream_t)st);
   cudaStream_t s = (cudaStream_t)st;
   const int64_t n = c->n_block;
   if (!n) return IBF_OK;
@@ -898,6 +904,7 @@ __global__ void k_find_dist(int64_t n, const double* __restrict__ dist, const do
 
 extern "C" int ibf_static_intersection(ibf_ccd* c, const double* x, int64_t* n_hits, int64_t* pairs_host,
                                        int64_t cap, ibf_stream st) {
+  ::ibf::StreamScope ibf_scope_((cudaStream_t)st);
   cudaStream_t s = (cudaStream_t)st;
   int64_t cnt = 0, all = 0;
   *n_hits = 0;
@@ -931,6 +938,7 @@ extern "C" int ibf_static_intersection(ibf_ccd* c, const double* x, int64_t* n_h
 
 extern "C" int ibf_min_distance(ibf_ccd* c, const double* x, double radius, double* d_host, int64_t* pair_host,
                                 ibf_stream st) {
+  ::ibf::StreamScope ibf_scope_((cudaStream_t)st);
   cudaStream_t s = (cudaStream_t)st;
   *d_host = INFINITY;
   if (pair_host)
@@ -986,6 +994,7 @@ int contacts_update_dev(ibf_contacts* c, int64_t nb, const int* bkind, const int
 
 extern "C" int ibf_contacts_update(ibf_contacts* c, const ibf_ccd* blocking, int64_t* admitted, int64_t* pruned,
                                    ibf_stream st) {
+  ::ibf::StreamScope ibf_scope_((cudaStream_t)st);
   const int64_t nb = blocking ? blocking->n_block : 0;
   return contacts_update_dev(c, nb, nb ? blocking->b_kind.p : nullptr, nb ? blocking->b_quad.p : nullptr,
                              nb ? blocking->b_toi.p : nullptr, admitted, pruned, (cudaStream_t)st);

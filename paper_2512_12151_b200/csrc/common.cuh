@@ -100,10 +100,25 @@ void alloc_report(const char* what, size_t bytes, double t0);
 // mapped for reuse.  Plain cudaMalloc / cudaFree inside the Newton loop (a
 // buffer outgrowing its capacity mid-press) measured 2-800 ms per call on the
 // B200 boxes, stalling the whole frame; the pool path is microseconds.
-// Semantics are kept: dev_free waits for the device like cudaFree, and
-// dev_alloc returns memory usable on any stream.
+// Inside a C-ABI call that names a stream (StreamScope, set by every such
+// entry point) both are ordered on that stream — a handle is used on one
+// stream only (ibf.h), so nothing else can still be reading the old block and
+// no device-wide sync is needed: one scene's buffer growth no longer stalls
+// the scenes in flight on other streams.  Outside such a call (handle create /
+// destroy) dev_alloc returns memory usable on any stream and dev_free waits
+// for the device, like cudaMalloc / cudaFree.
 int dev_alloc(void** p, size_t bytes);
 void dev_free(void* p);
+
+// The stream of the innermost C-ABI call on this thread (0: none).
+extern thread_local cudaStream_t tl_stream;
+struct StreamScope {
+  cudaStream_t prev;
+  explicit StreamScope(cudaStream_t s) : prev(tl_stream) { tl_stream = s; }
+  ~StreamScope() { tl_stream = prev; }
+  StreamScope(const StreamScope&) = delete;
+  StreamScope& operator=(const StreamScope&) = delete;
+};
 
 // Growable device buffer owned by a handle.  Never shrinks.
 template <typename T>

@@ -544,6 +544,7 @@ extern "C" int64_t ibf_contacts_size(const ibf_contacts* c) { return c ? c->n : 
 
 extern "C" int ibf_contacts_update_host(ibf_contacts* c, int64_t n, const int64_t* kinds, const int64_t* quads,
                                         const double* tois, int64_t* admitted, int64_t* pruned, ibf_stream st) {
+  ::ibf::StreamScope ibf_scope_((cudaStream_t)st);
   cudaStream_t s = (cudaStream_t)st;
   std::vector<int> k32(n), q32(4 * n);
   for (int64_t j = 0; j < n; ++j) {
@@ -563,6 +564,7 @@ extern "C" int ibf_contacts_update_host(ibf_contacts* c, int64_t n, const int64_
 }
 
 extern "C" int ibf_contacts_refresh_anchors(ibf_contacts* c, const double* x, int64_t* n_degenerate, ibf_stream st) {
+  ::ibf::StreamScope ibf_scope_((cudaStream_t)st);
   cudaStream_t s = (cudaStream_t)st;
   IBF_TRY(c->iscratch.reserve(2));
   IBF_CUDA(cudaMemsetAsync(c->iscratch.p, 0, sizeof(int), s));
@@ -576,6 +578,7 @@ extern "C" int ibf_contacts_refresh_anchors(ibf_contacts* c, const double* x, in
 
 extern "C" int ibf_contacts_dual_sweep(ibf_contacts* c, const double* x_hat, double offset, double mu, double decay,
                                        double* worst_host, ibf_stream st) {
+  ::ibf::StreamScope ibf_scope_((cudaStream_t)st);
   cudaStream_t s = (cudaStream_t)st;
   IBF_TRY(c->dscratch.reserve(2));
   IBF_TRY(contacts_dual(c, x_hat, offset, mu, decay, c->dscratch.p, s));
@@ -587,6 +590,7 @@ extern "C" int ibf_contacts_dual_sweep(ibf_contacts* c, const double* x_hat, dou
 extern "C" int ibf_contacts_export(const ibf_contacts* cc, int64_t* kind, int64_t* quad, double* lam, double* gamma,
                                    double* s_, double* anchor_d, double* anchor_grad, double* anchor_x,
                                    ibf_stream st) {
+  ::ibf::StreamScope ibf_scope_((cudaStream_t)st);
   ibf_contacts* c = const_cast<ibf_contacts*>(cc);
   cudaStream_t s = (cudaStream_t)st;
   const int64_t n = c->n;
@@ -611,6 +615,7 @@ extern "C" int ibf_contacts_export(const ibf_contacts* cc, int64_t* kind, int64_
 extern "C" int ibf_contacts_import(ibf_contacts* c, int64_t n, const int64_t* kind, const int64_t* quad,
                                    const double* lam, const double* gamma, const double* s_, const double* anchor_d,
                                    const double* anchor_grad, const double* anchor_x, ibf_stream st) {
+  ::ibf::StreamScope ibf_scope_((cudaStream_t)st);
   cudaStream_t s = (cudaStream_t)st;
   std::vector<int> k32(n), q32(4 * n);
   for (int64_t j = 0; j < n; ++j) {

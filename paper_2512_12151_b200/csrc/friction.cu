@@ -257,6 +257,7 @@ extern "C" int64_t ibf_friction_size(const ibf_friction* f) { return f ? f->n : 
 extern "C" int ibf_friction_precompute(ibf_friction* f, const ibf_contacts* c, const double* x, double mu,
                                        double offset, double h, double mu_f, double eps_v, int64_t* n_terms,
                                        ibf_stream st) {
+  ::ibf::StreamScope ibf_scope_((cudaStream_t)st);
   cudaStream_t s = (cudaStream_t)st;
   f->n = 0;
   f->vf_nverts = -1;
@@ -295,6 +296,7 @@ extern "C" int ibf_friction_precompute(ibf_friction* f, const ibf_contacts* c, c
 extern "C" int ibf_friction_import(ibf_friction* f, int64_t n, const int64_t* quad, const double* w,
                                    const double* frames, const double* coeff, const double* ref, double eps,
                                    ibf_stream st) {
+  ::ibf::StreamScope ibf_scope_((cudaStream_t)st);
   cudaStream_t s = (cudaStream_t)st;
   if (n < 0) {
     set_error("ibf_friction_import: negative size");
@@ -319,6 +321,7 @@ extern "C" int ibf_friction_import(ibf_friction* f, int64_t n, const int64_t* qu
 
 extern "C" int ibf_friction_export(const ibf_friction* f, int64_t* quad, double* w, double* frames, double* coeff,
                                    double* ref, double* eps, ibf_stream st) {
+  ::ibf::StreamScope ibf_scope_((cudaStream_t)st);
   cudaStream_t s = (cudaStream_t)st;
   const int64_t n = f->n;
   *eps = f->eps;

@@ -53,18 +53,23 @@ int dev_alloc(void** p, size_t bytes) {
     IBF_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
     pools_ready.fetch_or(1u << dev);
   }
+  const cudaStream_t s = tl_stream;
+  IBF_CUDA(cudaMallocAsync(p, bytes, s));
   // legacy default stream: ordered after prior work on blocking streams; the
   // sync makes the block usable from any (non-blocking) stream at once
-  IBF_CUDA(cudaMallocAsync(p, bytes, 0));
-  IBF_CUDA(cudaStreamSynchronize(0));
+  if (!s) IBF_CUDA(cudaStreamSynchronize(0));
   return IBF_OK;
 }
 
 void dev_free(void* p) {
-  // the old buffer may still be read by queued kernels on any stream
-  cudaDeviceSynchronize();
-  cudaFreeAsync(p, 0);
+  const cudaStream_t s = tl_stream;
+  // outside a stream-scoped call the old buffer may still be read by queued
+  // kernels on any stream
+  if (!s) cudaDeviceSynchronize();
+  cudaFreeAsync(p, s);
 }
+
+thread_local cudaStream_t tl_stream = 0;
 
 void alloc_report(const char* what, size_t bytes, double t0) {
   const double ms = 1e3 * (wall_now() - t0);
@@ -194,6 +199,7 @@ extern "C" const char* ibf_last_error(void) { return g_err.c_str(); }
 
 extern "C" int ibf_inertia_target(int64_t n, const double* x, const double* v, double h, const double* g3,
                                   double* x_tilde, ibf_stream st) {
+  ::ibf::StreamScope ibf_scope_((cudaStream_t)st);
   if (n <= 0) return IBF_OK;
   k_inertia<<<grid_for(3 * n), 256, 0, (cudaStream_t)st>>>(3 * n, x, v, h, g3[0], g3[1], g3[2], x_tilde);
   IBF_LAUNCH_CHECK();
@@ -201,6 +207,7 @@ extern "C" int ibf_inertia_target(int64_t n, const double* x, const double* v, d
 }
 
 extern "C" int ibf_clamp_state(int64_t n, double* x, const double* x_hat, double alpha, ibf_stream st) {
+  ::ibf::StreamScope ibf_scope_((cudaStream_t)st);
   if (n <= 0) return IBF_OK;
   k_clamp<<<grid_for(3 * n), 256, 0, (cudaStream_t)st>>>(3 * n, alpha, x, x_hat);
   IBF_LAUNCH_CHECK();
@@ -208,6 +215,7 @@ extern "C" int ibf_clamp_state(int64_t n, double* x, const double* x_hat, double
 }
 
 extern "C" int ibf_velocity_update(int64_t n, const double* x, const double* x_t, double h, double* v, ibf_stream st) {
+  ::ibf::StreamScope ibf_scope_((cudaStream_t)st);
   if (n <= 0) return IBF_OK;
   k_velocity<<<grid_for(3 * n), 256, 0, (cudaStream_t)st>>>(3 * n, x, x_t, h, v);
   IBF_LAUNCH_CHECK();
@@ -225,6 +233,7 @@ extern "C" int ibf_system_spmv_stats(const ibf_system* s, double* bytes_per_spmv
 extern "C" int ibf_solve_subproblem(ibf_system* s, ibf_contacts* c, const double* x_tilde, const double* x,
                                     double* x_hat, double mu, double offset, double h, double cg_tol, double decay,
                                     double* result_host, ibf_stream st) {
+  ::ibf::StreamScope ibf_scope_((cudaStream_t)st);
   cudaStream_t stream = (cudaStream_t)st;
   const int64_t n = s->n;
   const int64_t n3 = 3 * n;
@@ -394,6 +403,7 @@ __global__ void k_sub(int64_t n, const double* __restrict__ a, const double* __r
 }  // namespace ibf
 
 extern "C" int ibf_vec_sub(int64_t n, const double* a, const double* b, double* out, ibf_stream st) {
+  ::ibf::StreamScope ibf_scope_((cudaStream_t)st);
   if (n <= 0) return IBF_OK;
   ibf::k_sub<<<ibf::grid_for(n), 256, 0, (cudaStream_t)st>>>(n, a, b, out);
   IBF_LAUNCH_CHECK();

@@ -1026,6 +1026,15 @@ struct PcgShape {
   int grid, threads, rows_per_thread, smem_rows;
 };
 
+// Runtime overrides of the launch shape (ibf_pcg_tuning): the row count up
+// to which rows get several lanes, and a cap on the CTA count (0: a full
+// wave).  Tests use them to drive the one-thread-per-row path with several
+// sweeps per thread on systems the oracle solves in seconds.
+static std::atomic<long long> g_lanes_max_n{IBF_PCG_LANES_MAX_N};
+static std::atomic<int> g_max_ctas{0};
+// shape of the last PCG launch in the process (ibf_pcg_last_shape)
+static std::atomic<long long> g_last_shape[6];
+
 static PcgShape pcg_shape(int n) {
   static std::atomic<int> max_b_cache{-1};
   int max_b = max_b_cache.load();
@@ -1042,8 +1051,11 @@ static PcgShape pcg_shape(int n) {
     max_b_cache.store(max_b);
   }
   n = std::max(n, 1);
+  const int cap = g_max_ctas.load();
   auto shape_for = [&](int b) {
-    const int grid = (int)std::min<int64_t>((int64_t)b * sm_count(), div_up(n, PCG_THREADS));
+    int64_t g = std::min<int64_t>((int64_t)b * sm_count(), div_up(n, PCG_THREADS));
+    if (cap > 0) g = std::min<int64_t>(g, cap);
+    const int grid = (int)g;
     const int rpt = (int)div_up(n, (int64_t)grid * PCG_THREADS);
     return PcgShape{grid, PCG_THREADS, rpt, 0};
   };
@@ -1110,7 +1122,7 @@ int pcg_solve(const Operator& op, const double* rhs, double* x_out, double rel_t
   IBF_TRY(w.hp.reserve(n3));
   IBF_TRY(w.X.reserve(3 * n3));
   IBF_TRY(w.info.reserve(4));
-  const int lanes = (IBF_PCG_LANES > 1 && !IBF_PCG_CARRY_QP && n <= IBF_PCG_LANES_MAX_N) ? IBF_PCG_LANES : 1;
+  const int lanes = (IBF_PCG_LANES > 1 && !IBF_PCG_CARRY_QP && n <= g_lanes_max_n.load()) ? IBF_PCG_LANES : 1;
   PcgShape sh = pcg_shape(n * lanes);   // grid sized for lanes x rows threads
   if (lanes > 1) {
     sh.rows_per_thread = (int)div_up(std::max(n, 1), (int64_t)sh.grid * sh.threads);
@@ -1165,6 +1177,12 @@ int pcg_solve(const Operator& op, const double* rhs, double* x_out, double rel_t
   const bool persist = l2_persist_budget() > 0 && op.val_bytes > 0;
   if (persist) l2_window(s, op.val, op.val_bytes, true);
   IBF_CUDA(cudaLaunchCooperativeKernel((void*)k_pcg, sh.grid, sh.threads, args, smem, s));
+  g_last_shape[0].store(sh.grid);
+  g_last_shape[1].store(sh.threads);
+  g_last_shape[2].store(sh.rows_per_thread);
+  g_last_shape[3].store(lanes);
+  g_last_shape[4].store(a.ready ? 1 : 0);
+  g_last_shape[5].store((long long)op.contact.n + op.friction.n);
   if (persist) l2_window(s, op.val, op.val_bytes, false);
   ++g_launches;
   if (IBF_PCG_PROFILE) {
@@ -1415,10 +1433,12 @@ extern "C" int ibf_bsr_create(int64_t n, int64_t nnz, const int64_t* rows, const
 extern "C" void ibf_bsr_destroy(ibf_bsr* m) { delete m; }
 
 extern "C" int ibf_bsr_matvec(ibf_bsr* m, const double* x, double* y, ibf_stream st) {
+  ::ibf::StreamScope ibf_scope_((cudaStream_t)st);
   return spmv(m->op(), x, y, (cudaStream_t)st);
 }
 
 extern "C" int ibf_bsr_mask_dirichlet(ibf_bsr* m, const uint8_t* vertex_mask, const double* diag, ibf_stream st) {
+  ::ibf::StreamScope ibf_scope_((cudaStream_t)st);
   cudaStream_t s = (cudaStream_t)st;
   DevBuf<uint8_t> dm;
   DevBuf<double> dd;
@@ -1436,6 +1456,7 @@ extern "C" int ibf_bsr_mask_dirichlet(ibf_bsr* m, const uint8_t* vertex_mask, co
 
 extern "C" int ibf_bsr_pcg(ibf_bsr* m, const double* rhs, double* x_out, double rel_tol, int64_t max_iters,
                            double* info_host, ibf_stream st) {
+  ::ibf::StreamScope ibf_scope_((cudaStream_t)st);
   cudaStream_t s = (cudaStream_t)st;
   IBF_TRY(invert_diag_blocks((int)m->pat.n, m->pat.val.p, m->pat.diag_q.p, m->pinv.p, s));
   IBF_TRY(pcg_solve(m->op(), rhs, x_out, rel_tol, max_iters, m->work, s));
@@ -1445,5 +1466,21 @@ extern "C" int ibf_bsr_pcg(ibf_bsr* m, const double* rhs, double* x_out, double 
 extern "C" int64_t ibf_bsr_size(const ibf_bsr* m) { return m ? m->pat.nb : 0; }
 
 extern "C" int ibf_bsr_export(const ibf_bsr* m, int64_t* rows, int64_t* cols, double* blocks, ibf_stream st) {
+  ::ibf::StreamScope ibf_scope_((cudaStream_t)st);
   return sell_export(m->pat, rows, cols, blocks, (cudaStream_t)st);
+}
+
+extern "C" int ibf_pcg_tuning(int64_t lanes_max_n, int max_ctas) {
+  if (max_ctas < 0) {
+    set_error("ibf_pcg_tuning: max_ctas must be >= 0");
+    return IBF_ERR_BAD_ARG;
+  }
+  ibf::g_lanes_max_n.store(lanes_max_n < 0 ? IBF_PCG_LANES_MAX_N : lanes_max_n);
+  ibf::g_max_ctas.store(max_ctas);
+  return IBF_OK;
+}
+
+extern "C" int ibf_pcg_last_shape(int64_t* out) {
+  for (int k = 0; k < 6; ++k) out[k] = ibf::g_last_shape[k].load();
+  return IBF_OK;
 }

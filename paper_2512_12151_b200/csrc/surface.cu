@@ -235,6 +235,7 @@ static int extract(ibf_surface* h, int64_t m, const int64_t* tets_dev, cudaStrea
 
 extern "C" int ibf_surface_extract(int64_t m, const int64_t* tets_dev, ibf_surface** out, int64_t* n_tris,
                                    int64_t* n_edges, int64_t* n_verts, int64_t* n_nonmanifold, ibf_stream st) {
+  ::ibf::StreamScope ibf_scope_((cudaStream_t)st);
   if (!out || !n_tris || !n_edges || !n_verts || !n_nonmanifold || m < 0 || (m > 0 && !tets_dev)) {
     set_error("ibf_surface_extract: bad arguments");
     return IBF_ERR_BAD_ARG;
@@ -259,6 +260,7 @@ extern "C" int ibf_surface_extract(int64_t m, const int64_t* tets_dev, ibf_surfa
 }
 
 extern "C" int ibf_surface_get(const ibf_surface* h, int64_t* tris, int64_t* edges, int64_t* verts, ibf_stream st) {
+  ::ibf::StreamScope ibf_scope_((cudaStream_t)st);
   if (!h) {
     set_error("ibf_surface_get: null handle");
     return IBF_ERR_BAD_ARG;

@@ -925,6 +925,7 @@ extern "C" int ibf_system_pattern(const ibf_system* s, int64_t* n_blocks, int64_
 
 extern "C" int ibf_assemble(ibf_system* s, ibf_contacts* c, const double* x_hat, const double* x_tilde, double mu,
                             double offset, double h, int apply_dbc, double* grad, ibf_stream st) {
+  ::ibf::StreamScope ibf_scope_((cudaStream_t)st);
   cudaStream_t stream = (cudaStream_t)st;
   IBF_TRY(system_assemble(s, c, x_hat, x_tilde, mu, offset, h, apply_dbc != 0, grad, false, stream));
   // NonFiniteEnergyError semantics: report synchronously
@@ -938,15 +939,83 @@ extern "C" int ibf_assemble(ibf_system* s, ibf_contacts* c, const double* x_hat,
 }
 
 extern "C" int ibf_system_matvec(ibf_system* s, const double* x, double* y, ibf_stream st) {
+  ::ibf::StreamScope ibf_scope_((cudaStream_t)st);
   return spmv(s->op(), x, y, (cudaStream_t)st);
 }
 
 extern "C" int ibf_system_export_bsr(ibf_system* s, int64_t* rows, int64_t* cols, double* blocks, ibf_stream st) {
+  ::ibf::StreamScope ibf_scope_((cudaStream_t)st);
   return sell_export(s->pat, rows, cols, blocks, (cudaStream_t)st);
+}
+
+// Explicit upper cliques of the matrix-free terms of the last assembly, in
+// the reference's COO form (clique_contributions, intact/sparse.py:17-36):
+// per term the 10 (i <= j) local pairs of triu_indices(4), block
+// coef * g_i g_j^T (contacts, ConstraintBatch.hessian_grids,
+// intact/contact.py:139-141) or w_i w_j H (friction, intact/friction.py:88-100),
+// transposed when the global row > col.  Contacts first, then friction.
+__global__ void k_term_blocks(ContactView cv, FrictionView fv, int64_t* rows, int64_t* cols, double* blocks) {
+  const int64_t n_terms = (int64_t)cv.n + fv.n;
+  for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < 10 * n_terms;
+       id += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = id / 10;
+    int q = (int)(id - 10 * t), i = 0;
+    while (q >= 4 - i) {   // q -> (i, j) of triu_indices(4), row-major
+      q -= 4 - i;
+      ++i;
+    }
+    const int j = i + q;
+    double B[9];
+    int vi, vj;
+    if (t < cv.n) {
+      const int c = (int)t;
+      vi = cv.quad[4 * c + i];
+      vj = cv.quad[4 * c + j];
+      const double* gi = cv.grad + 12 * c + 3 * i;
+      const double* gj = cv.grad + 12 * c + 3 * j;
+      for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) B[3 * a + b] = cv.coef[c] * gi[a] * gj[b];
+    } else {
+      const int k = (int)(t - cv.n);
+      vi = fv.quad[4 * k + i];
+      vj = fv.quad[4 * k + j];
+      const double w = fv.w[4 * k + i] * fv.w[4 * k + j];
+      for (int e = 0; e < 9; ++e) B[e] = w * fv.hw[9 * k + e];
+    }
+    const bool sw = vi > vj;
+    rows[id] = sw ? vj : vi;
+    cols[id] = sw ? vi : vj;
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) blocks[9 * id + 3 * a + b] = sw ? B[3 * b + a] : B[3 * a + b];
+  }
+}
+
+extern "C" int ibf_system_export_terms(ibf_system* s, int64_t* n_blocks, int64_t* rows, int64_t* cols,
+                                       double* blocks, ibf_stream st) {
+  ::ibf::StreamScope ibf_scope_((cudaStream_t)st);
+  cudaStream_t stream = (cudaStream_t)st;
+  const Operator o = s->op();
+  const int64_t nb = 10 * ((int64_t)o.contact.n + o.friction.n);
+  if (n_blocks) *n_blocks = nb;
+  if (!rows || nb == 0) return IBF_OK;
+  DevBuf<int64_t> dr, dc;
+  DevBuf<double> db;
+  IBF_TRY(dr.reserve(nb));
+  IBF_TRY(dc.reserve(nb));
+  IBF_TRY(db.reserve(9 * nb));
+  k_term_blocks<<<(int)std::min<int64_t>(div_up(nb, 256), 4LL * 148), 256, 0, stream>>>(o.contact, o.friction, dr.p,
+                                                                                       dc.p, db.p);
+  IBF_LAUNCH_CHECK();
+  IBF_CUDA(cudaMemcpyAsync(rows, dr.p, nb * sizeof(int64_t), cudaMemcpyDeviceToHost, stream));
+  IBF_CUDA(cudaMemcpyAsync(cols, dc.p, nb * sizeof(int64_t), cudaMemcpyDeviceToHost, stream));
+  IBF_CUDA(cudaMemcpyAsync(blocks, db.p, 9 * nb * sizeof(double), cudaMemcpyDeviceToHost, stream));
+  IBF_CUDA(cudaStreamSynchronize(stream));
+  return IBF_OK;
 }
 
 extern "C" int ibf_system_pcg(ibf_system* s, const double* rhs, double* x_out, double rel_tol, int64_t max_iters,
                               double* info_host, ibf_stream st) {
+  ::ibf::StreamScope ibf_scope_((cudaStream_t)st);
   cudaStream_t stream = (cudaStream_t)st;
   IBF_TRY(pcg_solve(s->op(), rhs, x_out, rel_tol, max_iters, s->work, stream));
   return pcg_info(s->work, info_host, stream);
@@ -955,6 +1024,7 @@ extern "C" int ibf_system_pcg(ibf_system* s, const double* rhs, double* x_out, d
 extern "C" int ibf_incremental_energy(ibf_system* s, ibf_contacts* c, const double* x_hat, const double* p, int n_r,
                                       const double* r_host, const double* x_tilde, double mu, double offset,
                                       double h, double* energies_host, ibf_stream st) {
+  ::ibf::StreamScope ibf_scope_((cudaStream_t)st);
   cudaStream_t stream = (cudaStream_t)st;
   const int T = p ? n_r : 1;
   IBF_TRY(system_energy_launch(s, c, x_hat, p, T, r_host, nullptr, x_tilde, mu, offset, h, s->dscal.p, stream));
@@ -965,6 +1035,7 @@ extern "C" int ibf_incremental_energy(ibf_system* s, ibf_contacts* c, const doub
 
 extern "C" int ibf_inversion_safe_step(ibf_system* s, const double* x, const double* p, double* out_host,
                                        ibf_stream st) {
+  ::ibf::StreamScope ibf_scope_((cudaStream_t)st);
   cudaStream_t stream = (cudaStream_t)st;
   IBF_TRY(system_inversion_cap_launch(s, x, p, s->dscal.p, stream));
   IBF_CUDA(cudaMemcpyAsync(out_host, s->dscal.p, sizeof(double), cudaMemcpyDeviceToHost, stream));
@@ -975,6 +1046,7 @@ extern "C" int ibf_inversion_safe_step(ibf_system* s, const double* x, const dou
 
 extern "C" int ibf_stiffness_diagonal_max(ibf_system* s, const double* x, double h, double* out_host,
                                           ibf_stream st) {
+  ::ibf::StreamScope ibf_scope_((cudaStream_t)st);
   cudaStream_t stream = (cudaStream_t)st;
   if (s->n == 0) {
     *out_host = 1.0;

@@ -98,6 +98,114 @@ def shell_sphere(n, radius=0.1, center=(0.0, 0.0, 0.0), layers=1) -> TetMesh:
     return build_tet_mesh(verts + np.asarray(center, dtype=np.float64), tets)
 
 
+def _sphere_map(c, radius, blend=0.8):
+    """Cube [-1,1]^3 -> rounded ball: each cube shell |c|_inf = r goes to
+    `blend` x the sphere of radius r * radius under the smooth "spherified
+    cube" map s_x sqrt(1 - s_y^2/2 - s_z^2/2 + s_y^2 s_z^2/3) of
+    s = c / |c|_inf, plus (1 - blend) x the cube itself.  The full radial
+    projection (intact/primitives.py:80-87, blend 1) flattens the Kuhn cells
+    at the cube corners to 1e-3..1e-2 of the median volume; blend 0.8 keeps
+    every tet above 0.29 of it."""
+    sup = np.abs(c).max(axis=1)
+    s = c / np.where(sup > 0.0, sup, 1.0)[:, None]
+    q = s * s
+    out = np.empty_like(s)
+    out[:, 0] = s[:, 0] * np.sqrt(np.maximum(1 - q[:, 1] / 2 - q[:, 2] / 2 + q[:, 1] * q[:, 2] / 3, 0.0))
+    out[:, 1] = s[:, 1] * np.sqrt(np.maximum(1 - q[:, 2] / 2 - q[:, 0] / 2 + q[:, 2] * q[:, 0] / 3, 0.0))
+    out[:, 2] = s[:, 2] * np.sqrt(np.maximum(1 - q[:, 0] / 2 - q[:, 1] / 2 + q[:, 0] * q[:, 1] / 3, 0.0))
+    return (blend * out * sup[:, None] + (1.0 - blend) * c) * radius
+
+
+def squishy_ball(n=32, shell=2, stem=23, tip=16, pitch=3, cell=0.01, center=(0.0, 0.0, 0.0)) -> TetMesh:
+    """Squishy ball: a hollow core with thin strands all over it.
+
+    The core is the outer `shell` Kuhn-cell layers of an n^3 grid mapped onto
+    a rounded ball of radius ~n/2 * cell (`_sphere_map`).  On every face of the grid, 2x2-cell strands
+    start at a `pitch`-cell spacing (one free cell between neighbours); each
+    runs `stem` cells out along the radial direction through its base centre,
+    then narrows to a 1x1-cell `tip` of `tip` cells, centred on the same axis.
+    All cells belong to one integer lattice, so the Kuhn (Freudenthal) split
+    is conforming everywhere, strand bases included.
+
+    Almost every vertex lies on the surface, as in the paper's squishy balls
+    (0.87M vertices, 1.59M surface triangles, 2.25M tets for
+    five balls): the defaults give 454k tets, 179k vertices and 319k surface
+    triangles per ball.
+    """
+    L = stem + tip
+    off = L                                   # lattice shift: coordinates >= 0
+    dim = n + 2 * L                           # cells per axis of the enclosing lattice
+    cells = []
+    # hollow core
+    i, j, k = np.meshgrid(np.arange(n), np.arange(n), np.arange(n), indexing="ij")
+    depth = np.minimum(np.minimum(np.minimum(i, j), k), np.minimum(np.minimum(n - 1 - i, n - 1 - j), n - 1 - k))
+    on = depth < shell
+    cells.append(np.stack([i[on], j[on], k[on]], axis=1))
+    # strand origins on a face: (a, b) lower corners of 2x2 patches
+    starts = np.arange(1, n - 1, pitch)
+    starts = starts[starts + 3 <= n]     # a free cell to the face edge on both sides
+    starts = starts + (n - (starts[-1] + 2) - starts[0]) // 2   # centre the pattern
+    A, B = np.meshgrid(starts, starts, indexing="ij")
+    A, B = A.ravel(), B.ravel()
+    for ax in range(3):
+        u_ax, v_ax = [a for a in range(3) if a != ax]
+        for sgn in (-1, 1):
+            for l in range(L):
+                w = 2 if l < stem else 1
+                layer = n + l if sgn > 0 else -1 - l
+                for du in range(w):
+                    for dv in range(w):
+                        c = np.empty((len(A), 3), dtype=np.int64)
+                        c[:, ax] = layer
+                        c[:, u_ax] = A + du
+                        c[:, v_ax] = B + dv
+                        cells.append(c)
+    cells = np.concatenate(cells) + off
+    tets = cell_tets(dim, dim, dim, cells)
+    used, tets = np.unique(tets, return_inverse=True)
+    tets = tets.reshape(-1, 4)
+    g = np.stack(np.unravel_index(used, (dim + 1, dim + 1, dim + 1)), axis=1) - off   # lattice coords
+    half = n / 2.0
+    radius = half * cell
+    pos = np.empty((len(g), 3))
+    inside = ((g >= 0) & (g <= n)).all(axis=1)
+    pos[inside] = _sphere_map((g[inside] - half) / half, radius)
+    out = np.flatnonzero(~inside)
+    go = g[out]
+    # face of each strand vertex: the axis that leaves [0, n]
+    ax = np.argmax((go < 0) | (go > n), axis=1)
+    rows = np.arange(len(out))
+    gax = go[rows, ax]
+    sgn = np.where(gax > n, 1, -1)
+    l = np.where(sgn > 0, gax - n, -gax)                     # layers out from the face
+    base = go.copy()
+    base[rows, ax] = np.where(sgn > 0, n, 0)
+    uv = np.stack([base[rows, (ax + 1) % 3], base[rows, (ax + 2) % 3]], axis=1)
+    # strand origin (lower corner) of each vertex: the start <= coordinate
+    org = starts[np.clip(np.searchsorted(starts, uv, side="right") - 1, 0, len(starts) - 1)]
+    centre = base.astype(np.float64)
+    centre[rows, (ax + 1) % 3] = org[:, 0] + 1.0
+    centre[rows, (ax + 2) % 3] = org[:, 1] + 1.0
+    bc = _sphere_map((centre - half) / half, radius)
+    axis = bc / np.linalg.norm(bc, axis=1)[:, None]
+    # tip vertices (l > stem) sit on a half-size cross-section: map the 1x1
+    # corner (a + du, b + dv), du, dv in {0, 1}, to the 2x2 corner (a + 2du, b + 2dv)
+    # and take half its offset from the axis
+    tipv = l > stem
+    wide = base.astype(np.float64)
+    wide[rows, (ax + 1) % 3] = np.where(tipv, org[:, 0] + 2 * (uv[:, 0] - org[:, 0]), uv[:, 0])
+    wide[rows, (ax + 2) % 3] = np.where(tipv, org[:, 1] + 2 * (uv[:, 1] - org[:, 1]), uv[:, 1])
+    bw = _sphere_map((wide - half) / half, radius)
+    shift = np.where(tipv[:, None], 0.5 * (bw - bc), bw - bc)
+    pos[out] = bc + shift + (l * cell)[:, None] * axis
+    return build_tet_mesh(pos + np.asarray(center, dtype=np.float64), tets)
+
+
+def squishy_extent(n=32, stem=23, tip=16, cell=0.01):
+    """Radius of the sphere holding a squishy_ball (strand tips included)."""
+    return (n / 2.0 + stem + tip) * cell
+
+
 def merge(bodies, boundary_bodies=(), scripted=None, h=0.01, scripted_stop=None):
     """Stack bodies [(mesh, material, density, velocity)] into a System.
 
@@ -219,6 +327,69 @@ def c4_scene(n=42, radius=0.1, gap=0.001, plate_speed=0.1, h=0.01, layers=None, 
     system, state, offs = merge(bodies, boundary_bodies=[0], scripted={len(bodies) - 1: (0.0, 0.0, -plate_speed)},
                                 h=h, scripted_stop=stop)
     params = StepParams(h=h, offset=1e-3, min_iterations=2)
+    return system, state, params
+
+
+def squishy_scene(cell=0.01, n=32, stem=23, tip=16, shell=2, gap=None, plate_speed=1.0, plate_stop=None, h=0.01,
+                  walls=True, seed=7, balls=5):
+    """C4, paper-scale: five squishy balls in a box, pressed by a plate.
+
+    Each ball is a `squishy_ball` (hollow core + 600 strands; the defaults
+    give 2.27M tets, 0.89M vertices and 1.60M surface triangles for five
+    balls, within 3 % of the paper's 2.25M / 0.87M / 1.59M),
+    COR with the paper's rho 1e2, E 1e4, nu 0.4, h = 0.01, offset 1e-3,
+    K_min 2.  Each ball gets a seeded random rotation so no strands of two
+    balls are aligned.  Four balls sit in a 2x2 square on a pinned floor and
+    the fifth in the pocket above; four pinned walls (with slits between
+    them, as in c2_scene) hold the stack, and a scripted plate starts one
+    gap above it and moves down at plate_speed, holding once its underside
+    reaches plate_stop (the container shrinking to a minimum height,
+    PAPER.md:596).
+    """
+    rng = np.random.default_rng(seed)
+    base = squishy_ball(n=n, shell=shell, stem=stem, tip=tip, cell=cell)
+    R = float(np.linalg.norm(base.rest_positions, axis=1).max())
+    gap = 2.0 * cell if gap is None else gap
+    mat = Material(MaterialModel.COR, 1e4, 0.4)
+    rho = 1e2
+    c = R + gap / 2
+    z0 = R + gap
+    centers = [(-c, -c, z0), (c, -c, z0), (-c, c, z0), (c, c, z0)]
+    dz = np.sqrt((2 * R + gap) ** 2 - 2 * c * c)
+    centers.append((0.0, 0.0, z0 + dz + gap))
+    centers = centers[:balls]
+    top = max(ct[2] for ct in centers) + R + gap
+    half = 2 * R + 2 * gap                      # inner half-width of the box
+    wall, slit = 4 * cell, 2 * cell
+    pc = 8                                      # wall / plate cells per ~8 ball cells
+    nc = max(2, int(round(2 * (half + wall) / (pc * cell))))
+    hc = max(2, int(round(top / (pc * cell))))
+    bodies = [_pinned_slab((2 * (half + wall), 2 * (half + wall), wall), (-half - wall, -half - wall, -wall),
+                           (nc, nc, 1), mat.young, rho, cell)]
+    n_fixed = 1
+    if walls:
+        height = top + 2 * cell
+        for sx, sy, cx, cy in ((wall, 2 * half - 2 * slit, -half - wall, -half + slit),
+                               (wall, 2 * half - 2 * slit, half, -half + slit),
+                               (2 * half, wall, -half, -half - wall),
+                               (2 * half, wall, -half, half)):
+            bodies.append(_pinned_slab((sx, sy, height), (cx, cy, slit),
+                                       (1 if sx == wall else nc, 1 if sy == wall else nc, hc), mat.young, rho, cell))
+        n_fixed = 5
+    for ct in centers:
+        Rm = rotation_matrix(rng.standard_normal(3), rng.uniform(-np.pi, np.pi))
+        bodies.append((transformed(base, translate=ct, rotate=Rm), mat, rho, (0.0, 0.0, 0.0)))
+    pl = half - slit
+    bodies.append(_pinned_slab((2 * pl, 2 * pl, wall), (-pl, -pl, top), (nc, nc, 1), mat.young, rho, cell))
+    stop = None
+    if plate_stop is not None:
+        stop = {len(bodies) - 1: max(0.0, (top - plate_stop) / plate_speed)}
+    system, state, offs = merge(bodies, boundary_bodies=list(range(n_fixed)),
+                                scripted={len(bodies) - 1: (0.0, 0.0, -plate_speed)}, h=h, scripted_stop=stop)
+    params = StepParams(h=h, offset=1e-3, min_iterations=2)
+    system.scene_info = {"ball_tets": int(base.n_tets), "ball_verts": int(base.n_verts),
+                         "ball_tris": int(len(base.surface_tris)), "balls": len(centers), "ball_radius": R,
+                         "plate_top": float(top), "cell": cell}
     return system, state, params
 
 

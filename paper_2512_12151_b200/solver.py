@@ -53,6 +53,7 @@ class DeviceSystem:
 
     def __init__(self, masses, regions, dbc_mask=None):
         self._friction = None
+        self._assembly_serial = 0
         masses = np.ascontiguousarray(masses, dtype=np.float64)
         n = len(masses)
         self.n = n
@@ -92,6 +93,7 @@ class DeviceSystem:
 
     # ---- device-tensor entry points (used by the stepper)
     def solve_subproblem(self, aset: ActiveSet | None, x_tilde, x, x_hat, mu, offset, h, cg_tol, decay):
+        self._assembly_serial += 1          # the native loop re-assembles
         res = np.zeros(4)
         ch = aset.ensure(self.n) if aset is not None else None
         _lib.check(_lib.lib().ibf_solve_subproblem(self.handle, ch, _lib.dev_ptr(x_tilde), _lib.dev_ptr(x),
@@ -104,6 +106,7 @@ class DeviceSystem:
         """Frozen friction terms for the following assemble / energy / solve
         calls (None removes them); keeps a reference to the handle."""
         from .friction import as_device
+        self._assembly_serial += 1          # the operator's friction part changes
         self._friction = as_device(friction)
         h = self._friction.handle if self._friction is not None and len(self._friction) else None
         _lib.check(_lib.lib().ibf_system_set_friction(self.handle, h), "ibf_system_set_friction")
@@ -121,6 +124,7 @@ class DeviceSystem:
         return float(out.value)
 
     def assemble(self, aset, x_hat, x_tilde, mu, offset, h, apply_dbc, grad_out):
+        self._assembly_serial += 1
         ch = aset.ensure(self.n) if (aset is not None and len(aset)) else None
         _lib.check(_lib.lib().ibf_assemble(self.handle, ch, _lib.dev_ptr(x_hat), _lib.dev_ptr(x_tilde), float(mu),
                                            float(offset), float(h), 1 if apply_dbc else 0, _lib.dev_ptr(grad_out),
@@ -152,6 +156,21 @@ class DeviceSystem:
         blocks = np.empty((self.n_blocks, 3, 3))
         _lib.check(_lib.lib().ibf_system_export_bsr(self.handle, _lib.host_ptr(rows), _lib.host_ptr(cols),
                                                     _lib.host_ptr(blocks), _lib.stream()), "export_bsr")
+        return rows, cols, blocks
+
+    def export_terms(self):
+        """Explicit upper cliques (rows, cols, blocks (k,3,3)) of the contact
+        and friction terms of the last assembly, unmasked and uncoalesced."""
+        nb = C.c_int64()
+        _lib.check(_lib.lib().ibf_system_export_terms(self.handle, C.byref(nb), None, None, None, _lib.stream()),
+                   "export_terms")
+        rows = np.empty(nb.value, dtype=np.int64)
+        cols = np.empty(nb.value, dtype=np.int64)
+        blocks = np.empty((nb.value, 3, 3))
+        if nb.value:
+            _lib.check(_lib.lib().ibf_system_export_terms(self.handle, C.byref(nb), _lib.host_ptr(rows),
+                                                          _lib.host_ptr(cols), _lib.host_ptr(blocks), _lib.stream()),
+                       "export_terms")
         return rows, cols, blocks
 
     def spmv_bytes(self) -> float:
@@ -187,22 +206,83 @@ def _batch_set(batch: ConstraintBatch | None, n):
 
 
 class AssembledMatrix:
-    """The assembled system matrix: elastic BSR + matrix-free contact term."""
+    """H of `assemble`: the reference's BlockSparseMatrix (intact/sparse.py:46-96)
+    as returned by intact/solver.py:109-156 — mass + h^2 PSD elasticity +
+    mu*gamma grad_d grad_d^T contact cliques + friction cliques, DBC-masked.
 
-    def __init__(self, dev: DeviceSystem, keep):
-        self.dev, self._keep = dev, keep
+    The elastic part is the device system's BSR; the contact and friction
+    parts stay matrix-free on the device.  `matvec` and `pcg_solve(H, ...)`
+    run on that device operator.  `rows` / `cols` / `blocks`,
+    `diagonal_blocks()` and `to_dense()` see the explicit matrix: the term
+    cliques are exported by the device (ibf_system_export_terms), masked like
+    the reference masks them, and coalesced with the elastic blocks into a
+    standalone `BlockSparseMatrix` on first use.  After `mask_dirichlet` the
+    explicit matrix is authoritative for every operation.
+
+    The device operator is that of the owning system's LAST assembly: a later
+    `assemble` on the same system makes earlier matrices stale (reading one
+    raises)."""
+
+    def __init__(self, dev: DeviceSystem, keep, dbc_mask, serial):
+        self.dev, self._keep, self._serial = dev, keep, serial
         self.n_vertices = dev.n
-        self.rows, self.cols, self.blocks = dev.export_bsr()
+        self._dbc = None if dbc_mask is None or not np.any(dbc_mask) else np.asarray(dbc_mask, dtype=bool)
+        self._explicit = None
+        self._detached = False
+
+    def _live(self):
+        if self.dev._assembly_serial != self._serial:
+            raise RuntimeError("stale AssembledMatrix: its DeviceSystem was assembled again")
+
+    def explicit(self):
+        """The explicit BlockSparseMatrix (built once, on first use)."""
+        if self._explicit is None:
+            from .sparse import BlockSparseMatrix
+            self._live()
+            rows, cols, blocks = self.dev.export_bsr()
+            tr, tc, tb = self.dev.export_terms()
+            if self._dbc is not None and len(tr):
+                keep = ~(self._dbc[tr] | self._dbc[tc])          # intact/sparse.py:81-87
+                tr, tc, tb = tr[keep], tc[keep], tb[keep]
+            self._explicit = BlockSparseMatrix(self.n_vertices, np.concatenate([rows, tr]),
+                                               np.concatenate([cols, tc]), np.concatenate([blocks, tb]))
+        return self._explicit
+
+    rows = property(lambda self: self.explicit().rows)
+    cols = property(lambda self: self.explicit().cols)
+    blocks = property(lambda self: self.explicit().blocks)
+
+    @property
+    def handle(self):
+        return self.explicit().handle
+
+    def diagonal_blocks(self):
+        return self.explicit().diagonal_blocks()
+
+    def mask_dirichlet(self, vertex_mask, diag_replacement):
+        self.explicit().mask_dirichlet(vertex_mask, diag_replacement)
+        self._detached = True
 
     def matvec(self, x):
-        xd, yd = to_dev(np.asarray(x).reshape(self.n_vertices, 3)), empty((self.n_vertices, 3))
+        if self._detached:
+            return self._explicit.matvec(x)
+        self._live()
+        xd, yd = to_dev(np.asarray(x, dtype=np.float64).reshape(self.n_vertices, 3)), empty((self.n_vertices, 3))
         self.dev.matvec(xd, yd)
         return to_host(yd)
 
+    def pcg(self, rhs, rel_tol, max_iters=None):
+        """Block-Jacobi PCG on the device operator (pcg_solve's fast path);
+        None once mask_dirichlet detached the explicit matrix."""
+        if self._detached:
+            return None
+        self._live()
+        bd, xd = to_dev(np.asarray(rhs, dtype=np.float64).reshape(self.n_vertices, 3)), empty((self.n_vertices, 3))
+        its, conv, rel = self.dev.pcg(bd, xd, rel_tol, int(max_iters) if max_iters else 0)
+        return to_host(xd), its, conv, rel
+
     def to_dense(self):
-        n3 = 3 * self.n_vertices
-        eye = np.eye(n3)
-        return np.stack([self.matvec(eye[k].reshape(-1, 3)).ravel() for k in range(n3)], axis=1)
+        return self.explicit().to_dense()
 
 
 def assemble(x_hat, x_tilde, masses, regions, batch, mu, offset, h, dbc_mask=None, friction=None):
@@ -214,7 +294,7 @@ def assemble(x_hat, x_tilde, masses, regions, batch, mu, offset, h, dbc_mask=Non
     g = empty((dev.n, 3))
     dev.set_friction(friction)
     dev.assemble(aset, xd, xt, mu, offset, h, dbc_mask is not None and np.any(dbc_mask), g)
-    return to_host(g), AssembledMatrix(dev, (aset, dev._friction))
+    return to_host(g), AssembledMatrix(dev, (aset, dev._friction), dbc_mask, dev._assembly_serial)
 
 
 def incremental_energy(x_hat, x_tilde, masses, regions, batch, mu, offset, h, friction=None) -> float:

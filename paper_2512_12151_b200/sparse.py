@@ -104,7 +104,15 @@ class BlockSparseMatrix:
 
 
 def pcg_solve(matrix: BlockSparseMatrix, rhs, rel_tol, max_iters=None):
-    """Block-Jacobi PCG (intact/sparse.py:99-150) as one persistent kernel."""
+    """Block-Jacobi PCG (intact/sparse.py:99-150) as one persistent kernel.
+    `matrix` is a BlockSparseMatrix or the AssembledMatrix that `assemble`
+    returns (solved on its device operator, contacts matrix-free)."""
+    fast = getattr(matrix, "pcg", None)
+    if fast is not None:
+        out = fast(rhs, rel_tol, max_iters)
+        if out is not None:
+            p, its, conv, rel = out
+            return p, PCGInfo(its, conv, rel)
     rhs = np.ascontiguousarray(rhs, dtype=np.float64).reshape(matrix.n_vertices, 3)
     bd, xd = to_dev(rhs), empty((matrix.n_vertices, 3))
     info = np.zeros(3)

@@ -506,3 +506,201 @@ def test_c3_twisted_rods_small_matches_oracle(pkg):
         assert len(d.iterations) == len(rec)
         assert all(abs(a.newton_iters - b[3]) <= 1 for a, b in zip(d.iterations, rec))
         assert kg == ko
+
+
+def test_reference_composition_through_mirror(pkg, rng):
+    """The reference's own Newton-step composition (intact/solver.py:209-219)
+    through the mirror: grad, H = assemble(...); p = pcg_solve(H, -grad, tol);
+    descent safeguard -inv(H.diagonal_blocks()) grad.  H is a
+    BlockSparseMatrix-compatible object whose explicit blocks include the
+    contact cliques (intact/solver.py:144-148) and the DBC mask
+    (intact/sparse.py:81-87)."""
+    from paper_2512_12151_b200.contact import ConstraintBatch
+    from paper_2512_12151_b200.solver import assemble
+    from paper_2512_12151_b200.sparse import pcg_solve
+    from oracle.blocksparse import pcg as opcg
+    g = golden("trajectory.npz")
+    x, v, aset = _oracle_set_after(g, 2)
+    aset.refresh_anchors(x)
+    ob = aset.snapshot()
+    assert len(ob) > 0
+    x_tilde = x + 0.01 * v + 1e-4 * np.array([0, 0, -9.81])
+    x_hat = x + 1e-4 * rng.standard_normal(x.shape)
+    n_slab = int(g["n_slab"])
+    x_hat[:n_slab] = x[:n_slab]
+    mu, off, h = 50.0, 1e-3, 0.01
+    dbc = np.zeros(len(x), dtype=bool)
+    dbc[:n_slab] = True
+    go, Ho = newton.assemble(x_hat, x_tilde, g["masses"], _oracle_regions(g), ob, mu, off, h, dbc)
+    sysm = _traj_system(pkg, g)
+    batch = ConstraintBatch(ob.kind, ob.quad, ob.lam, ob.gamma, ob.anchor_d, ob.anchor_grad, ob.anchor_x)
+    gg, Hg = assemble(x_hat, x_tilde, sysm.masses, sysm.regions, batch, mu, off, h, dbc)
+    # explicit matrix: same coalesced (row, col) keys, blocks to 1e-10 of the largest
+    assert np.array_equal(Hg.rows, Ho.rows) and np.array_equal(Hg.cols, Ho.cols)
+    scale = np.abs(Ho.blocks).max()
+    err_blocks = np.abs(Hg.blocks - Ho.blocks).max() / scale
+    assert err_blocks <= 1e-10, err_blocks
+    np.testing.assert_allclose(Hg.diagonal_blocks(), Ho.diag(), rtol=0, atol=1e-10 * scale)
+    # pcg_solve on the assembled matrix (device operator, contacts matrix-free)
+    p, info = pcg_solve(Hg, -gg, 1e-4)
+    po, its, conv, _ = opcg(Ho, -go, 1e-4)
+    assert info.converged and conv and abs(info.iterations - its) <= 1
+    err_p = np.abs(p - po).max() / np.abs(po).max()
+    assert err_p <= 1e-6, err_p
+    # descent safeguard as the reference writes it
+    pre = np.linalg.inv(Hg.diagonal_blocks())
+    ps = -np.einsum("nij,nj->ni", pre, gg)
+    pso = -np.einsum("nij,nj->ni", np.linalg.inv(Ho.diag()), go)
+    assert np.abs(ps - pso).max() <= 1e-9 * np.abs(pso).max()
+    # a second mask_dirichlet (here: also pin the top layer) detaches the explicit matrix
+    top = x[:, 2] >= np.sort(x[:, 2])[-20]
+    diag = g["masses"][:, None, None] * np.eye(3)
+    Ho.mask(top, diag)
+    Hg.mask_dirichlet(top, diag)
+    q = rng.standard_normal(x.shape)
+    assert np.abs(Hg.matvec(q) - Ho.matvec(q)).max() <= 1e-10 * np.abs(Ho.matvec(q)).max()
+    p2, info2 = pcg_solve(Hg, -gg, 1e-4)
+    po2, its2, _, _ = opcg(Ho, -go, 1e-4)
+    assert abs(info2.iterations - its2) <= 1
+    assert np.abs(p2 - po2).max() <= 1e-6 * np.abs(po2).max()
+    print(f"explicit blocks err {err_blocks:.1e}, pcg its {info.iterations}/{its}, p err {err_p:.1e}")
+
+
+def _squishy_press_state(fric, min_constraints, max_frames=160):
+    """A reduced squishy-ball press (scenes.squishy_scene: five 7.9k-tet balls
+    in the pinned box) stepped on the GPU until at least `min_constraints`
+    constraints are active."""
+    import torch
+    from paper_2512_12151_b200 import scenes
+    from paper_2512_12151_b200.contact import ActiveSet
+    from paper_2512_12151_b200.stepper import StepParams, step_device
+    system, state, params = scenes.squishy_scene(cell=0.01, n=8, stem=8, tip=4, plate_speed=2.0, plate_stop=0.12)
+    if fric:
+        params = StepParams(h=params.h, offset=params.offset, min_iterations=2, friction_coefficient=fric,
+                            eps_v=1e-3)
+    aset = ActiveSet()
+    aset.ensure(system.n_vertices)
+    x = torch.from_numpy(state.x).cuda()
+    v = torch.from_numpy(state.v).cuda()
+    ft = None
+    k = 0
+    while len(aset) < min_constraints:
+        assert k < max_frames, f"only {len(aset)} constraints after {k} frames"
+        x, v, d = step_device(x, v, system, aset, params, step_index=k, friction=ft)
+        ft = d.friction
+        k += 1
+    return system, params, aset, x, v, ft, k
+
+
+@pytest.mark.parametrize("fric", [0.0, 0.3])
+def test_production_pcg_path_subproblem_parity(pkg, fric):
+    """The PCG configuration of the C4 bench — one thread per row, several
+    row sweeps per thread with the last sweep dealt out by slices, residual
+    carried on chip, split phase-B barrier, contact (and friction) dots behind
+    the ld.acquire ready counter — on one AL subproblem of a squishy-ball
+    press state with >= 5k active constraints, vs the oracle
+    (intact/solver.py:178-233, intact/sparse.py:99-150).  The grid is capped
+    at 12 CTAs so each thread sweeps >= 4 rows.  Bars: equal Newton counts,
+    CG counts within 2x the oracle's own spread under a 1e-15 input
+    perturbation (or 2 %), positions within 4x that spread (or 1e-9 of the
+    step), identical gamma, multipliers within the propagated bound."""
+    from oracle import friction as ofriction
+    from paper_2512_12151_b200 import _lib
+    from paper_2512_12151_b200.device import to_dev, to_host
+    system, params, aset, x, v, ft, frames = _squishy_press_state(fric, 5000)
+    dev = system.device
+    xt, vt, h = to_host(x), to_host(v), params.h
+    x_tilde = xt + h * vt + (h * h) * np.array(params.gravity)
+    mu = params.stiffness_constant * dev.stiffness_diagonal_max(x, h)
+    x_hat0 = xt.copy()
+    for bc in system.boundary:
+        if bc.kind == "scripted":
+            x_hat0[bc.vertices] = bc.targets(None, frames)
+    st = aset.export_state()
+    fo = None
+    if fric:
+        assert ft is not None and len(ft) > 1000
+        fo = ofriction.FrictionSet(ft.indices, ft.weights, ft.frames, ft.coeff, ft.ref, ft.eps)
+    regions = [(r.material.model.value, r.material.mu, r.material.lam, r.tets, r.shape_rows, r.volumes)
+               for r in system.regions]
+
+    def oracle_run(xtil):
+        o = ocontact.ConstraintSet()
+        o._append(st[0], st[1], [ocontact.key_of(a, b) for a, b in zip(st[0], st[1])], lam=st[2].copy(),
+                  gamma=st[3].copy(), s=st[4].copy(), anchor_d=st[5], anchor_grad=st[6], anchor_x=st[7])
+        out = newton.subproblem(xtil, xt, x_hat0, system.masses, regions, o, mu, params.offset, h,
+                                dbc=system.dbc_mask, friction=fo)
+        return out, o
+
+    (xo, nwo, cgo, _, wo), o = oracle_run(x_tilde)
+    pert = x_tilde * (1.0 + 1e-15 * np.random.default_rng(1).standard_normal(x_tilde.shape))
+    (xo2, _, cgo2, _, _), _ = oracle_run(pert)
+    dev.set_friction(ft if fric else None)
+    xh = to_dev(x_hat0)
+    try:
+        with _lib.pcg_tuning(lanes_max_n=0, max_ctas=12):
+            nw, cg, _, w = dev.solve_subproblem(aset, to_dev(x_tilde), x, xh, mu, params.offset, h, params.cg_tol,
+                                                params.decay)
+            shape = _lib.pcg_last_shape()
+    finally:
+        dev.set_friction(None)
+    ctas, threads, sweeps, lanes, ready, terms = shape
+    assert lanes == 1 and ctas == 12 and sweeps >= 2 and ready == 1, shape
+    assert terms >= len(st[0]) + (len(ft) if fric else 0) >= 5000, shape
+    xg = to_host(xh)
+    step = np.abs(xo - x_hat0).max()
+    spread = np.abs(xo2 - xo).max()
+    err = np.abs(xg - xo).max()
+    print(f"\n[production PCG path, fric={fric}] frames {frames}, constraints {len(st[0])}, "
+          f"friction terms {len(ft) if fric else 0}, shape {shape}; Newton {nw}/{nwo}; CG {cg}/{cgo} "
+          f"(oracle spread {abs(cgo2 - cgo)}); max|dx| {err:.3e} = {err / step:.2e} of the step "
+          f"= {err / params.offset:.2e} of the offset; oracle spread {spread:.3e}")
+    assert nw == nwo
+    assert abs(cg - cgo) <= max(1, 2 * abs(cgo2 - cgo), int(0.02 * cgo)), (cg, cgo, cgo2)
+    assert err <= max(4.0 * spread, 1e-9 * step), (err, spread, step)
+    sg = aset.export_state()
+    assert np.array_equal(sg[3], o.gamma)
+    dc = 2.0 * np.sqrt(3.0) * err
+    assert np.abs(sg[2] - o.lam).max() <= mu * dc + 1e-12 * np.abs(o.lam).max()
+    assert abs(w - wo) <= dc + 1e-12 * abs(wo)
+
+
+def test_press_state_step_limit_and_update_on_identical_inputs(pkg):
+    """One outer pass's max_step_size and ActiveSet.update on a squishy-ball
+    press state with >= 5k constraints (intact/ccd.py:168-193,
+    intact/contact.py:179-205): fed identical (x, x_hat, blocking, resident
+    set), alpha is bit-equal, the blocking (kind, quad, TOI) sets are equal,
+    and the updated key sequences are identical."""
+    from paper_2512_12151_b200.ccd import BlockingPairs
+    from paper_2512_12151_b200.contact import ActiveSet
+    from paper_2512_12151_b200.device import to_dev, to_host
+    from oracle import geometry
+    system, params, aset, x, v, _, frames = _squishy_press_state(0.0, 5000)
+    xt = to_host(x)
+    # a trial x_hat: the inertial target, which moves every free vertex
+    x_hat = xt + params.h * to_host(v) + params.h ** 2 * np.array(params.gravity)
+    x_hat[system.dbc_mask] = xt[system.dbc_mask]
+    gap = 0.1 * params.offset
+    ccd = system.ccd
+    alpha = ccd.max_step_size(x, to_dev(x_hat), gap, 1.0)
+    bl = ccd.blocking()
+    ao, ok, oq, ot = geometry.step_limit(xt, x_hat, system.surface_triangles, system.surface_edges,
+                                         system.surface_vertices, gap)
+    assert alpha == ao
+    gset = {(int(a), tuple(b), c) for a, b, c in zip(bl.kinds, bl.indices.tolist(), bl.tois)}
+    assert gset == {(int(a), tuple(b), c) for a, b, c in zip(ok, oq.tolist(), ot)}
+    assert len(ot) > 100
+    st = aset.export_state()
+    o = ocontact.ConstraintSet()
+    o._append(st[0], st[1], [ocontact.key_of(a, b) for a, b in zip(st[0], st[1])], lam=st[2], gamma=st[3],
+              s=st[4], anchor_d=st[5], anchor_grad=st[6], anchor_x=st[7])
+    ga = ActiveSet()
+    ga.ensure(system.n_vertices)
+    ga.import_state(*st)
+    res_g = ga.update(BlockingPairs(ok, oq, ot))
+    res_o = o.update(ok, oq, ot)
+    gk, gq = ga.export_state()[:2]
+    print(f"\n[press pass] frames {frames}, resident {len(st[0])}, alpha {alpha:.6e}, blocking {len(ot)}, "
+          f"admitted/pruned GPU {res_g} oracle {res_o}, set size {len(gk)}")
+    assert tuple(res_g) == tuple(res_o)
+    assert np.array_equal(gk, np.asarray(o.kind)) and np.array_equal(gq, np.asarray(o.quad))
