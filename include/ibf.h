@@ -295,8 +295,23 @@ int ibf_system_spmv_stats(const ibf_system* s, double* bytes_per_spmv);
  * assembly count, PCG ms, PCG launches, CG iterations, line-search energy ms,
  * energy launches, inversion-cap ms, sum over PCG launches of C x iterations. */
 int ibf_system_stats(ibf_system* s, double* out, int reset);
+/* Operation counts since the last reset: out[0] = Newton iterations of
+ * ibf_solve_subproblem, out[1] = energy evaluations the reference's sequential
+ * line search makes for the same iterations (base + trials up to the first
+ * strict decrease, intact/solver.py:159-175) — the bench's CPU cost model. */
+int ibf_system_counts(ibf_system* s, double* out, int reset);
 /* CCD phase: out[0..2] = max_step_size device ms, calls, broad-phase candidates. */
 int ibf_ccd_stats(ibf_ccd* c, double* out, int reset);
+/* Per-kernel device clocks (roofline bookkeeping; no reference counterpart).
+ * on: 1 starts bracketing the instrumented launches with events on their
+ * stream, 0 stops, < 0 leaves the state.  out (may be NULL) receives 7 rows
+ * of 5 doubles — ms, launches, algorithmic bytes, algorithmic flops, units —
+ * for k_elem, k_gather_blocks, k_vertex_rows, k_energy, k_traverse,
+ * k_pair_toi, k_pcg (units: tets, blocks, vertices, trial points, candidate
+ * pairs, narrow-phase pairs, -); pending events are harvested first (waits
+ * for them).  reset != 0 zeroes the counters after reading. */
+int ibf_kernel_clocks(int on, double* out, int reset);
+
 /* Number of kernels libibf has launched in this process (CUB internals excluded). */
 unsigned long long ibf_launch_count(void);
 

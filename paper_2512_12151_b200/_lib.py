@@ -87,6 +87,8 @@ _PROTOS = {
     "ibf_bsr_export": (_int, [_vp, _vp, _vp, _vp, _vp]),
     "ibf_pcg_tuning": (_int, [_i64, _int]),
     "ibf_pcg_last_shape": (_int, [_vp]),
+    "ibf_kernel_clocks": (_int, [_int, _vp, _int]),
+    "ibf_system_counts": (_int, [_vp, _vp, _int]),
     "ibf_system_export_terms": (_int, [_vp, _pi64, _vp, _vp, _vp, _vp]),
 }
 
@@ -143,6 +145,17 @@ def dev_ptr(t):
 def stream():
     import torch
     return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+KERNEL_CLOCKS = ("k_elem", "k_gather_blocks", "k_vertex_rows", "k_energy", "k_traverse", "k_pair_toi", "k_pcg")
+
+
+def kernel_clocks(on=-1, reset=False):
+    """{kernel: {ms, launches, bytes, flops, units}} from ibf_kernel_clocks."""
+    out = np.zeros(5 * len(KERNEL_CLOCKS))
+    check(lib().ibf_kernel_clocks(int(on), host_ptr(out), 1 if reset else 0), "ibf_kernel_clocks")
+    return {k: dict(zip(("ms", "launches", "bytes", "flops", "units"), out[5 * i:5 * i + 5].tolist()))
+            for i, k in enumerate(KERNEL_CLOCKS)}
 
 
 def pcg_last_shape():

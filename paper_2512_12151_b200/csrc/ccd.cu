@@ -505,11 +505,18 @@ static int broad_pass(ibf_ccd* c, int kind, const double* x0, const double* x1, 
     a.out = c->pairs.p;
     a.cap = c->pairs.cap;
     a.counters = c->counters.p;
-    k_traverse<<<grid_for(nq, 128), 128, 0, s>>>(a);
-    IBF_LAUNCH_CHECK();
     unsigned long long* h = (unsigned long long*)c->host.p;
-    IBF_CUDA(cudaMemcpyAsync(h, c->counters.p, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
-    IBF_CUDA(cudaStreamSynchronize(s));
+    {
+      // algorithmic: 48 B per query box + 48 B per primitive box (each leaf
+      // read once) + 16 B per candidate pair out (booked after the count)
+      KernelClock kc(KC_TRAVERSE, s, 48.0 * (nq + tree.n), 0.0, 0.0);
+      k_traverse<<<grid_for(nq, 128), 128, 0, s>>>(a);
+      IBF_LAUNCH_CHECK();
+      IBF_CUDA(cudaMemcpyAsync(h, c->counters.p, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+      IBF_CUDA(cudaStreamSynchronize(s));
+      kc.bytes += 16.0 * (double)h[1];
+      kc.units = (double)h[1];
+    }
     *count = (int64_t)h[0];
     *n_candidates = (int64_t)h[1];
     if (h[0] <= c->pairs.cap) break;
@@ -660,6 +667,8 @@ extern "C" int ibf_max_step_size(ibf_ccd* c, const double* x, const double* x_ha
     if (cnt[kind]) {
       IBF_TRY(quads[kind].reserve(4 * cnt[kind]));
       IBF_TRY(tois[kind].reserve(cnt[kind]));
+      // algorithmic: 4 vertices x (x, x_hat) 192 B + quad 16 B in, TOI 8 B out per pair
+      KernelClock kc(KC_TOI, s, 216.0 * cnt[kind], 0.0, (double)cnt[kind]);
       k_pair_toi<<<grid_for(cnt[kind], 128), 128, 0, s>>>(
           cnt[kind], kind, c->pairs_sorted.p, kind == 0 ? c->verts.p : c->edges.p, kind == 0 ? c->tris.p : c->edges.p,
           x, x_hat, min_gap, tois[kind].p, quads[kind].p);

@@ -75,6 +75,34 @@ struct PhaseTimer {
   }
 };
 
+// Per-kernel device clocks for the roofline lines of the bench
+// (ibf_kernel_clocks): when switched on, a KernelClock scope brackets one
+// launch with an event pair on its stream and books the launch's ALGORITHMIC
+// bytes and flops (computed at the launch site from the
+// sizes it processes).  Events are harvested when the clocks are read.  Off:
+// one relaxed atomic load per launch.
+enum KernelClockId {
+  KC_ELEM = 0,      // k_elem: F, energy, PK1, SVD/eigen, 10 PSD blocks per tet
+  KC_GATHER,        // k_gather_blocks: staging -> BSR slots
+  KC_ROWS,          // k_vertex_rows: gradient rows, contact diagonal, Jacobi inverse
+  KC_ENERGY,        // k_energy: incremental potential at up to 8 trial points
+  KC_TRAVERSE,      // k_traverse: LBVH queries + fused ACCD prefilter
+  KC_TOI,           // k_pair_toi: ACCD narrow phase on the survivors
+  KC_PCG,           // k_pcg: one persistent PCG solve
+  KC_COUNT
+};
+extern std::atomic<bool> g_kclock_on;
+struct KernelClock {
+  int id;
+  cudaStream_t s;
+  cudaEvent_t b = nullptr;
+  double bytes, flops, units;
+  KernelClock(int id_, cudaStream_t s_, double bytes_, double flops_ = 0.0, double units_ = 0.0);
+  ~KernelClock();
+  KernelClock(const KernelClock&) = delete;
+  KernelClock& operator=(const KernelClock&) = delete;
+};
+
 // Opt-in host-side phase trace (IBF_TRACE=1): synchronises the stream at
 // each mark and prints the elapsed wall time per phase to stderr.  Off by
 // default; a dev tool for finding host/device stalls, never on the timed path.

@@ -17,6 +17,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <ctime>
 #include <string>
 
@@ -70,6 +71,81 @@ void dev_free(void* p) {
 }
 
 thread_local cudaStream_t tl_stream = 0;
+
+// ------------------------------------------------------- per-kernel clocks
+std::atomic<bool> g_kclock_on{false};
+namespace {
+struct KcPending {
+  cudaEvent_t b, e;
+  double bytes, flops, units;
+};
+struct KcTable {
+  std::mutex m;
+  std::vector<cudaEvent_t> pool;
+  std::vector<KcPending> pending[KC_COUNT];
+  double ms[KC_COUNT] = {}, bytes[KC_COUNT] = {}, flops[KC_COUNT] = {}, units[KC_COUNT] = {};
+  long long launches[KC_COUNT] = {};
+  cudaEvent_t get() {
+    if (pool.empty()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      return e;
+    }
+    cudaEvent_t e = pool.back();
+    pool.pop_back();
+    return e;
+  }
+  void harvest(bool wait) {
+    for (int k = 0; k < KC_COUNT; ++k) {
+      auto& v = pending[k];
+      size_t keep = 0;
+      for (size_t j = 0; j < v.size(); ++j) {
+        KcPending& q = v[j];
+        if (!wait && cudaEventQuery(q.e) != cudaSuccess) {
+          v[keep++] = q;
+          continue;
+        }
+        cudaEventSynchronize(q.e);
+        float t = 0.0f;
+        if (cudaEventElapsedTime(&t, q.b, q.e) == cudaSuccess) {
+          ms[k] += t;
+          bytes[k] += q.bytes;
+          flops[k] += q.flops;
+          units[k] += q.units;
+          ++launches[k];
+        }
+        pool.push_back(q.b);
+        pool.push_back(q.e);
+      }
+      v.resize(keep);
+    }
+    cudaGetLastError();
+  }
+};
+KcTable& kc_table() {
+  static KcTable t;
+  return t;
+}
+}  // namespace
+
+KernelClock::KernelClock(int id_, cudaStream_t s_, double bytes_, double flops_, double units_)
+    : id(id_), s(s_), bytes(bytes_), flops(flops_), units(units_) {
+  if (!g_kclock_on.load(std::memory_order_relaxed)) return;
+  KcTable& t = kc_table();
+  std::lock_guard<std::mutex> lk(t.m);
+  b = t.get();
+  cudaEventRecord(b, s);
+}
+
+KernelClock::~KernelClock() {
+  if (!b) return;
+  KcTable& t = kc_table();
+  std::lock_guard<std::mutex> lk(t.m);
+  cudaEvent_t e = t.get();
+  cudaEventRecord(e, s);
+  t.pending[id].push_back({b, e, bytes, flops, units});
+  if (t.pending[id].size() > 512) t.harvest(false);
+}
 
 void alloc_report(const char* what, size_t bytes, double t0) {
   const double ms = 1e3 * (wall_now() - t0);
@@ -193,6 +269,27 @@ int contacts_dual(ibf_contacts* c, const double* x_hat, double offset, double mu
 }  // namespace ibf
 
 using namespace ibf;
+
+extern "C" int ibf_kernel_clocks(int on, double* out, int reset) {
+  KcTable& t = kc_table();
+  std::lock_guard<std::mutex> lk(t.m);
+  t.harvest(true);
+  if (out)
+    for (int k = 0; k < KC_COUNT; ++k) {
+      out[5 * k + 0] = t.ms[k];
+      out[5 * k + 1] = (double)t.launches[k];
+      out[5 * k + 2] = t.bytes[k];
+      out[5 * k + 3] = t.flops[k];
+      out[5 * k + 4] = t.units[k];
+    }
+  if (reset)
+    for (int k = 0; k < KC_COUNT; ++k) {
+      t.ms[k] = t.bytes[k] = t.flops[k] = t.units[k] = 0.0;
+      t.launches[k] = 0;
+    }
+  if (on >= 0) g_kclock_on.store(on != 0);
+  return IBF_OK;
+}
 
 extern "C" const char* ibf_version(void) { return "ibf-b200 0.1 (sm_100a)"; }
 extern "C" const char* ibf_last_error(void) { return g_err.c_str(); }
@@ -321,6 +418,9 @@ extern "C" int ibf_solve_subproblem(ibf_system* s, ibf_contacts* c, const double
     const double rfirst = hd[8];
     double r = rfirst, e_acc = hd[0];
     bool stall = false;
+    // the reference evaluates the base energy and then trials r0, r0/2, ...
+    // until the first strict decrease (intact/solver.py:159-175)
+    long long ref_trials = 1;
     if (!(hd[0] < base)) {
       // backtracking: r0 / 2^k, k = 1..30, strict decrease (intact/solver.py:159-175)
       double best_r = rfirst, best_e = INFINITY;
@@ -347,6 +447,7 @@ extern "C" int ibf_solve_subproblem(ibf_system* s, ibf_contacts* c, const double
         s->t_ls.harvest();
         for (int j = 0; j < T2; ++j) {
           const double rj = rfirst * rs[j];
+          ++ref_trials;
           if (hd[j] < base) {
             r = rj;
             e_acc = hd[j];
@@ -368,6 +469,8 @@ extern "C" int ibf_solve_subproblem(ibf_system* s, ibf_contacts* c, const double
     }
     k_step<<<grid_for(n3), 256, 0, stream>>>(n3, r, p, x_hat);
     IBF_LAUNCH_CHECK();
+    s->ref_energy_evals += 1 + ref_trials;
+    ++s->newton_iters;
     base = e_acc;
     have_base = e_acc < INFINITY;  // stalled on all-inf trials: recompute next time
     ++newton;
@@ -434,6 +537,13 @@ extern "C" int ibf_system_stats(ibf_system* s, double* out, int reset) {
     s->pcg_iters = 0;
     s->contact_terms = 0;
   }
+  return IBF_OK;
+}
+
+extern "C" int ibf_system_counts(ibf_system* s, double* out, int reset) {
+  out[0] = (double)s->newton_iters;
+  out[1] = (double)s->ref_energy_evals;
+  if (reset) s->newton_iters = s->ref_energy_evals = 0;
   return IBF_OK;
 }
 

@@ -628,6 +628,12 @@ __global__ void k_diag_max(int64_t n, const int* __restrict__ diag_q, const doub
 
 // ------------------------------------------------------------ host side
 
+// FP64 flops per tet of k_elem, frozen from ncu (2 x DFMA + DMUL + DADD
+// thread instructions per tet, COR model; profiles/).
+// The reference's own counter gives 927 multiplies per tet for the 10-block
+// PSD part alone (tests/test_elasticity.py:381-420).
+constexpr double kFlopPerTet = 0.0;
+
 int system_assemble(ibf_system* s, ibf_contacts* c, const double* x_hat, const double* x_tilde, double mu,
                     double offset, double h, bool apply_dbc, double* grad, bool contacts_ready,
                     cudaStream_t st) {
@@ -636,10 +642,15 @@ int system_assemble(ibf_system* s, ibf_contacts* c, const double* x_hat, const d
   if (s->m) {
     ElemArgs a{s->m, s->n_tiles, s->tets.p, s->shape_rows.p, s->volumes.p, s->regions.p, s->n_regions, x_hat, h2,
                s->elem_grad.p, s->elem_blk.p, s->flags.p};
+    // algorithmic: tet data 120 B + x once; FLOP_PER_TET
+    KernelClock kc(KC_ELEM, st, 120.0 * s->m + 24.0 * s->n, kFlopPerTet * s->m, (double)s->m);
     k_elem<true><<<(int)div_up(s->n_tiles, ELEM_THREADS / 32), ELEM_THREADS, 0, st>>>(a);
     IBF_LAUNCH_CHECK();
   }
   const uint8_t* mask = (apply_dbc && s->any_dbc) ? s->dbc.p : nullptr;
+  // algorithmic: one 72 B write per stored block (N + E_u) — the staging
+  // round trip k_elem -> k_gather_blocks is not algorithmic traffic
+  KernelClock kcg(KC_GATHER, st, 72.0 * s->pat.nb, 0.0, (double)s->pat.nb);
   k_gather_blocks<<<(int)std::min<int64_t>(div_up(s->pat.nq, 256), 148LL * 32), 256, 0, st>>>(
       s->pat.nq, s->pat.qrow.p, s->pat.col.p, s->pat.qreal.p, s->blk_ptr.p, s->blk_src.p, s->elem_blk.p,
       s->masses.p, mask, s->pat.val.p);
@@ -666,6 +677,8 @@ int system_assemble(ibf_system* s, ibf_contacts* c, const double* x_hat, const d
   RowArgs r{s->n, x_hat, x_tilde, s->masses.p, mask, s->vt_ptr.p, s->vt_src.p, s->elem_grad.p,
             s->pat.diag_q.p, s->pat.val.p, cv, coef_g, fv, fr_gw, grad, s->pinv.p, s->flags.p};
   if (s->n) {
+    // algorithmic: x_tilde 24 + mass 8 + grad 24 per vertex, 232 B per constraint
+    KernelClock kc(KC_ROWS, st, 56.0 * s->n + 232.0 * cv.n, 0.0, (double)s->n);
     k_vertex_rows<<<(int)std::min<int64_t>(div_up(s->n, 256), 148LL * 32), 256, 0, st>>>(r);
     IBF_LAUNCH_CHECK();
   }
@@ -724,8 +737,13 @@ int system_energy_launch(ibf_system* s, ibf_contacts* c, const double* x_hat, co
   }
   IBF_TRY(s->epart.reserve((size_t)(a.bv + a.bt + a.bc + a.bf) * MAXT));
   a.part = s->epart.p;
-  k_energy<<<a.bv + a.bt + a.bc + a.bf, 256, 0, st>>>(a);
-  IBF_LAUNCH_CHECK();
+  {
+    // algorithmic: 120 B/tet + x_hat, p, x_tilde, mass (80 B/vertex) + 232 B per
+    // constraint, read once for all n_r trial points
+    KernelClock kc(KC_ENERGY, st, 120.0 * s->m + 80.0 * s->n + 232.0 * a.nc, 0.0, (double)n_r);
+    k_energy<<<a.bv + a.bt + a.bc + a.bf, 256, 0, st>>>(a);
+    IBF_LAUNCH_CHECK();
+  }
   k_energy_final<<<1, 32 * MAXT, 0, st>>>(s->epart.p, n_r, a.bv, a.bt, a.bc, a.bf, h * h, out_dev);
   IBF_LAUNCH_CHECK();
   return IBF_OK;

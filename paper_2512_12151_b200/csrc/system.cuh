@@ -36,6 +36,8 @@ struct ibf_system {
   ibf::PhaseTimer t_asm, t_pcg, t_ls, t_cap;
   long long pcg_iters = 0;       // CG iterations since the last stats reset
   long long contact_terms = 0;   // sum over PCG launches of C (matrix-free contact)
+  long long ref_energy_evals = 0;  // energy evaluations the reference's sequential line search makes
+  long long newton_iters = 0;      // Newton iterations since the last stats reset
   ibf_contacts* assembled_contacts = nullptr;  // contact term of the last assembly
   ibf_friction* friction = nullptr;            // frozen friction terms (ibf_system_set_friction)
   bool assembled_friction = false;

@@ -330,7 +330,7 @@ def c4_scene(n=42, radius=0.1, gap=0.001, plate_speed=0.1, h=0.01, layers=None, 
     return system, state, params
 
 
-def squishy_scene(cell=0.01, n=32, stem=23, tip=16, shell=2, gap=None, plate_speed=1.0, plate_stop=None, h=0.01,
+def squishy_scene(cell=0.02, n=32, stem=23, tip=16, shell=2, gap=None, plate_speed=1.0, plate_stop=None, h=0.01,
                   walls=True, seed=7, balls=5):
     """C4, paper-scale: five squishy balls in a box, pressed by a plate.
 
@@ -339,12 +339,14 @@ def squishy_scene(cell=0.01, n=32, stem=23, tip=16, shell=2, gap=None, plate_spe
     balls, within 3 % of the paper's 2.25M / 0.87M / 1.59M),
     COR with the paper's rho 1e2, E 1e4, nu 0.4, h = 0.01, offset 1e-3,
     K_min 2.  Each ball gets a seeded random rotation so no strands of two
-    balls are aligned.  Four balls sit in a 2x2 square on a pinned floor and
-    the fifth in the pocket above; four pinned walls (with slits between
-    them, as in c2_scene) hold the stack, and a scripted plate starts one
-    gap above it and moves down at plate_speed, holding once its underside
-    reaches plate_stop (the container shrinking to a minimum height,
-    PAPER.md:596).
+    balls are aligned.  Four balls rest one gap above a pinned floor in a
+    2x2 square and the fifth in the pocket above; four pinned walls (with
+    slits between them, as in c2_scene) hold the stack, and a scripted plate
+    starts one gap above it and moves down at plate_speed, holding once its
+    underside reaches plate_stop (the container shrinking to a minimum
+    height, PAPER.md:596).  Physical scale: `cell` is the strand cell edge;
+    2 cm puts block-Jacobi PCG at ~90-110 CG iterations per solve (the
+    paper's average is 28, its peak 146), see DESIGN.md.
     """
     rng = np.random.default_rng(seed)
     base = squishy_ball(n=n, shell=shell, stem=stem, tip=tip, cell=cell)
@@ -352,13 +354,18 @@ def squishy_scene(cell=0.01, n=32, stem=23, tip=16, shell=2, gap=None, plate_spe
     gap = 2.0 * cell if gap is None else gap
     mat = Material(MaterialModel.COR, 1e4, 0.4)
     rho = 1e2
+    rots = [rotation_matrix(rng.standard_normal(3), rng.uniform(-np.pi, np.pi)) for _ in range(balls)]
     c = R + gap / 2
-    z0 = R + gap
-    centers = [(-c, -c, z0), (c, -c, z0), (-c, c, z0), (c, c, z0)]
+    # the bottom four rest one gap above the floor (lowest vertex), the fifth
+    # sits in their pocket, its bounding sphere one gap above theirs
+    lows = [float((base.rest_positions @ Rm.T)[:, 2].min()) for Rm in rots]
+    centers = [(-c, -c, gap - lows[0]), (c, -c, gap - lows[1]), (-c, c, gap - lows[2]), (c, c, gap - lows[3])]
+    z0 = max(ct[2] for ct in centers[:4])
     dz = np.sqrt((2 * R + gap) ** 2 - 2 * c * c)
     centers.append((0.0, 0.0, z0 + dz + gap))
     centers = centers[:balls]
-    top = max(ct[2] for ct in centers) + R + gap
+    meshes = [transformed(base, translate=ct, rotate=Rm) for ct, Rm in zip(centers, rots)]
+    top = max(float(m.rest_positions[:, 2].max()) for m in meshes) + gap
     half = 2 * R + 2 * gap                      # inner half-width of the box
     wall, slit = 4 * cell, 2 * cell
     pc = 8                                      # wall / plate cells per ~8 ball cells
@@ -376,9 +383,8 @@ def squishy_scene(cell=0.01, n=32, stem=23, tip=16, shell=2, gap=None, plate_spe
             bodies.append(_pinned_slab((sx, sy, height), (cx, cy, slit),
                                        (1 if sx == wall else nc, 1 if sy == wall else nc, hc), mat.young, rho, cell))
         n_fixed = 5
-    for ct in centers:
-        Rm = rotation_matrix(rng.standard_normal(3), rng.uniform(-np.pi, np.pi))
-        bodies.append((transformed(base, translate=ct, rotate=Rm), mat, rho, (0.0, 0.0, 0.0)))
+    for m in meshes:
+        bodies.append((m, mat, rho, (0.0, 0.0, 0.0)))
     pl = half - slit
     bodies.append(_pinned_slab((2 * pl, 2 * pl, wall), (-pl, -pl, top), (nc, nc, 1), mat.young, rho, cell))
     stop = None

@@ -242,8 +242,10 @@ class AssembledMatrix:
             rows, cols, blocks = self.dev.export_bsr()
             tr, tc, tb = self.dev.export_terms()
             if self._dbc is not None and len(tr):
-                keep = ~(self._dbc[tr] | self._dbc[tc])          # intact/sparse.py:81-87
-                tr, tc, tb = tr[keep], tc[keep], tb[keep]
+                # intact/sparse.py:81-87 zeroes (and keeps) every block touching a
+                # masked vertex; the masked diagonals are already mass * I
+                tb = tb.copy()
+                tb[self._dbc[tr] | self._dbc[tc]] = 0.0
             self._explicit = BlockSparseMatrix(self.n_vertices, np.concatenate([rows, tr]),
                                                np.concatenate([cols, tc]), np.concatenate([blocks, tb]))
         return self._explicit

@@ -32,6 +32,10 @@ ap.add_argument("--plate-stop", type=float, default=None)
 ap.add_argument("--certify", action="store_true")
 ap.add_argument("--every", type=int, default=1, help="print every k-th frame")
 ap.add_argument("--out", default=None)
+ap.add_argument("--dump", default=None, help="save (x, v, active set, frame) after the last frame to this .npz")
+ap.add_argument("--load", default=None, help="start from a --dump file instead of the scene's rest state")
+ap.add_argument("--profile-frames", type=int, default=0,
+                help="run the last k frames inside cudaProfilerStart/Stop (ncu --profile-from-start off)")
 args = ap.parse_args()
 
 t = time.perf_counter()
@@ -45,6 +49,12 @@ aset = ActiveSet()
 aset.ensure(system.n_vertices)
 ccd = system.ccd
 x, v = to_dev(state.x), to_dev(state.v)
+k0 = 0
+if args.load:
+    z = np.load(args.load)
+    x, v, k0 = to_dev(z["x"]), to_dev(z["v"]), int(z["frame"])
+    aset.import_state(*(z[f"a{j}"] for j in range(8)))
+    print(json.dumps({"loaded": args.load, "frame": k0, "constraints": len(aset)}), flush=True)
 if args.certify:
     n_hits, _ = ccd.static_intersections(x, cap=16)
     dmin, _, _ = ccd.min_distance(x, params.offset)
@@ -54,7 +64,10 @@ from paper_2512_12151_b200 import _lib
 L = _lib.lib()
 dev = system.device
 free = torch.from_numpy(~system.dbc_mask).cuda()
-for k in range(args.frames):
+for k in range(k0, k0 + args.frames):
+    if args.profile_frames and k == k0 + args.frames - args.profile_frames:
+        torch.cuda.synchronize()
+        torch.cuda.profiler.start()
     stats, cst = np.zeros(9), np.zeros(3)
     L.ibf_system_stats(dev.handle, _lib.host_ptr(stats), 1)
     L.ibf_ccd_stats(ccd.handle, _lib.host_ptr(cst), 1)
@@ -80,6 +93,13 @@ for k in range(args.frames):
     rows.append(row)
     if k % args.every == 0 or k == args.frames - 1:
         print(json.dumps(row), flush=True)
+if args.profile_frames:
+    torch.cuda.synchronize()
+    torch.cuda.profiler.stop()
+if args.dump:
+    st = aset.export_state()
+    np.savez(args.dump, x=x.cpu().numpy(), v=v.cpu().numpy(), frame=k0 + args.frames,
+             **{f"a{j}": a for j, a in enumerate(st)})
 ms = np.array([r["ms"] for r in rows])
 summary = {"frames": len(rows), "mean_ms": float(ms.mean()), "max_ms": float(ms.max()),
            "mean_newton": float(np.mean([r["newton"] for r in rows])),
