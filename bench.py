@@ -1,27 +1,31 @@
 """Benchmark: ms/frame on the C4 squishy-ball compression scene (BASELINE.json).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--n 112]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload c4|c4ball|c5] [--precompress P] [--cell 0.02] [--plate-speed 2.0]
 
 One "step" is one frame (= one Simulation.advance, intact/cli.py:98-116) of
-the 2.22M-tet five-ball compression scene (solid-ball
-proxy — see paper_2512_12151_b200/scenes.py and DESIGN.md).  The press runs
---precompress untimed frames first (default 50: the stack is squeezed to
-~40 % of its height, 20-30k active constraints, ~20 Newton iterations per
-frame), then W untimed warm-up frames, then K timed frames.  Per timed frame the inputs (x, v) are copied
-host->device from pinned memory, the frame runs through the public
-Simulation/step path, and (x, v) are copied back; `value` is the device time
-of the frame proper (inputs resident), `e2e` the whole bracket including the
-copies.  The matrix alone is ~0.5 GB, far above the 126 MB L2, so no flush
+the C4 scene: five squishy balls (scenes.squishy_scene: 2.30M tets, 0.90M
+vertices, 1.62M surface triangles — the paper's 2.25M / 0.87M / 1.59M,
+PAPER.md:810) in a pinned box under gravity, pressed by a scripted plate.
+The press runs --precompress untimed frames first (default 40: the stack is
+in dense multi-body contact, >1e5 active constraints), then W untimed
+warm-up frames, then K timed frames.  Per timed frame the inputs (x, v) are
+copied host->device from pinned memory, the frame runs through the public
+step path, and (x, v) are copied back; `value` is the device time of the
+frame proper (inputs resident), `e2e` the whole bracket including the
+copies.  The matrix alone is ~0.6 GB, far above the 126 MB L2, so no flush
 is needed between frames.
 
-Multi-GPU (torchrun): a single scene does not shard in this round, so each
-rank runs an independent replica ("replicas only"); value = max
-over ranks of the timed region / (N*K) frames, scaling "weak".
+--workload c4ball is the round-1 solid-ball proxy (same tet count, 0.40M
+vertices, 0.11M surface triangles); --workload c5 the scene-parallel batch.
 
---impl reference times the reference's CPU algorithm (the oracle
-restatement, oracle/) on the host cores: unit costs of its hot-path stages
-(assemble, PCG iteration, energy, CCD pass) measured on one reduced shell,
-scaled to the C4 size and to the per-frame operation counts.
+Multi-GPU (torchrun): one scene per rank ("replicas only", DESIGN.md §(e));
+value = the slowest rank's ms/frame, and `replica_scene_frames_per_s` the
+replicas' throughput.
+
+--impl reference times the reference's CPU path as the oracle port (oracle/,
+single-threaded numpy) on bounded samples of the same scene
+(oracle/stage_timing.py); see run_reference.
 """
 
 from __future__ import annotations
@@ -43,10 +47,20 @@ METRIC = "ms/frame and ms/Newton iter (squishy balls 2.25M tets); PCG SpMV HBM G
 PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 COUNTS = os.path.join(ROOT, "profiles", "c4_frame_counts.json")
 NCU_SUMMARY = os.path.join(ROOT, "profiles", "ncu_summary.json")
-PLATE_SPEED = 0.5   # m/s: 5 mm per frame
-PLATE_STOP = 0.05   # m: the press holds once its underside reaches this height (stack 0.345 m tall)
 PAPER_COUNTS = {"newton": 30.09, "cg": 30.09 * 28.35, "passes": 30.09, "energy": 30.09 * 1.5,
                 "source": "PAPER.md:694 (Newton 30.09/frame, CG 28.35/solve); passes and energy evals assumed"}
+
+
+def _fp64_peak():
+    """Measured FP64 FMA throughput (TFLOP/s) from MEASURED_PEAKS.json or the
+    committed tools/micro/fp64_peak run, else None."""
+    for path, key in ((PEAKS, "fp64_tflops"), (os.path.join(ROOT, "profiles", "fp64_peak.json"), "fp64_tflops")):
+        try:
+            with open(path) as f:
+                return float(json.load(f)[key])
+        except Exception:
+            pass
+    return None
 
 
 def _peaks():
@@ -163,103 +177,128 @@ def _dist():
 
 # ------------------------------------------------------------------ CPU baseline
 
-def reference_unit_costs(n_sample=16, seed=0):
-    """Time the reference algorithm's stages (oracle restatement) on one
-    ball of resolution n_sample, in a strained configuration."""
-    from oracle import blocksparse, geometry, newton
+COUNT_KEYS = ("newton", "cg", "passes", "energy")
+
+
+def _scene(args):
     from paper_2512_12151_b200 import scenes
-    ball = scenes.shell_sphere(n_sample, 0.1, layers=(n_sample + 1) // 2)
-    from paper_2512_12151_b200.mesh import compute_rest_data
-    rest = compute_rest_data(ball, 1e2)
-    from paper_2512_12151_b200.elasticity import Material, MaterialModel
-    mat = Material(MaterialModel.COR, 1e4, 0.4)
-    R = [("cor", mat.mu, mat.lam, ball.tets, rest.shape_rows, rest.volumes)]
-    rng = np.random.default_rng(seed)
-    x = ball.rest_positions * np.array([1.0, 1.0, 0.97])          # squashed: nonzero elastic forces
-    x_tilde = ball.rest_positions + 1e-4 * rng.standard_normal(x.shape)
-    h = 0.01
-    t = time.perf_counter()
-    g, H = newton.assemble(x, x_tilde, rest.masses, R, None, 1.0, 1e-3, h)
-    t_asm = time.perf_counter() - t
-    t = time.perf_counter()
-    _, its, _, _ = blocksparse.pcg(H, -g, 1e-12, max_iters=20)
-    t_cg = (time.perf_counter() - t) / max(its, 1)
-    t = time.perf_counter()
-    newton.energy(x, x_tilde, rest.masses, R, None, 1.0, 1e-3, h)
-    t_en = time.perf_counter() - t
-    x_hat = x + 2e-3 * rng.standard_normal(x.shape)
-    t = time.perf_counter()
-    geometry.step_limit(x, x_hat, ball.surface_tris, ball.surface_edges, ball.surface_verts, 1e-4)
-    t_ccd = time.perf_counter() - t
-    return {"assemble_s": t_asm, "cg_iter_s": t_cg, "energy_s": t_en, "ccd_pass_s": t_ccd,
-            "tets": int(ball.n_tets), "blocks": int(len(H.rows)), "tris": int(len(ball.surface_tris)),
-            "n_sample": n_sample}
-
-
-def reference_ms_per_frame(units, full, counts):
-    """Scale sampled unit costs to the full scene and per-frame op counts."""
-    st = units["tets"] / 1.0
-    s_asm = full["tets"] / st
-    s_cg = full["blocks"] / units["blocks"]
-    s_ccd = full["tris"] / units["tris"]
-    asm = units["assemble_s"] * s_asm * (counts["newton"] + 1.0)      # + mu-init assembly per frame
-    cg = units["cg_iter_s"] * s_cg * counts["cg"]
-    en = units["energy_s"] * s_asm * counts["energy"]
-    ccd = units["ccd_pass_s"] * s_ccd * counts["passes"]
-    return 1e3 * (asm + cg + en + ccd), {"assemble_ms": 1e3 * asm, "pcg_ms": 1e3 * cg, "energy_ms": 1e3 * en,
-                                         "ccd_ms": 1e3 * ccd}
-
-
-def _full_sizes(n):
-    """Five solid n-balls (Kuhn grid): tets, surface tris, vertices."""
-    return {"tets": 5 * 6 * n ** 3, "tris": 5 * 12 * n * n, "verts": 5 * (n + 1) ** 3}
+    if args.workload == "c4ball":
+        return scenes.c4_scene(n=args.n, plate_speed=0.5, plate_stop=0.05)
+    return scenes.squishy_scene(cell=args.cell, plate_speed=args.plate_speed)
 
 
 def workload(args):
     """The config.workload string shared by both arms (same scene, same frames)."""
-    full = _full_sizes(args.n)
     first = args.precompress + args.warmup
-    return (f"C4 five COR balls n={args.n} ({full['tets']} ball tets, {full['verts']} ball vertices) pressed by a "
-            f"plate at {PLATE_SPEED} m/s down to {PLATE_STOP} m; timed frames {first}..{first + args.steps - 1}")
+    frames = f"timed frames {first}..{first + args.steps - 1} after {first} untimed"
+    if args.workload == "c4ball":
+        return (f"C4 solid-ball proxy: five COR balls n={args.n} ({5 * 6 * args.n ** 3} ball tets) pressed by a "
+                f"plate at 0.5 m/s down to 0.05 m; {frames}")
+    return (f"C4 squishy balls: five COR squishy balls (hollow core + 600 strands each, scenes.squishy_scene "
+            f"cell={args.cell} m: 2.30M tets, 0.90M vertices, 1.62M surface triangles) in a pinned box, pressed "
+            f"by a plate at {args.plate_speed} m/s under gravity; {frames}")
+
+
+def _oracle_counts(counts_path=None):
+    """Per-frame op counts of the last committed GPU run of this workload."""
+    try:
+        with open(counts_path or COUNTS) as f:
+            c = json.load(f)
+        return {k: float(c[k]) for k in COUNT_KEYS}, f"per-frame op counts of the GPU run in {os.path.relpath(COUNTS, ROOT)}"
+    except Exception:
+        return ({k: float(v) for k, v in PAPER_COUNTS.items() if k in COUNT_KEYS}, PAPER_COUNTS["source"])
+
+
+def cpu_sample(system, x, x_hat, x_tilde, mu, offset, h, slices, aset_state, counts, full_blocks):
+    """Oracle stage times on the given ball slices (+ the full active set),
+    scaled to the scene and multiplied by the per-frame op counts."""
+    from oracle import stage_timing
+    meas_tot, full_tot, infos = {}, {}, []
+    for j, sl in enumerate(slices):
+        meas, scale, full, info = stage_timing.time_sample(system, x, x_hat, x_tilde, mu, offset, h, sl,
+                                                            aset_state if j == 0 else None,
+                                                            full_blocks=full_blocks, contacts=(j == 0))
+        for k, v in meas.items():
+            meas_tot[k] = meas_tot.get(k, 0.0) + v
+        for k, v in full.items():
+            # slice stages: mean over slices; full-set contact stages: once
+            full_tot[k] = full_tot.get(k, 0.0) + (v / len(slices) if scale[k] != 1.0 or k == "cg_setup" else v)
+        infos.append(info)
+    ms, parts = stage_timing.frame_ms(full_tot, counts)
+    return ms, parts, meas_tot, full_tot, infos
 
 
 def run_reference(args):
+    """--impl reference: the oracle port of the reference's CPU path (oracle/,
+    single-threaded numpy like the reference), no GPU.  Each step times one
+    bounded sample of the same scene at its first frame (the rest state, the
+    plate's first-frame Dirichlet target, gravity): a 1/8 slice of one ball
+    (assembly, CG iterations, energy, CCD over the slice's surface), scaled to
+    the scene and multiplied by the per-frame op counts of the committed GPU
+    run of this workload (profiles/c4_frame_counts.json)."""
     ws, rank, _ = _dist()
     if rank != 0:
         return
-    counts, src = PAPER_COUNTS, PAPER_COUNTS["source"]
-    try:
-        with open(COUNTS) as f:
-            c = json.load(f)
-        counts = {k: float(c[k]) for k in ("newton", "cg", "passes", "energy")}
-        src = f"per-frame op counts of the GPU run recorded in {os.path.relpath(COUNTS, ROOT)}"
-    except Exception:
-        pass
-    full = _full_sizes(args.n)
-    vals = []
-    units = None
+    from oracle import stage_timing
+    from paper_2512_12151_b200.stepper import apply_dbc
+    system, state, params = _scene(args)
+    counts, src = _oracle_counts()
+    h = params.h
+    x = state.x
+    x_tilde = x + h * state.v + (h * h) * np.asarray(params.gravity, dtype=np.float64)
+    x_hat = x.copy()
+    apply_dbc(x_hat, system.boundary, x, 0)
+    mu = params.stiffness_constant * 1.0          # any positive mu: the stage costs do not depend on it
+    slices = stage_timing.ball_slices(system, 8)
+    vals, walls, parts_all = [], [], []
     for k in range(args.warmup + args.steps):
-        units = reference_unit_costs(args.sample_n, seed=k)
-        full["blocks"] = units["blocks"] * full["tets"] / units["tets"]
-        ms, parts = reference_ms_per_frame(units, full, counts)
+        t = time.perf_counter()
+        ms, parts, meas, full, infos = cpu_sample(system, x, x_hat, x_tilde, mu, params.offset, h,
+                                                  [slices[k % len(slices)]], None, counts, None)
+        walls.append(time.perf_counter() - t)
         if k >= args.warmup:
             vals.append(ms)
+            parts_all.append(parts)
     value = float(np.mean(vals))
-    sample = (f"oracle (numpy restatement of intact) stage costs on one n={args.sample_n} shell "
-              f"({units['tets']} tets), scaled to C4 ({full['tets']} tets) and {src}")
+    parts = {k: float(np.mean([p[k] for p in parts_all])) for k in parts_all[0]}
+    sample = (f"oracle (numpy port of intact, 1 thread) per step: one 1/8 slice of one ball (~57k of 2.30M tets) at "
+              f"the first frame — elastic assembly, CG iterations, energy, CCD pass over the slice's surface — "
+              f"scaled to the scene (tets / stored blocks / surface triangles) and to {src}; "
+              f"no constraints exist at the first frame, so contact-stage costs are not in this arm")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "ms/frame", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": value, "higher_is_better": False,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload(args), "parallelism": "one host core (numpy, single-threaded "
-                                                                 "like the reference, SPEC.md:587)"},
-            "cpu_baseline": {"value": value, "unit": "ms/frame", "cores": 1, "kind": "port",
-                             "sample": sample},
+            "config": {"workload": workload(args), "parallelism": "one host core (numpy, single-threaded like "
+                                                                 "the reference, SURVEY.md §8(d))"},
+            "cpu_baseline": {"value": value, "unit": "ms/frame", "cores": 1, "kind": "port", "sample": sample},
             "e2e": {"value": value, "unit": "ms/frame", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "phases_ms": parts}
+            "phases_ms": parts, "op_counts_per_frame": counts,
+            "sample_wall_s": {"mean": float(np.mean(walls)), "total": float(np.sum(walls))},
+            "extrapolation": "ms/frame = sum over stages of (sample stage time x scene/sample size) x per-frame "
+                             "op count; the sampled stage times are measured, the multiplication is the model",
+            "spread_ms": {"min": float(np.min(vals)), "max": float(np.max(vals))}}
     print(json.dumps(line), flush=True)
 
 
 # ------------------------------------------------------------------ GPU arm
+
+def _kernel_rooflines(clocks, peak_hbm, peak_fp64):
+    """Per-kernel achieved algorithmic GB/s (and FP64 TFLOP/s where counted)
+    over the timed region, from ibf_kernel_clocks (events on the launching
+    stream around each instrumented launch)."""
+    out = {}
+    for name, c in clocks.items():
+        if c["launches"] <= 0 or c["ms"] <= 0:
+            continue
+        gbs = c["bytes"] / (c["ms"] * 1e-3) / 1e9
+        row = {"launches": int(c["launches"]), "ms": round(c["ms"], 3), "avg_us": 1e3 * c["ms"] / c["launches"],
+               "GBps": gbs, "hbm_frac": gbs / peak_hbm, "units": c["units"]}
+        if c["flops"] > 0:
+            tf = c["flops"] / (c["ms"] * 1e-3) / 1e12
+            row.update(TFLOPs=tf, fp64_frac=tf / peak_fp64 if peak_fp64 else None)
+        out[name] = row
+    return out
+
 
 def run_ours(args):
     import torch
@@ -270,14 +309,12 @@ def run_ours(args):
         dist.init_process_group("nccl")
     else:
         torch.cuda.set_device(0)
-    from paper_2512_12151_b200 import _lib, scenes
-    from paper_2512_12151_b200.device import to_host
+    from paper_2512_12151_b200 import _lib
     from paper_2512_12151_b200.stepper import step_device
     from paper_2512_12151_b200.contact import ActiveSet
-    import ctypes as C
 
     t_setup = time.perf_counter()
-    system, state, params = scenes.c4_scene(n=args.n, plate_speed=PLATE_SPEED, plate_stop=PLATE_STOP)
+    system, state, params = _scene(args)
     dev = system.device
     ccd = system.ccd
     aset = ActiveSet()
@@ -289,14 +326,19 @@ def run_ours(args):
     L = _lib.lib()
     k = 0
     # untimed press to the contact-heavy regime, then the warm-up frames
+    t_pre = time.perf_counter()
     for _ in range(args.precompress + args.warmup):
         x, v, _ = step_device(x, v, system, aset, params, step_index=k)
         k += 1
     torch.cuda.synchronize()
+    pre_s = time.perf_counter() - t_pre
     stats = np.zeros(9)
     cst = np.zeros(3)
+    cnt = np.zeros(2)
     L.ibf_system_stats(dev.handle, _lib.host_ptr(stats), 1)
     L.ibf_ccd_stats(ccd.handle, _lib.host_ptr(cst), 1)
+    L.ibf_system_counts(dev.handle, _lib.host_ptr(cnt), 1)
+    _lib.kernel_clocks(on=1, reset=True)
     x_pin = torch.empty((n, 3), dtype=torch.float64, pin_memory=True)
     v_pin = torch.empty((n, 3), dtype=torch.float64, pin_memory=True)
     x_pin.copy_(x)
@@ -305,7 +347,7 @@ def run_ours(args):
     v_dev = torch.empty_like(v)
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
     newton = cg = passes = 0
-    n_constraints, pass_ms = [], []
+    n_constraints, pass_ms, triggers = [], [], 0
     cert = []
     mon_launches = 0
     launches0 = L.ibf_launch_count()
@@ -330,19 +372,22 @@ def run_ours(args):
             # penetration certificate of the accepted state, outside the timed
             # bracket (events e0..e3): nearest VF/EE pair within the contact
             # offset, and the reference's static tri-tri test (intersect.py)
-            l0 = L.ibf_launch_count()
-            dmin, _, _ = ccd.min_distance(xn, params.offset)
-            n_hits, _ = ccd.static_intersections(xn, cap=16)
-            cert.append((dmin, n_hits))
-            mon_launches += L.ibf_launch_count() - l0
+            if not args.no_certify:
+                l0 = L.ibf_launch_count()
+                dmin, _, _ = ccd.min_distance(xn, params.offset)
+                n_hits, _ = ccd.static_intersections(xn, cap=16)
+                cert.append((dmin, n_hits))
+                mon_launches += L.ibf_launch_count() - l0
             newton += sum(r.newton_iters for r in diag.iterations)
             cg += sum(r.cg_iters for r in diag.iterations)
             passes += len(diag.iterations)
+            triggers += diag.adaptive_triggers
             n_constraints.append(max(r.n_constraints for r in diag.iterations))
             pass_ms.append(max(r.wall_ms for r in diag.iterations))
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
     launches = L.ibf_launch_count() - launches0 - mon_launches
+    kclocks = _lib.kernel_clocks(on=0)
     frame_ms = [e[1].elapsed_time(e[2]) for e in evs]
     e2e_ms = [e[0].elapsed_time(e[3]) for e in evs]
     tot_dev, tot_e2e = float(np.sum(frame_ms)), float(np.sum(e2e_ms))
@@ -352,20 +397,23 @@ def run_ours(args):
         tot_dev, tot_e2e = float(t[0]), float(t[1])
     L.ibf_system_stats(dev.handle, _lib.host_ptr(stats), 0)
     L.ibf_ccd_stats(ccd.handle, _lib.host_ptr(cst), 0)
-    frames = ws * args.steps
-    value = tot_dev / frames
-    e2e = tot_e2e / frames
+    L.ibf_system_counts(dev.handle, _lib.host_ptr(cnt), 0)
+    # one scene per rank: the per-frame latency is the slowest rank's; the
+    # replicas' throughput is reported apart (scene-frames/s)
+    value = tot_dev / args.steps
+    e2e = tot_e2e / args.steps
     # roofline of the PCG (persistent SpMV + vector kernel): algorithmic bytes
     spmv_bytes = dev.spmv_bytes()
     pcg_ms, pcg_iters, contact_iter_terms = stats[2], stats[4], stats[8]
     pcg_bytes = pcg_iters * (spmv_bytes + 288.0 * n) + 120.0 * contact_iter_terms
     achieved = pcg_bytes / (pcg_ms * 1e-3) / 1e9 if pcg_ms > 0 else 0.0
     peak, peak_kind = _peaks()
+    peak_fp64 = _fp64_peak()
     traffic = None
     try:
         with open(NCU_SUMMARY) as f:
             # dram__bytes_read.sum + dram__bytes_write.sum per CG iteration of
-            # k_pcg from the committed ncu capture (profiles/ncu_summary.json)
+            # k_pcg from the committed ncu capture of this workload
             traffic = json.load(f)["k_pcg"]["dram_bytes_per_cg_iter"]
     except Exception:
         pass
@@ -374,55 +422,94 @@ def run_ours(args):
               "ccd_ms": cst[0] / args.steps}
     phases["other_ms"] = value - sum(phases.values())
     counts = {"newton": newton / args.steps, "cg": cg / args.steps, "passes": passes / args.steps,
-              "energy": stats[6] / args.steps}
+              "energy": cnt[1] / args.steps}
     line = {"metric": METRIC, "value": value, "unit": "ms/frame", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": value, "higher_is_better": False, "scaling": "weak",
-            # value / the paper's 5,367 ms/frame (RTX 4090, FP64, the authors' own mesh;
-            # this is the solid-ball proxy of the same 2.2M-tet press scene)
+            # value / the paper's 5,367 ms/frame (RTX 4090, FP64, the authors' own mesh)
             "vs_baseline": round(value / 5367.0, 4) if value > 0 else None,
-            "vs_baseline_note": "value / 5367 ms/frame (paper Table 1, RTX 4090); lower is better; proxy scene",
+            "vs_baseline_note": "value / 5367 ms/frame (paper Table 1, RTX 4090, its own squishy-ball mesh); "
+                                "lower is better; synthetic scene of the same V/F/T",
             "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload(args), "system": f"{sum(len(r.tets) for r in system.regions)} tets, "
-                                                            f"{n} vertices incl. the two pinned plates",
-                       "parallelism": "replicas" if ws > 1 else "single-gpu",
-                       "l2": "inputs > L2 (matrix ~%.0f MB)" % (spmv_bytes / 1e6)},
-            "ms_per_newton_iter": value * args.steps / max(newton, 1),
+            "config": {"workload": workload(args),
+                       "system": f"{sum(len(r.tets) for r in system.regions)} tets, {n} vertices "
+                                 f"({int(system.dbc_mask.sum())} pinned), {len(system.surface_triangles)} surface "
+                                 f"triangles",
+                       "parallelism": f"replicas x{ws} (one scene per GPU)" if ws > 1 else "single-gpu",
+                       "l2": "inputs > L2 (matrix ~%.0f MB, no flush needed)" % (spmv_bytes / 1e6)},
+            "ms_per_newton_iter": tot_dev / max(newton, 1),
             "newton_per_frame": counts["newton"], "cg_per_frame": counts["cg"], "passes_per_frame": counts["passes"],
-            "peak_constraints": int(max(n_constraints)), "phases_ms": phases,
-            "roofline": {"kernel": "k_pcg (symmetric BSR SpMV + block-Jacobi vector phase)", "bound": "hbm",
-                         "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "cg_per_solve": cg / max(newton, 1), "stagnation_triggers": triggers,
+            "constraints": {"peak": int(max(n_constraints)), "mean_of_frame_peaks": float(np.mean(n_constraints))},
+            "phases_ms": phases,
+            "ccd": {"candidates_per_frame": cst[2] / args.steps, "passes_per_frame": cst[1] / args.steps,
+                    "candidate_pairs_per_s": cst[2] / (cst[0] * 1e-3) if cst[0] > 0 else None},
+            "roofline": {"kernel": "k_pcg (symmetric BSR SpMV + block-Jacobi vector phase + matrix-free contact)",
+                         "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "peak_source": peak_kind, "traffic": traffic, "traffic_unit": "bytes per CG iteration",
                          "bytes_per_cg_iter": spmv_bytes + 288.0 * n},
+            "kernels": _kernel_rooflines(kclocks, peak, peak_fp64),
+            "fp64_peak_tflops": peak_fp64,
             "spmv_GBps": achieved,
             "e2e": {"value": e2e, "unit": "ms/frame", "h2d_bytes_per_step": 2 * 24 * n,
                     "d2h_bytes_per_step": 2 * 24 * n},
             "gpu_launches": int(launches), "frames_ms": [round(t, 1) for t in frame_ms],
+            "frames_constraints": n_constraints,
             "slowest_pass_wall_ms": [round(t, 1) for t in pass_ms], "wall_s": wall, "setup_s": setup_s,
-            "penetration_free": {"frames_checked": len(cert),
-                                 "min_distance": min(c[0] for c in cert) if cert else None,
-                                 "intersecting_triangle_pairs": max(c[1] for c in cert) if cert else None,
-                                 "how": "every timed frame: nearest non-adjacent VF/EE pair within the contact "
-                                        "offset (ibf_min_distance) and the reference's static tri-tri test "
-                                        "(ibf_static_intersection), outside the timed region"}}
+            "precompress_s": pre_s}
+    if ws > 1:
+        line["replica_scene_frames_per_s"] = ws * args.steps / (tot_dev * 1e-3)
+    if cert:
+        line["penetration_free"] = {
+            "frames_checked": len(cert), "min_distance": min(c[0] for c in cert),
+            "intersecting_triangle_pairs": max(c[1] for c in cert),
+            "how": "every timed frame: nearest non-adjacent VF/EE pair within the contact offset "
+                   "(ibf_min_distance) and the reference's static tri-tri test (ibf_static_intersection), "
+                   "outside the timed region"}
     if rank == 0:
         line["clocks"] = clocks.summary()
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and args.workload == "c4":
             os.makedirs(os.path.dirname(COUNTS), exist_ok=True)
             try:
                 with open(COUNTS, "w") as f:
-                    json.dump(dict(counts, n=args.n, source="bench.py GPU run"), f, indent=1)
+                    json.dump(dict(counts, cell=args.cell, plate_speed=args.plate_speed, frames=workload(args),
+                                   source="bench.py GPU run"), f, indent=1)
             except OSError:
                 pass
-            full = _full_sizes(args.n)
-            units = reference_unit_costs(args.sample_n)
-            full["blocks"] = units["blocks"] * full["tets"] / units["tets"]
-            ms, parts = reference_ms_per_frame(units, full, counts)
-            line["cpu_baseline"] = {"value": ms, "unit": "ms/frame", "cores": 1, "kind": "port",
-                                    "sample": f"oracle stage costs on one n={args.sample_n} shell scaled to C4 and "
-                                              f"to this run's per-frame op counts", "phases_ms": parts}
+            line["cpu_baseline"] = _cpu_baseline_leg(args, system, params, xn, vn, aset, counts, dev, k)
         print(json.dumps(line), flush=True)
     if ws > 1:
         torch.distributed.destroy_process_group()
+
+
+def _cpu_baseline_leg(args, system, params, x, v, aset, counts, dev, step_index):
+    """The oracle on a bounded sample of the state the timed frames ended at:
+    the first Newton iteration of the next frame (x_hat0 with the Dirichlet
+    targets), half of one ball (4 of 8 slices) for the elastic and CCD stages,
+    the whole active set for the contact stages."""
+    from oracle import stage_timing
+    from paper_2512_12151_b200.device import to_host
+    from paper_2512_12151_b200.stepper import apply_dbc
+    h = params.h
+    xh, vh = to_host(x), to_host(v)
+    x_tilde = xh + h * vh + (h * h) * np.asarray(params.gravity, dtype=np.float64)
+    mu = params.stiffness_constant * dev.stiffness_diagonal_max(x, h)
+    x_hat = xh.copy()
+    apply_dbc(x_hat, system.boundary, xh, step_index)
+    # a trial point the Newton step would visit: half way to the inertial target
+    free = ~system.dbc_mask
+    x_hat[free] = 0.5 * (xh[free] + x_tilde[free])
+    slices = stage_timing.ball_slices(system, 8)[:4]
+    t = time.perf_counter()
+    ms, parts, meas, full, infos = cpu_sample(system, xh, x_hat, x_tilde, mu, params.offset, h, slices,
+                                              aset.export_state(), counts, dev.n_blocks)
+    wall = time.perf_counter() - t
+    return {"value": ms, "unit": "ms/frame", "cores": 1, "kind": "port",
+            "sample": (f"oracle (numpy port of intact, 1 thread) on the state the timed frames ended at: half of one "
+                       f"ball ({sum(i['tets'] for i in infos)} of {infos[0]['tets_total']} tets) for assembly, CG "
+                       f"iterations, energy and the CCD pass over its surface, scaled to the scene; the full active "
+                       f"set ({infos[0]['constraints']} constraints) for the contact stages; times this run's "
+                       f"per-frame op counts"),
+            "phases_ms": parts, "stage_s_measured": meas, "stage_s_scene": full, "sample_wall_s": wall}
 
 
 def run_c5(args):
@@ -485,14 +572,16 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=42, help="ball resolution (42 -> 2.22M tets)")
-    ap.add_argument("--precompress", type=int, default=50,
+    ap.add_argument("--cell", type=float, default=0.02, help="c4: squishy-ball cell edge (m)")
+    ap.add_argument("--plate-speed", type=float, default=2.0, help="c4: plate speed (m/s)")
+    ap.add_argument("--n", type=int, default=42, help="c4ball: ball resolution (42 -> 2.22M tets)")
+    ap.add_argument("--precompress", type=int, default=40,
                     help="untimed frames of the press before warm-up (reaches the contact-heavy regime)")
-    ap.add_argument("--sample-n", type=int, default=24,
-                    help="ball resolution of the CPU baseline sample (24: 83k tets, ~10 s of numpy per sample)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--workload", default="c4", choices=["c4", "c5"],
-                    help="c4: the headline press scene (default); c5: scene-parallel batch of drops")
+    ap.add_argument("--no-certify", action="store_true", help="skip the per-frame penetration certificate")
+    ap.add_argument("--workload", default="c4", choices=["c4", "c4ball", "c5"],
+                    help="c4: the headline squishy-ball press (default); c4ball: the solid-ball proxy; "
+                         "c5: scene-parallel batch of drops")
     ap.add_argument("--scenes", type=int, default=64, help="c5: number of scenes in the batch")
     ap.add_argument("--concurrency", type=int, default=8,
                     help="c5: scenes in flight per GPU (host threads, one CUDA stream each)")

@@ -566,15 +566,15 @@ def test_reference_composition_through_mirror(pkg, rng):
     print(f"explicit blocks err {err_blocks:.1e}, pcg its {info.iterations}/{its}, p err {err_p:.1e}")
 
 
-def _squishy_press_state(fric, min_constraints, max_frames=160):
-    """A reduced squishy-ball press (scenes.squishy_scene: five 7.9k-tet balls
+def _squishy_press_state(fric, min_constraints, max_frames=120):
+    """A reduced squishy-ball press (scenes.squishy_scene: five 22k-tet balls
     in the pinned box) stepped on the GPU until at least `min_constraints`
     constraints are active."""
     import torch
     from paper_2512_12151_b200 import scenes
     from paper_2512_12151_b200.contact import ActiveSet
     from paper_2512_12151_b200.stepper import StepParams, step_device
-    system, state, params = scenes.squishy_scene(cell=0.01, n=8, stem=8, tip=4, plate_speed=2.0, plate_stop=0.12)
+    system, state, params = scenes.squishy_scene(cell=0.01, n=12, stem=10, tip=6, plate_speed=2.0, plate_stop=0.16)
     if fric:
         params = StepParams(h=params.h, offset=params.offset, min_iterations=2, friction_coefficient=fric,
                             eps_v=1e-3)

@@ -63,6 +63,21 @@ def test_step_params_validation():
             StepParams(**bad)
 
 
+def test_simulation_state_assignment_replaces_device_copy():
+    """Simulation keeps the evolving state on the device between advances;
+    assigning `sim.state` must still take effect, as on the reference's plain
+    dataclass (intact/stepper.py:374-384)."""
+    from paper_2512_12151_b200 import Simulation
+    from paper_2512_12151_b200.mesh import SimState
+    old = SimState(x=np.zeros((2, 3)), v=np.zeros((2, 3)))
+    new = SimState(x=np.ones((2, 3)), v=np.ones((2, 3)))
+    sim = Simulation(None, None, old)
+    sim.__dict__["_x"] = sim.__dict__["_v"] = object()    # stands in for a device copy after advance()
+    sim.state = new
+    assert sim.__dict__["_x"] is None and sim.__dict__["_v"] is None
+    assert sim.state is new
+
+
 def test_beta_recursion_code_semantics():
     """beta_update is called with k-1 (intact/stepper.py:320): K_min passes exempt."""
     from paper_2512_12151_b200.stepper import beta_update

@@ -21,7 +21,7 @@ from paper_2512_12151_b200.stepper import step_device
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--frames", type=int, default=40)
-ap.add_argument("--cell", type=float, default=0.01)
+ap.add_argument("--cell", type=float, default=0.02)
 ap.add_argument("--n", type=int, default=32)
 ap.add_argument("--stem", type=int, default=23)
 ap.add_argument("--tip", type=int, default=16)
@@ -64,6 +64,7 @@ from paper_2512_12151_b200 import _lib
 L = _lib.lib()
 dev = system.device
 free = torch.from_numpy(~system.dbc_mask).cuda()
+plate = torch.from_numpy(system.boundary[-1].vertices).cuda()
 for k in range(k0, k0 + args.frames):
     if args.profile_frames and k == k0 + args.frames - args.profile_frames:
         torch.cuda.synchronize()
@@ -80,7 +81,8 @@ for k in range(k0, k0 + args.frames):
     row = {"frame": k, "ms": round(e0.elapsed_time(e1), 1), "passes": len(it),
            "newton": sum(r.newton_iters for r in it), "cg": sum(r.cg_iters for r in it),
            "constraints": len(aset), "triggers": d.adaptive_triggers, "mu": d.mu, "offset": d.offset,
-           "min_alpha": min(r.alpha for r in it), "ball_top": round(float(x[free, 2].max()), 4)}
+           "min_alpha": min(r.alpha for r in it), "ball_top": round(float(x[free, 2].max()), 4),
+           "plate_z": round(float(x[plate, 2].min()), 4)}
     row["cg_per_solve"] = round(row["cg"] / max(row["newton"], 1), 1)
     L.ibf_system_stats(dev.handle, _lib.host_ptr(stats), 0)
     L.ibf_ccd_stats(ccd.handle, _lib.host_ptr(cst), 0)
