@@ -97,19 +97,33 @@ __device__ __forceinline__ void apply_pinv6(const double* __restrict__ P, double
 
 struct Operator {
   int n = 0;
+  const int* perm = nullptr;          // (n) storage position -> row (null: identity)
   const int* slice_ptr = nullptr;     // (S+1) storage block offset per slice
   const int* col = nullptr;           // (nq) column of each storage block
   const double* val = nullptr;        // 9 (nq + 32) entries, qel layout
   size_t val_bytes = 0;
   const int* low_ptr = nullptr;       // (S+1) lower-entry offset per slice
   const int2* low = nullptr;          // (nlq) (storage block, source row)
+  int zero_q = 0;                     // storage index of the zero block padded lower entries point at
   const uint8_t* mask = nullptr;      // (n) DBC mask (contact masking) or null
   const double* pinv = nullptr;       // (n,6) inverse diagonal blocks (upper triangle)
   ContactView contact;
   FrictionView friction;
 };
 
+// row held at storage position pos (slices are over positions, vectors over rows)
+__device__ __forceinline__ int row_at(const Operator& op, int pos) { return op.perm ? __ldg(op.perm + pos) : pos; }
+
 // Host + device halves of the sliced symmetric pattern (built once).
+//
+// Rows are placed at storage positions in windows of SELL_WINDOW rows, each
+// window sorted by (upper count, lower count) descending, so the 32 rows of a
+// slice have near-equal slot counts: on a surface-heavy mesh (squishy balls)
+// lattice order leaves 36 % of the upper slots and 41 % of the lower entries
+// as padding, the sorted windows 6 % and 16 %.  A window is one PCG CTA's
+// rows, so each CTA still owns the same rows as a set (vectors stay in row
+// order; the permutation only changes which thread takes which row).
+constexpr int SELL_WINDOW = 256;
 struct SellPattern {
   int64_t n = 0, nb = 0, nl = 0;      // rows, real blocks, real strict-upper blocks
   int n_slices = 0;
@@ -117,7 +131,8 @@ struct SellPattern {
   int zero_q = 0;                     // an all-zero storage block
   std::vector<int64_t> rows, cols;    // real blocks sorted by (row, col)
   std::vector<int> q_of_b;            // real block -> storage index
-  DevBuf<int> slice_ptr, col, qrow, low_ptr, diag_q;
+  std::vector<int> perm_h;            // storage position -> row
+  DevBuf<int> perm, slice_ptr, col, qrow, low_ptr, diag_q;
   DevBuf<uint8_t> qreal;
   DevBuf<int2> low;
   DevBuf<double> val;

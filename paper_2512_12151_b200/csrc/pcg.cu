@@ -249,9 +249,14 @@ __device__ __forceinline__ void acc_lower(const double b[9], double x0, double x
 // (18 matrix entries, 2 indices, 6 p entries): the product is latency-bound
 // otherwise.
 template <class Gather, class Terms = StoredTerms>
-__device__ __forceinline__ void row_product(const Operator& op, const Gather& gp, int i, double y[3],
+__device__ __forceinline__ void row_product(const Operator& op, const Gather& gp, int pos, int i, double y[3],
                                             const Terms& terms = Terms()) {
-  const int s = i >> 5, lane = i & 31;
+  // storage by position; row i (= row_at(pos)) for the contact incidences
+  // and the padding sentinel: a padded upper slot has col == i past slot 0
+  // (slot 0 is the diagonal), a padded lower entry points at the zero block,
+  // and both sit at the end of the row, so the row stops at its first one —
+  // lanes of shorter rows issue no loads for the slice's longer rows' slots
+  const int s = pos >> 5, lane = pos & 31;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
   {
     const int q0 = __ldg(op.slice_ptr + s), w = (__ldg(op.slice_ptr + s + 1) - q0) >> 5;
@@ -261,9 +266,10 @@ __device__ __forceinline__ void row_product(const Operator& op, const Gather& gp
     if (IBF_SPMV_UNROLL >= 2) {
       // column indices are loaded one slot pair ahead, so the p gathers of a
       // pair never wait on an index load (the chain per pair is one level)
-      int n0 = w > 0 ? __ldg(C) : 0, n1 = w > 1 ? __ldg(C + 32) : 0;
+      int n0 = w > 0 ? __ldg(C) : 0, n1 = w > 1 ? __ldg(C + 32) : i;
       for (; k + 2 <= w; k += 2) {
         const int j0 = n0, j1 = n1;
+        if (k > 0 && j0 == i) break;
         if (k + 2 < w) n0 = __ldg(C + 32 * (k + 2));
         if (k + 3 < w) n1 = __ldg(C + 32 * (k + 3));
         const double* B = V + 288 * (size_t)k;
@@ -282,6 +288,7 @@ __device__ __forceinline__ void row_product(const Operator& op, const Gather& gp
     }
     for (; k < w; ++k) {
       const int j = __ldg(C + 32 * k);
+      if (k > 0 && j == i) break;
       const double* B = V + 288 * (size_t)k;
       double b[9];
 #pragma unroll
@@ -294,11 +301,13 @@ __device__ __forceinline__ void row_product(const Operator& op, const Gather& gp
   {
     const int l0 = __ldg(op.low_ptr + s), w = (__ldg(op.low_ptr + s + 1) - l0) >> 5;
     const int2* L = op.low + l0 + lane;
+    const int zq = op.zero_q;
     int t = 0;
     if (IBF_SPMV_UNROLL >= 2) {
-      int2 n0 = w > 0 ? __ldg(L) : make_int2(0, 0), n1 = w > 1 ? __ldg(L + 32) : make_int2(0, 0);
+      int2 n0 = w > 0 ? __ldg(L) : make_int2(zq, 0), n1 = w > 1 ? __ldg(L + 32) : make_int2(zq, 0);
       for (; t + 2 <= w; t += 2) {
         const int2 e0 = n0, e1 = n1;
+        if (e0.x == zq) break;
         if (t + 2 < w) n0 = __ldg(L + 32 * (t + 2));
         if (t + 3 < w) n1 = __ldg(L + 32 * (t + 3));
         const double* B0 = op.val + qel(e0.x, 0);
@@ -318,6 +327,7 @@ __device__ __forceinline__ void row_product(const Operator& op, const Gather& gp
     }
     for (; t < w; ++t) {
       const int2 le = __ldg(L + 32 * t);
+      if (le.x == zq) break;
       const double* B = op.val + qel(le.x, 0);
       double b[9];
 #pragma unroll
@@ -364,9 +374,9 @@ __device__ __forceinline__ void row_product(const Operator& op, const Gather& gp
 // L partial results with shuffles in a fixed order.  For small systems, where
 // a CG iteration is the latency of one row's chain of block loads.
 template <class Gather, class Terms = StoredTerms>
-__device__ __forceinline__ void row_product_lanes(const Operator& op, const Gather& gp, int i, double y[3], int sub,
-                                                  int L, const Terms& terms = Terms()) {
-  const int s = i >> 5, lane = i & 31;
+__device__ __forceinline__ void row_product_lanes(const Operator& op, const Gather& gp, int pos, int i, double y[3],
+                                                  int sub, int L, const Terms& terms = Terms()) {
+  const int s = pos >> 5, lane = pos & 31;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
   {
     const int q0 = __ldg(op.slice_ptr + s), w = (__ldg(op.slice_ptr + s + 1) - q0) >> 5;
@@ -435,9 +445,10 @@ __global__ void k_contact_dot(Operator op, const double* __restrict__ p) {
 
 __global__ void __launch_bounds__(256, 2) k_spmv(Operator op, const double* __restrict__ p, double* __restrict__ y) {
   const PlainGather gp{p};
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < op.n; i += gridDim.x * blockDim.x) {
+  for (int pos = blockIdx.x * blockDim.x + threadIdx.x; pos < op.n; pos += gridDim.x * blockDim.x) {
+    const int i = row_at(op, pos);
     double v[3];
-    row_product(op, gp, i, v);
+    row_product(op, gp, pos, i, v);
     y[3 * (size_t)i] = v[0];
     y[3 * (size_t)i + 1] = v[1];
     y[3 * (size_t)i + 2] = v[2];
@@ -498,7 +509,8 @@ __global__ void __launch_bounds__(TMA_WARPS * 32, 1) k_spmv_tma(Operator op, con
   const PlainGather gp{p};
   const int n_slices = (op.n + 31) >> 5;
   for (int sl = blockIdx.x * TMA_WARPS + warp; sl < n_slices; sl += gridDim.x * TMA_WARPS) {
-    const int i = 32 * sl + lane;
+    const int pos = 32 * sl + lane;
+    const int i = pos < op.n ? row_at(op, pos) : 0;
     const int q0 = __ldg(op.slice_ptr + sl), w = (__ldg(op.slice_ptr + sl + 1) - q0) >> 5;
     const double* V = op.val + 9 * (size_t)q0;
     const int* C = op.col + q0 + lane;
@@ -538,7 +550,7 @@ __global__ void __launch_bounds__(TMA_WARPS * 32, 1) k_spmv_tma(Operator op, con
       }
     }
     __syncwarp();
-    if (i < op.n) {
+    if (pos < op.n) {
       // transposed part and contact/friction as in row_product
       const int l0 = __ldg(op.low_ptr + sl), lw = (__ldg(op.low_ptr + sl + 1) - l0) >> 5;
       const int2* L = op.low + l0 + lane;
@@ -701,8 +713,9 @@ __global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
   // ---- r = b, z = P^-1 r, x = 0
   double acc_b = 0.0, acc_rz = 0.0;
   for (int k = 0; k < R; ++k) {
-    const int i = row_of(k);
-    if (i >= n) break;
+    const int pos = row_of(k);
+    if (pos >= n) break;
+    const int i = row_at(op, pos);
     const double r0 = a.rhs[3 * (size_t)i], r1 = a.rhs[3 * (size_t)i + 1], r2 = a.rhs[3 * (size_t)i + 2];
     double zv[3];
     apply_pinv6(op.pinv + PINV_STRIDE * (size_t)i, r0, r1, r2, zv);
@@ -745,11 +758,11 @@ __global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
       // their term loop, instead of every CTA waiting at a grid barrier.
       const bool counted = a.ready != nullptr;
       const CountedTerms sterms{a.ready, (unsigned)it * a.n_home};
-      auto product = [&](int i, double v[3]) {
+      auto product = [&](int pos, int i, double v[3]) {
         if (counted)
-          row_product(op, gd, i, v, sterms);
+          row_product(op, gd, pos, i, v, sterms);
         else
-          row_product(op, gd, i, v);
+          row_product(op, gd, pos, i, v);
       };
       if (op.contact.n || op.friction.n) {
         if (counted) {
@@ -783,11 +796,12 @@ __global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
           const int ch = chunk_sh;
           __syncthreads();
           if (ch >= a.n_chunks) break;
-          const int i = ch * blockDim.x + threadIdx.x;
+          const int pos = ch * blockDim.x + threadIdx.x;
           double accc = 0.0;
-          if (i < n) {
+          if (pos < n) {
+            const int i = row_at(op, pos);
             double v[3], pv[3];
-            product(i, v);
+            product(pos, i, v);
             gd.get(i, pv[0], pv[1], pv[2]);
             double* pki = pk + 3 * (size_t)i;
             pki[0] = pv[0]; pki[1] = pv[1]; pki[2] = pv[2];
@@ -814,13 +828,14 @@ __global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
           // small system: L lanes per row; warp-uniform loop for the shuffles
           const int L = a.lanes, sub = threadIdx.x & (L - 1);
           for (int base = (blockIdx.x * blockDim.x + (threadIdx.x & ~31)) / L; base < n; base += S / L) {
-            const int i = base + (threadIdx.x & 31) / L;
+            const int pos = base + (threadIdx.x & 31) / L;
+            const int i = pos < n ? row_at(op, pos) : n;
             double v[3] = {0.0, 0.0, 0.0};
-            if (i < n) {
+            if (pos < n) {
               if (counted)
-                row_product_lanes(op, gd, i, v, sub, L, sterms);
+                row_product_lanes(op, gd, pos, i, v, sub, L, sterms);
               else
-                row_product_lanes(op, gd, i, v, sub, L);
+                row_product_lanes(op, gd, pos, i, v, sub, L);
             }
             for (int o = 1; o < L; o <<= 1)
               for (int c = 0; c < 3; ++c) v[c] += __shfl_xor_sync(0xffffffffu, v[c], o);
@@ -836,10 +851,11 @@ __global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
           }
         }
         for (int k = 0; k < R && a.lanes == 1; ++k) {
-          const int i = row_of(k);
-          if (i >= n) break;
+          const int pos = row_of(k);
+          if (pos >= n) break;
+          const int i = row_at(op, pos);
           double v[3], pv[3];
-          product(i, v);
+          product(pos, i, v);
           const double* Z = a.z + 3 * (size_t)i;
           if (first) {
             pv[0] = Z[0]; pv[1] = Z[1]; pv[2] = Z[2];
@@ -886,8 +902,9 @@ __global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
       acc_rz = 0.0;
       const bool split = a.bar != nullptr && !qp_smem;
       for (int k = 0; k < R; ++k) {
-        const int i = row_of(k);
-        if (i >= n) break;
+        const int pos = row_of(k);
+        if (pos >= n) break;
+        const int i = row_at(op, pos);
         double qv[3], pv[3], rv[3], zv[3];
         if (qp_smem) {
           for (int c = 0; c < 3; ++c) {
@@ -925,8 +942,9 @@ __global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
           atomicAdd(a.bar, 1u);
         }
         for (int k = 0; k < R; ++k) {
-          const int i = row_of(k);
-          if (i >= n) break;
+          const int pos = row_of(k);
+          if (pos >= n) break;
+          const int i = row_at(op, pos);
           for (int c = 0; c < 3; ++c) {
             const size_t e = 3 * (size_t)i + c;
             xn[e] = xc[e] + alpha * pk[e];
@@ -963,10 +981,11 @@ __global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
         }
         acc_rz = 0.0;
         for (int k = 0; k < R; ++k) {
-          const int i = row_of(k);
-          if (i >= n) break;
+          const int pos = row_of(k);
+          if (pos >= n) break;
+          const int i = row_at(op, pos);
           double v[3], zv[3];
-          row_product(op, gx, i, v);
+          row_product(op, gx, pos, i, v);
           const double r0 = a.rhs[3 * (size_t)i] - v[0];
           const double r1 = a.rhs[3 * (size_t)i + 1] - v[1];
           const double r2 = a.rhs[3 * (size_t)i + 2] - v[2];
@@ -1242,12 +1261,26 @@ int SellPattern::build(int64_t n_, const std::vector<int64_t>& rows_, const std:
     up[i + 1] += up[i];
     lo[i + 1] += lo[i];
   }
+  auto ucount = [&](int64_t i) { return up[i + 1] - up[i]; };
+  auto lcount = [&](int64_t i) { return lo[i + 1] - lo[i]; };
+  // storage positions: windows of SELL_WINDOW rows sorted by (upper, lower)
+  // slot counts, descending; ties keep row order
+  perm_h.resize(n);
+  std::vector<int> pos_of(n);
+  for (int64_t w0 = 0; w0 < n; w0 += SELL_WINDOW) {
+    const int64_t w1 = std::min<int64_t>(n, w0 + SELL_WINDOW);
+    for (int64_t i = w0; i < w1; ++i) perm_h[i] = (int)i;
+    std::stable_sort(perm_h.begin() + w0, perm_h.begin() + w1, [&](int a, int b) {
+      return ucount(a) != ucount(b) ? ucount(a) > ucount(b) : lcount(a) > lcount(b);
+    });
+  }
+  for (int64_t p = 0; p < n; ++p) pos_of[perm_h[p]] = (int)p;
   std::vector<int> sp(S + 1, 0), lp(S + 1, 0);
   for (int s = 0; s < S; ++s) {
     int w = 0, lw = 0;
-    for (int64_t i = 32LL * s; i < std::min<int64_t>(n, 32LL * s + 32); ++i) {
-      w = std::max(w, up[i + 1] - up[i]);
-      lw = std::max(lw, lo[i + 1] - lo[i]);
+    for (int64_t p = 32LL * s; p < std::min<int64_t>(n, 32LL * s + 32); ++p) {
+      w = std::max(w, ucount(perm_h[p]));
+      lw = std::max(lw, lcount(perm_h[p]));
     }
     sp[s + 1] = sp[s] + 32 * w;
     lp[s + 1] = lp[s] + 32 * lw;
@@ -1262,20 +1295,22 @@ int SellPattern::build(int64_t n_, const std::vector<int64_t>& rows_, const std:
   std::vector<int> qc(nq + 32), qr(nq + 32), dq(n, -1);
   std::vector<uint8_t> qre(nq + 32, 0);
   for (int64_t q = 0; q < nq + 32; ++q) qc[q] = qr[q] = 0;
-  // padding: own row (rows past n in the last slice keep row/col 0, zero values)
+  // padding: the position's own row (positions past n in the last slice keep
+  // row/col 0, zero values)
   for (int s = 0; s < S; ++s) {
     const int w = (sp[s + 1] - sp[s]) / 32;
     for (int k = 0; k < w; ++k)
       for (int l = 0; l < 32; ++l) {
-        const int64_t i = 32LL * s + l;
+        const int64_t p = 32LL * s + l;
         const int64_t q = sp[s] + 32LL * k + l;
-        qc[q] = qr[q] = (i < n) ? (int)i : 0;
+        qc[q] = qr[q] = (p < n) ? perm_h[p] : 0;
       }
   }
   q_of_b.assign(nb, 0);
   for (int64_t i = 0; i < n; ++i) {
-    const int s = (int)(i >> 5), l = (int)(i & 31);
-    for (int k = 0; k < up[i + 1] - up[i]; ++k) {
+    const int p = pos_of[i];
+    const int s = p >> 5, l = p & 31;
+    for (int k = 0; k < ucount(i); ++k) {
       const int64_t b = up[i] + k;
       const int q = sp[s] + 32 * k + l;
       q_of_b[b] = q;
@@ -1292,18 +1327,20 @@ int SellPattern::build(int64_t n_, const std::vector<int64_t>& rows_, const std:
     const int w = (lp[s + 1] - lp[s]) / 32;
     for (int t = 0; t < w; ++t)
       for (int l = 0; l < 32; ++l) {
-        const int64_t i = 32LL * s + l;
-        le[lp[s] + 32LL * t + l] = make_int2(zero_q, (i < n) ? (int)i : 0);
+        const int64_t p = 32LL * s + l;
+        le[lp[s] + 32LL * t + l] = make_int2(zero_q, (p < n) ? perm_h[p] : 0);
       }
   }
   std::vector<int> fill(n, 0);
   for (int64_t b = 0; b < nb; ++b) {
     if (rows[b] == cols[b]) continue;
     const int64_t j = cols[b];
-    const int s = (int)(j >> 5), l = (int)(j & 31);
+    const int p = pos_of[j];
+    const int s = p >> 5, l = p & 31;
     const int t = fill[j]++;
     le[lp[s] + 32LL * t + l] = make_int2(q_of_b[b], (int)rows[b]);
   }
+  if (n > 0) IBF_TRY(perm.upload(perm_h.data(), perm_h.size()));
   IBF_TRY(slice_ptr.upload(sp.data(), sp.size()));
   IBF_TRY(low_ptr.upload(lp.data(), lp.size()));
   IBF_TRY(col.upload(qc.data(), qc.size()));
@@ -1319,6 +1356,8 @@ int SellPattern::build(int64_t n_, const std::vector<int64_t>& rows_, const std:
 Operator SellPattern::op() const {
   Operator o;
   o.n = (int)n;
+  o.perm = perm.p;
+  o.zero_q = zero_q;
   o.slice_ptr = slice_ptr.p;
   o.col = col.p;
   o.val = val.p;

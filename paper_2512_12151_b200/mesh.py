@@ -143,6 +143,37 @@ def build_tet_mesh(positions, tets) -> TetMesh:
     return TetMesh(positions, tets, t, e, v)
 
 
+def _morton3(points, bits=21):
+    """Interleaved 3 x `bits`-bit Morton codes of points normalised to their box."""
+    lo = points.min(axis=0)
+    ext = np.maximum(points.max(axis=0) - lo, 1e-300)
+    q = np.minimum(((points - lo) / ext * ((1 << bits) - 1)).astype(np.uint64), (1 << bits) - 1)
+    code = np.zeros(len(points), dtype=np.uint64)
+    for b in range(bits):
+        for a in range(3):
+            code |= ((q[:, a] >> np.uint64(b)) & np.uint64(1)) << np.uint64(3 * b + a)
+    return code
+
+
+def reorder_for_locality(mesh: TetMesh) -> TetMesh:
+    """The same mesh with vertices renumbered along a Morton curve of their
+    rest positions and tets sorted by their smallest vertex.
+
+    Pure data layout (no reference counterpart; the reference is order
+    agnostic): the symmetric SpMV reads each stored block twice (row and
+    transposed) and gathers p at the block columns, so both stay L2 hits only
+    if a block's rows and columns are near in index.  Lattice-index numbering
+    of a sparse lattice (hollow cores, thin strands) puts neighbours up to a
+    lattice plane apart; on the squishy-ball scene the PCG's DRAM traffic was
+    1.42x its algorithmic bytes with that numbering."""
+    perm = np.argsort(_morton3(mesh.rest_positions), kind="stable")
+    inv = np.empty_like(perm)
+    inv[perm] = np.arange(len(perm))
+    tets = inv[mesh.tets]
+    tets = tets[np.lexsort((tets.max(axis=1), tets.min(axis=1)))]
+    return build_tet_mesh(mesh.rest_positions[perm], tets)
+
+
 def compute_rest_data(mesh: TetMesh, density: float) -> RestData:
     """Dm^-1, volumes, shape rows A_i (dF = sum dx_i A_i), lumped masses."""
     if density <= 0.0:

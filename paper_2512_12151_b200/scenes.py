@@ -28,7 +28,7 @@ from __future__ import annotations
 import numpy as np
 
 from .elasticity import Material, MaterialModel
-from .mesh import SimState, TetMesh, build_tet_mesh, compute_rest_data
+from .mesh import SimState, TetMesh, build_tet_mesh, compute_rest_data, reorder_for_locality
 from .solver import ElasticRegion
 from .stepper import BoundaryCondition, StepParams, System
 
@@ -116,7 +116,8 @@ def _sphere_map(c, radius, blend=0.8):
     return (blend * out * sup[:, None] + (1.0 - blend) * c) * radius
 
 
-def squishy_ball(n=32, shell=2, stem=23, tip=16, pitch=3, cell=0.01, center=(0.0, 0.0, 0.0)) -> TetMesh:
+def squishy_ball(n=32, shell=2, stem=23, tip=16, pitch=3, cell=0.01, center=(0.0, 0.0, 0.0),
+                 reorder=True) -> TetMesh:
     """Squishy ball: a hollow core with thin strands all over it.
 
     The core is the outer `shell` Kuhn-cell layers of an n^3 grid mapped onto
@@ -198,7 +199,8 @@ def squishy_ball(n=32, shell=2, stem=23, tip=16, pitch=3, cell=0.01, center=(0.0
     bw = _sphere_map((wide - half) / half, radius)
     shift = np.where(tipv[:, None], 0.5 * (bw - bc), bw - bc)
     pos[out] = bc + shift + (l * cell)[:, None] * axis
-    return build_tet_mesh(pos + np.asarray(center, dtype=np.float64), tets)
+    mesh = build_tet_mesh(pos + np.asarray(center, dtype=np.float64), tets)
+    return reorder_for_locality(mesh) if reorder else mesh
 
 
 def squishy_extent(n=32, stem=23, tip=16, cell=0.01):
@@ -331,7 +333,7 @@ def c4_scene(n=42, radius=0.1, gap=0.001, plate_speed=0.1, h=0.01, layers=None, 
 
 
 def squishy_scene(cell=0.02, n=32, stem=23, tip=16, shell=2, gap=None, plate_speed=1.0, plate_stop=None, h=0.01,
-                  walls=True, seed=7, balls=5):
+                  walls=True, seed=7, balls=5, reorder=True):
     """C4, paper-scale: five squishy balls in a box, pressed by a plate.
 
     Each ball is a `squishy_ball` (hollow core + 600 strands; the defaults
@@ -349,7 +351,7 @@ def squishy_scene(cell=0.02, n=32, stem=23, tip=16, shell=2, gap=None, plate_spe
     paper's average is 28, its peak 146), see DESIGN.md.
     """
     rng = np.random.default_rng(seed)
-    base = squishy_ball(n=n, shell=shell, stem=stem, tip=tip, cell=cell)
+    base = squishy_ball(n=n, shell=shell, stem=stem, tip=tip, cell=cell, reorder=reorder)
     R = float(np.linalg.norm(base.rest_positions, axis=1).max())
     gap = 2.0 * cell if gap is None else gap
     mat = Material(MaterialModel.COR, 1e4, 0.4)
