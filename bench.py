@@ -228,6 +228,69 @@ def cpu_sample(system, x, x_hat, x_tilde, mu, offset, h, slices, aset_state, cou
     return ms, parts, meas_tot, full_tot, infos
 
 
+def _oracle_c5_scene(job):
+    """One C5 scene on the oracle (a pool worker): (seed, frames) -> (frames done, s)."""
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    seed, frames = job
+    from oracle import contact as ocontact, timestep
+    from paper_2512_12151_b200 import scenes
+    system, state, params = scenes.c5_scene(seed)
+    regions = [(r.material.model.value, r.material.mu, r.material.lam, r.tets, r.shape_rows, r.volumes)
+               for r in system.regions]
+    scene = timestep.Scene(system.masses, regions, system.surface_triangles, system.surface_edges,
+                           system.surface_vertices, [(bc.vertices, None) for bc in system.boundary])
+    x, v = state.x.copy(), state.v.copy()
+    aset = ocontact.ConstraintSet()
+    t = time.perf_counter()
+    done = 0
+    for k in range(frames):
+        try:
+            x, v, _, _, _ = timestep.step(x, v, scene, aset, h=params.h, offset=params.offset,
+                                          k_min=params.min_iterations, step_index=k)
+        except timestep.Aborted:
+            break
+        done += 1
+    return done, time.perf_counter() - t
+
+
+def run_reference_c5(args):
+    """--impl reference --workload c5: the oracle port of the reference on a
+    process pool with one single-threaded process per host core, one scene
+    per process; each step runs one frame of `cores`
+    scenes (seeds dealt in order), so a step is bounded by the slowest of
+    them.  value = scene-frames / wall over the timed steps."""
+    import multiprocessing as mp
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    seeds = list(range(args.scenes))
+    ctx = mp.get_context("fork")
+    frames_done, walls = 0, []
+    with ctx.Pool(cores) as pool:
+        for k in range(args.warmup + args.steps):
+            batch = [(seeds[(k * cores + j) % len(seeds)], 1) for j in range(cores)]
+            t = time.perf_counter()
+            res = pool.map(_oracle_c5_scene, batch)
+            w = time.perf_counter() - t
+            if k >= args.warmup:
+                walls.append(w)
+                frames_done += sum(r[0] for r in res)
+    value = frames_done / max(sum(walls), 1e-9)
+    sample = (f"oracle (numpy port of intact) on a {cores}-process pool (one single-threaded process per host "
+              f"core); each step = frame 0 of {cores} C5 scenes (seeds dealt round-robin), {args.steps} timed steps")
+    line = {"impl": "reference", "metric": "C5 scene-frames/s (64 randomized NH drops, scene-parallel)",
+            "value": value, "unit": "scene-frames/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * float(np.mean(walls)), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"C5: {args.scenes} C1-like drops (seeded jitter)",
+                       "parallelism": f"process pool x{cores} host cores"},
+            "cpu_baseline": {"value": value, "unit": "scene-frames/s", "cores": cores, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "scene-frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
 def run_reference(args):
     """--impl reference: the oracle port of the reference's CPU path (oracle/,
     single-threaded numpy like the reference), no GPU.  Each step times one
@@ -587,7 +650,10 @@ def main():
                     help="c5: scenes in flight per GPU (host threads, one CUDA stream each)")
     args = ap.parse_args()
     if args.impl == "reference":
-        run_reference(args)
+        if args.workload == "c5":
+            run_reference_c5(args)
+        else:
+            run_reference(args)
     elif args.workload == "c5":
         run_c5(args)
     else:

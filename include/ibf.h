@@ -304,11 +304,12 @@ int ibf_system_counts(ibf_system* s, double* out, int reset);
 int ibf_ccd_stats(ibf_ccd* c, double* out, int reset);
 /* Per-kernel device clocks (roofline bookkeeping; no reference counterpart).
  * on: 1 starts bracketing the instrumented launches with events on their
- * stream, 0 stops, < 0 leaves the state.  out (may be NULL) receives 7 rows
+ * stream, 0 stops, < 0 leaves the state.  out (may be NULL) receives 8 rows
  * of 5 doubles — ms, launches, algorithmic bytes, algorithmic flops, units —
  * for k_elem, k_gather_blocks, k_vertex_rows, k_energy, k_traverse,
- * k_pair_toi, k_pcg (units: tets, blocks, vertices, trial points, candidate
- * pairs, narrow-phase pairs, -); pending events are harvested first (waits
+ * k_pair_toi, k_pcg, k_prefilter (units: tets, blocks, vertices, trial
+ * points, candidate pairs, narrow-phase pairs, -, candidate pairs); pending
+ * events are harvested first (waits
  * for them).  reset != 0 zeroes the counters after reading. */
 int ibf_kernel_clocks(int on, double* out, int reset);
 

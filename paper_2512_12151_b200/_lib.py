@@ -147,7 +147,8 @@ def stream():
     return C.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
-KERNEL_CLOCKS = ("k_elem", "k_gather_blocks", "k_vertex_rows", "k_energy", "k_traverse", "k_pair_toi", "k_pcg")
+KERNEL_CLOCKS = ("k_elem", "k_gather_blocks", "k_vertex_rows", "k_energy", "k_traverse", "k_pair_toi", "k_pcg",
+                 "k_prefilter")
 
 
 def kernel_clocks(on=-1, reset=False):

@@ -181,18 +181,51 @@ __global__ void k_build(int n, const unsigned long long* __restrict__ k, int* __
   }
 }
 
+// Traversal record of an internal node: both children's boxes in float,
+// rounded outward (lo toward -inf, hi toward +inf), and the child indices —
+// 64 bytes, one aligned half line per visited node, two children tested per
+// fetch.  The float boxes contain the exact FP64 ones, so they never prune a
+// real overlap; leaves are then tested exactly against the primitive's FP64
+// box, so the candidate set is the one the FP64 tree gives (bit-identical to
+// the reference's, intact/ccd.py:104-145).
+struct __align__(16) PackedNode {
+  float4 a;  // lo_L.xyz, hi_L.x
+  float4 b;  // hi_L.yz, lo_R.xy
+  float4 c;  // lo_R.z, hi_R.xyz
+  int4 d;    // left, right, -, -
+};
+
+// write node `node`'s FP64 box (lo, hi) into its parent's packed record
+__device__ __forceinline__ void pack_child(PackedNode* packed, int par, bool is_left, const double lo[3],
+                                           const double hi[3]) {
+  float* f = reinterpret_cast<float*>(packed + par);
+  const int o = is_left ? 0 : 6;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    f[o + c] = __double2float_rd(lo[c]);
+    f[o + 3 + c] = __double2float_ru(hi[c]);
+  }
+}
+
 __global__ void k_refit(int n, const unsigned long long* __restrict__ k, const double* __restrict__ plo,
                         const double* __restrict__ phi, const int* __restrict__ left, const int* __restrict__ right,
                         const int* __restrict__ parent, int* __restrict__ flag, double* __restrict__ nlo,
-                        double* __restrict__ nhi) {
+                        double* __restrict__ nhi, PackedNode* __restrict__ packed) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const int prim = (int)(k[i] & 0xffffffffull);
     int node = n - 1 + i;
+    double lo[3], hi[3];
     for (int c = 0; c < 3; ++c) {
-      nlo[3 * node + c] = plo[3 * prim + c];
-      nhi[3 * node + c] = phi[3 * prim + c];
+      lo[c] = plo[3 * prim + c];
+      hi[c] = phi[3 * prim + c];
+      nlo[3 * node + c] = lo[c];
+      nhi[3 * node + c] = hi[c];
     }
     if (n == 1) continue;
+    if (packed) {
+      const int par = parent[node];
+      pack_child(packed, par, left[par] == node, lo, hi);
+    }
     __threadfence();
     node = parent[node];
     while (true) {
@@ -200,8 +233,17 @@ __global__ void k_refit(int n, const unsigned long long* __restrict__ k, const d
       if (old == 0) break;  // first arrival: the sibling finishes this node
       const int a = left[node], b = right[node];
       for (int c = 0; c < 3; ++c) {
-        nlo[3 * node + c] = fmin(__ldcg(nlo + 3 * a + c), __ldcg(nlo + 3 * b + c));
-        nhi[3 * node + c] = fmax(__ldcg(nhi + 3 * a + c), __ldcg(nhi + 3 * b + c));
+        lo[c] = fmin(__ldcg(nlo + 3 * a + c), __ldcg(nlo + 3 * b + c));
+        hi[c] = fmax(__ldcg(nhi + 3 * a + c), __ldcg(nhi + 3 * b + c));
+        nlo[3 * node + c] = lo[c];
+        nhi[3 * node + c] = hi[c];
+      }
+      if (packed) {
+        packed[node].d = make_int4(a, b, 0, 0);
+        if (node != 0) {
+          const int par = parent[node];
+          pack_child(packed, par, left[par] == node, lo, hi);
+        }
       }
       __threadfence();
       if (node == 0) break;
@@ -217,6 +259,9 @@ struct Tree {
   const int* right;
   const double* lo;
   const double* hi;
+  const PackedNode* packed;        // internal-node records (null: FP64 node arrays only)
+  const double* plo;               // primitive boxes (exact leaf test with `packed`)
+  const double* phi;
 };
 
 __device__ __forceinline__ bool overlap(const double ql[3], const double qh[3], const double* lo, const double* hi) {
@@ -269,12 +314,88 @@ __device__ __forceinline__ bool make_quad(const TraverseArgs& a, int qi, int pi,
   return true;
 }
 
+// one leaf of the query's traversal: shared-vertex / ordering filter, the
+// ACCD prefilter, warp-aggregated append
+template <bool FILTER>
+__device__ __forceinline__ void traverse_leaf(const TraverseArgs& a, int64_t qi, int pi,
+                                              unsigned long long& n_cand) {
+  int q[4];
+  if (!make_quad(a, (int)qi, pi, q)) return;
+  ++n_cand;
+  bool emit = true;
+  if (FILTER) {
+    V3 X0[4], X1[4];
+    for (int k = 0; k < 4; ++k) {
+      X0[k] = geo::ld3(a.x0 + 3 * (int64_t)q[k]);
+      X1[k] = geo::ld3(a.x1 + 3 * (int64_t)q[k]);
+    }
+    emit = geo::accd_class(a.kind, X0, X1, a.min_gap) != 1;
+  }
+  if (emit) {
+    // warp-aggregated append: the lanes emitting at this point take
+    // consecutive slots with one atomic for the group
+    const unsigned grp = __activemask();
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(grp) - 1;
+    unsigned long long base = 0;
+    if (lane == leader) base = atomicAdd(a.counters, (unsigned long long)__popc(grp));
+    base = __shfl_sync(grp, base, leader);
+    const unsigned long long slot = base + __popc(grp & ((1u << lane) - 1u));
+    if (slot < a.cap) a.out[slot] = ((unsigned long long)qi << 32) | (unsigned long long)pi;
+  }
+}
+
+__device__ __forceinline__ bool overlap_f(const float ql[3], const float qh[3], float lx, float ly, float lz,
+                                          float hx, float hy, float hz) {
+  return ql[0] <= hx && ql[1] <= hy && ql[2] <= hz && qh[0] >= lx && qh[1] >= ly && qh[2] >= lz;
+}
+
+template <bool FILTER, bool PACKED>
 __global__ void __launch_bounds__(128) k_traverse(TraverseArgs a) {
   unsigned long long n_cand = 0;
+  const int nl = a.tree.n - 1;   // first leaf node
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < a.nq; t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t qi = a.qorder ? (int64_t)(a.qorder[t] & 0xffffffffull) : t;
     const double ql[3] = {a.qlo[3 * qi], a.qlo[3 * qi + 1], a.qlo[3 * qi + 2]};
     const double qh[3] = {a.qhi[3 * qi], a.qhi[3 * qi + 1], a.qhi[3 * qi + 2]};
+    if (PACKED) {
+      // packed records: both children per fetch, float tests, exact FP64
+      // test at the leaves; near child first, the other on the stack
+      const float qlf[3] = {__double2float_rd(ql[0]), __double2float_rd(ql[1]), __double2float_rd(ql[2])};
+      const float qhf[3] = {__double2float_ru(qh[0]), __double2float_ru(qh[1]), __double2float_ru(qh[2])};
+      int stack[64];
+      int sp = 0;
+      int node = 0;
+      while (true) {
+        const PackedNode* P = a.tree.packed + node;
+        const float4 A = __ldg(&P->a), B = __ldg(&P->b), Cq = __ldg(&P->c);
+        const int4 D = __ldg(&P->d);
+        bool hl = overlap_f(qlf, qhf, A.x, A.y, A.z, A.w, B.x, B.y);
+        bool hr = overlap_f(qlf, qhf, B.z, B.w, Cq.x, Cq.y, Cq.z, Cq.w);
+        if (hl && D.x >= nl) {
+          const int pi = (int)(a.tree.keys[D.x - nl] & 0xffffffffull);
+          if (overlap(ql, qh, a.tree.plo + 3 * pi, a.tree.phi + 3 * pi)) traverse_leaf<FILTER>(a, qi, pi, n_cand);
+          hl = false;
+        }
+        if (hr && D.y >= nl) {
+          const int pi = (int)(a.tree.keys[D.y - nl] & 0xffffffffull);
+          if (overlap(ql, qh, a.tree.plo + 3 * pi, a.tree.phi + 3 * pi)) traverse_leaf<FILTER>(a, qi, pi, n_cand);
+          hr = false;
+        }
+        if (hl && hr) {
+          stack[sp++] = D.y;
+          node = D.x;
+        } else if (hl) {
+          node = D.x;
+        } else if (hr) {
+          node = D.y;
+        } else {
+          if (sp == 0) break;
+          node = stack[--sp];
+        }
+      }
+      continue;
+    }
     // LBVH depth is bounded by the 64 key bits, so depth+1 entries suffice
     int stack[80];
     int sp = 0;
@@ -282,32 +403,8 @@ __global__ void __launch_bounds__(128) k_traverse(TraverseArgs a) {
     while (sp) {
       const int node = stack[--sp];
       if (!overlap(ql, qh, a.tree.lo + 3 * node, a.tree.hi + 3 * node)) continue;
-      if (node >= a.tree.n - 1) {
-        const int pi = (int)(a.tree.keys[node - (a.tree.n - 1)] & 0xffffffffull);
-        int q[4];
-        if (!make_quad(a, (int)qi, pi, q)) continue;
-        ++n_cand;
-        bool emit = true;
-        if (a.filter) {
-          V3 X0[4], X1[4];
-          for (int k = 0; k < 4; ++k) {
-            X0[k] = geo::ld3(a.x0 + 3 * (int64_t)q[k]);
-            X1[k] = geo::ld3(a.x1 + 3 * (int64_t)q[k]);
-          }
-          emit = geo::accd_class(a.kind, X0, X1, a.min_gap) != 1;
-        }
-        if (emit) {
-          // warp-aggregated append: the lanes emitting at this point take
-          // consecutive slots with one atomic for the group
-          const unsigned grp = __activemask();
-          const int lane = threadIdx.x & 31;
-          const int leader = __ffs(grp) - 1;
-          unsigned long long base = 0;
-          if (lane == leader) base = atomicAdd(a.counters, (unsigned long long)__popc(grp));
-          base = __shfl_sync(grp, base, leader);
-          const unsigned long long slot = base + __popc(grp & ((1u << lane) - 1u));
-          if (slot < a.cap) a.out[slot] = ((unsigned long long)qi << 32) | (unsigned long long)pi;
-        }
+      if (node >= nl) {
+        traverse_leaf<FILTER>(a, qi, (int)(a.tree.keys[node - nl] & 0xffffffffull), n_cand);
       } else {
         stack[sp++] = a.tree.right[node];
         stack[sp++] = a.tree.left[node];
@@ -315,6 +412,33 @@ __global__ void __launch_bounds__(128) k_traverse(TraverseArgs a) {
     }
   }
   if (n_cand) atomicAdd(a.counters + 1, n_cand);
+}
+
+// Second stage of the filtered broad phase: the traversal emits every
+// candidate (no FP64 work inside the tree walk, so it keeps ~40 % of the
+// registers and its warps stay converged between leaves), then one thread
+// per candidate runs the ACCD prefilter and appends the survivors.
+__global__ void __launch_bounds__(256) k_prefilter(TraverseArgs a, int64_t n, const unsigned long long* __restrict__ cand) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long e = cand[i];
+    const int qi = (int)(e >> 32), pi = (int)(e & 0xffffffffull);
+    int q[4];
+    make_quad(a, qi, pi, q);
+    V3 X0[4], X1[4];
+    for (int k = 0; k < 4; ++k) {
+      X0[k] = geo::ld3(a.x0 + 3 * (int64_t)q[k]);
+      X1[k] = geo::ld3(a.x1 + 3 * (int64_t)q[k]);
+    }
+    if (geo::accd_class(a.kind, X0, X1, a.min_gap) != 1) {
+      const unsigned grp = __activemask();
+      const int lane = threadIdx.x & 31;
+      const int leader = __ffs(grp) - 1;
+      unsigned long long base = 0;
+      if (lane == leader) base = atomicAdd(a.counters, (unsigned long long)__popc(grp));
+      base = __shfl_sync(grp, base, leader);
+      a.out[base + __popc(grp & ((1u << lane) - 1u))] = e;
+    }
+  }
 }
 
 __global__ void k_pair_toi(int64_t n, int kind, const unsigned long long* __restrict__ pairs,
@@ -382,11 +506,25 @@ static int grid_for(int64_t n, int threads = 256) {
 #ifndef IBF_CCD_REBUILD
 #define IBF_CCD_REBUILD 16
 #endif
+// traversal over packed float child-box records (1) or the FP64 node arrays (0)
+#ifndef IBF_CCD_PACKED
+#define IBF_CCD_PACKED 1
+#endif
+// VF queries visited in Morton order of their boxes (1) or in vertex order (0)
+#ifndef IBF_CCD_VF_ORDER
+#define IBF_CCD_VF_ORDER 1
+#endif
+// filtered broad phase as traversal + a separate prefilter pass (1) or with
+// the prefilter inside the traversal (0)
+#ifndef IBF_CCD_SPLIT
+#define IBF_CCD_SPLIT 1
+#endif
 static int build_tree(ibf_ccd* c, int64_t n, cudaStream_t s, Tree& t, ibf_ccd::TreeCache* cache = nullptr) {
   const int64_t nn = std::max<int64_t>(2 * n - 1, 1);
   unsigned long long* keys_sorted = c->keys_sorted.p;
   int *left, *right, *parent, *flag;
   double *lo, *hi;
+  float4* packed4;
   bool refit_only = false;
   if (cache) {
     IBF_TRY(cache->keys_sorted.reserve(n));
@@ -396,10 +534,12 @@ static int build_tree(ibf_ccd* c, int64_t n, cudaStream_t s, Tree& t, ibf_ccd::T
     IBF_TRY(cache->flag.reserve(nn));
     IBF_TRY(cache->lo.reserve(3 * nn));
     IBF_TRY(cache->hi.reserve(3 * nn));
+    IBF_TRY(cache->packed.reserve(4 * nn));
     refit_only = cache->n == n && cache->uses < IBF_CCD_REBUILD;
     keys_sorted = cache->keys_sorted.p;
     left = cache->left.p, right = cache->right.p, parent = cache->parent.p, flag = cache->flag.p;
     lo = cache->lo.p, hi = cache->hi.p;
+    packed4 = cache->packed.p;
   } else {
     IBF_TRY(c->keys_sorted.reserve(n));
     IBF_TRY(c->node_left.reserve(nn));
@@ -408,10 +548,13 @@ static int build_tree(ibf_ccd* c, int64_t n, cudaStream_t s, Tree& t, ibf_ccd::T
     IBF_TRY(c->node_flag.reserve(nn));
     IBF_TRY(c->node_lo.reserve(3 * nn));
     IBF_TRY(c->node_hi.reserve(3 * nn));
+    IBF_TRY(c->node_packed.reserve(4 * nn));
     keys_sorted = c->keys_sorted.p;
     left = c->node_left.p, right = c->node_right.p, parent = c->node_parent.p, flag = c->node_flag.p;
     lo = c->node_lo.p, hi = c->node_hi.p;
+    packed4 = c->node_packed.p;
   }
+  PackedNode* packed = IBF_CCD_PACKED ? reinterpret_cast<PackedNode*>(packed4) : nullptr;
   if (!refit_only) {
     const int nparts = (int)std::min<int64_t>(grid_for(n), 148 * 2);
     IBF_TRY(c->dscratch.reserve(6 * (size_t)nparts + 8));
@@ -437,8 +580,11 @@ static int build_tree(ibf_ccd* c, int64_t n, cudaStream_t s, Tree& t, ibf_ccd::T
   if (cache) ++cache->uses;
   IBF_CUDA(cudaMemsetAsync(flag, 0, nn * sizeof(int), s));
   k_refit<<<grid_for(n), 256, 0, s>>>((int)n, keys_sorted, c->box_lo.p, c->box_hi.p, left, right, parent, flag, lo,
-                                       hi);
+                                       hi, packed);
   IBF_LAUNCH_CHECK();
+  t.packed = n > 1 ? packed : nullptr;
+  t.plo = c->box_lo.p;
+  t.phi = c->box_hi.p;
   t.n = (int)n;
   t.keys = keys_sorted;
   t.left = left;
@@ -484,14 +630,39 @@ static int broad_pass(ibf_ccd* c, int kind, const double* x0, const double* x1, 
   Tree tree;
   IBF_TRY(build_tree(c, nt, s, tree, (kind < 2 && IBF_CCD_REBUILD > 1) ? &c->tc[kind] : nullptr));
   tr.mark("tree", s);
+  // VF queries (surface vertices) in Morton order of their boxes, so the 32
+  // walks of a warp follow nearly the same path (EE and TT self-queries use
+  // the tree's own sorted keys); recomputed when the triangle tree is rebuilt
+  const unsigned long long* qorder = (kind == 0) ? nullptr : tree.keys;
+  if (kind == 0 && IBF_CCD_VF_ORDER) {
+    const bool fresh = !(IBF_CCD_REBUILD > 1) || c->tc[0].uses == 1 || c->vf_order_n != nq;
+    if (fresh) {
+      const int nparts = (int)std::min<int64_t>(grid_for(nq), 148 * 2);
+      IBF_TRY(c->dscratch.reserve(6 * (size_t)nparts + 8));
+      IBF_TRY(c->keys.reserve(nq));
+      IBF_TRY(c->vf_order.reserve(nq));
+      k_bounds<<<nparts, 256, 0, s>>>(nq, c->qlo.p, c->qhi.p, c->dscratch.p);
+      IBF_LAUNCH_CHECK();
+      k_morton<<<grid_for(nq), 256, 0, s>>>(nq, c->qlo.p, c->qhi.p, c->dscratch.p, nparts, c->keys.p);
+      IBF_LAUNCH_CHECK();
+      size_t need = 0;
+      cub::DeviceRadixSort::SortKeys(nullptr, need, c->keys.p, c->vf_order.p, (int)nq, 0, 64, s);
+      IBF_TRY(c->cub_tmp.reserve(need + 16));
+      size_t have = c->cub_tmp.cap;
+      IBF_CUDA(cub::DeviceRadixSort::SortKeys(c->cub_tmp.p, have, c->keys.p, c->vf_order.p, (int)nq, 0, 64, s));
+      c->vf_order_n = nq;
+    }
+    qorder = c->vf_order.p;
+  }
   IBF_TRY(c->counters.reserve(4));
   IBF_TRY(c->host.reserve(64));
   if (c->pairs.cap < 4096) IBF_TRY(c->pairs.reserve(1 << 16));
+  const bool split = filter && IBF_CCD_SPLIT;
+  TraverseArgs a;
   for (int attempt = 0; attempt < 3; ++attempt) {
     IBF_CUDA(cudaMemsetAsync(c->counters.p, 0, 2 * sizeof(unsigned long long), s));
-    TraverseArgs a;
     a.tree = tree;
-    a.qorder = (kind == 0) ? nullptr : tree.keys;
+    a.qorder = qorder;
     a.nq = nq;
     a.qlo = c->qlo.p;
     a.qhi = c->qhi.p;
@@ -501,7 +672,7 @@ static int broad_pass(ibf_ccd* c, int kind, const double* x0, const double* x1, 
     a.x0 = x0;
     a.x1 = x1;
     a.min_gap = min_gap;
-    a.filter = filter ? 1 : 0;
+    a.filter = (filter && !split) ? 1 : 0;
     a.out = c->pairs.p;
     a.cap = c->pairs.cap;
     a.counters = c->counters.p;
@@ -510,7 +681,10 @@ static int broad_pass(ibf_ccd* c, int kind, const double* x0, const double* x1, 
       // algorithmic: 48 B per query box + 48 B per primitive box (each leaf
       // read once) + 16 B per candidate pair out (booked after the count)
       KernelClock kc(KC_TRAVERSE, s, 48.0 * (nq + tree.n), 0.0, 0.0);
-      k_traverse<<<grid_for(nq, 128), 128, 0, s>>>(a);
+      const bool packed = tree.packed != nullptr;
+      auto kern = a.filter ? (packed ? k_traverse<true, true> : k_traverse<true, false>)
+                           : (packed ? k_traverse<false, true> : k_traverse<false, false>);
+      kern<<<grid_for(nq, 128), 128, 0, s>>>(a);
       IBF_LAUNCH_CHECK();
       IBF_CUDA(cudaMemcpyAsync(h, c->counters.p, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
       IBF_CUDA(cudaStreamSynchronize(s));
@@ -529,14 +703,35 @@ static int broad_pass(ibf_ccd* c, int kind, const double* x0, const double* x1, 
     IBF_TRY(c->pairs.reserve((size_t)h[0]));
   }
   tr.mark("traverse", s, *n_candidates);
+  const unsigned long long* unsorted = c->pairs.p;
+  if (split && *count) {
+    const int64_t n_all = *count;
+    IBF_TRY(c->pairs2.reserve(n_all));
+    IBF_CUDA(cudaMemsetAsync(c->counters.p, 0, sizeof(unsigned long long), s));
+    a.out = c->pairs2.p;
+    a.cap = c->pairs2.cap;
+    unsigned long long* h = (unsigned long long*)c->host.p;
+    {
+      // algorithmic: 8 B per candidate in, 8 vertices x 24 B gathered, 8 B per survivor out
+      KernelClock kc(KC_PREFILTER, s, 200.0 * (double)n_all, 0.0, (double)n_all);
+      k_prefilter<<<grid_for(n_all, 256), 256, 0, s>>>(a, n_all, c->pairs.p);
+      IBF_LAUNCH_CHECK();
+      IBF_CUDA(cudaMemcpyAsync(h, c->counters.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+      IBF_CUDA(cudaStreamSynchronize(s));
+      kc.bytes += 8.0 * (double)h[0];
+    }
+    *count = (int64_t)h[0];
+    unsorted = c->pairs2.p;
+    tr.mark("prefilter", s, *count);
+  }
   const int64_t cnt = *count;
   IBF_TRY(c->pairs_sorted.reserve(std::max<int64_t>(cnt, 1)));
   if (cnt) {
     size_t need = 0;
-    cub::DeviceRadixSort::SortKeys(nullptr, need, c->pairs.p, c->pairs_sorted.p, (int)cnt, 0, 64, s);
+    cub::DeviceRadixSort::SortKeys(nullptr, need, unsorted, c->pairs_sorted.p, (int)cnt, 0, 64, s);
     IBF_TRY(c->cub_tmp.reserve(need + 16));
     size_t have = c->cub_tmp.cap;
-    IBF_CUDA(cub::DeviceRadixSort::SortKeys(c->cub_tmp.p, have, c->pairs.p, c->pairs_sorted.p, (int)cnt, 0, 64, s));
+    IBF_CUDA(cub::DeviceRadixSort::SortKeys(c->cub_tmp.p, have, unsorted, c->pairs_sorted.p, (int)cnt, 0, 64, s));
   }
   tr.mark("sort", s, cnt);
   tr.mark("exit", s);

@@ -89,6 +89,7 @@ enum KernelClockId {
   KC_TRAVERSE,      // k_traverse: LBVH queries + fused ACCD prefilter
   KC_TOI,           // k_pair_toi: ACCD narrow phase on the survivors
   KC_PCG,           // k_pcg: one persistent PCG solve
+  KC_PREFILTER,     // k_prefilter: ACCD prefilter over the broad-phase candidates
   KC_COUNT
 };
 extern std::atomic<bool> g_kclock_on;

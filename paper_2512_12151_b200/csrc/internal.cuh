@@ -116,14 +116,19 @@ __device__ __forceinline__ int row_at(const Operator& op, int pos) { return op.p
 
 // Host + device halves of the sliced symmetric pattern (built once).
 //
-// Rows are placed at storage positions in windows of SELL_WINDOW rows, each
-// window sorted by (upper count, lower count) descending, so the 32 rows of a
-// slice have near-equal slot counts: on a surface-heavy mesh (squishy balls)
-// lattice order leaves 36 % of the upper slots and 41 % of the lower entries
-// as padding, the sorted windows 6 % and 16 %.  A window is one PCG CTA's
-// rows, so each CTA still owns the same rows as a set (vectors stay in row
-// order; the permutation only changes which thread takes which row).
-constexpr int SELL_WINDOW = 256;
+// Rows can be placed at storage positions in windows of SELL_WINDOW rows,
+// each window sorted by (upper count, lower count) descending, so the 32 rows
+// of a slice have near-equal slot counts (vectors stay in row order; the
+// permutation only changes which thread takes which row).  On the squishy
+// balls lattice order leaves 36 % of the upper slots and 41 % of the lower
+// entries as padding, 256-row windows 6 % and 16 % — and k_pcg measured
+// 201 / 219 / 255 us per CG iteration with windows of 1 / 64 / 256 rows
+// (DESIGN.md): the scattered per-row vector accesses cost more than the
+// padding.  Default 1 (positions = rows).
+#ifndef IBF_SELL_WINDOW
+#define IBF_SELL_WINDOW 1
+#endif
+constexpr int SELL_WINDOW = IBF_SELL_WINDOW;   // 1: no sorting (positions = rows)
 struct SellPattern {
   int64_t n = 0, nb = 0, nl = 0;      // rows, real blocks, real strict-upper blocks
   int n_slices = 0;
@@ -218,18 +223,22 @@ struct ibf_ccd {
   ibf::DevBuf<int> order;                               // sorted primitive order
   ibf::DevBuf<int> node_left, node_right, node_parent, node_flag;
   ibf::DevBuf<double> node_lo, node_hi;
+  ibf::DevBuf<float4> node_packed;                      // 4 per internal node (ccd.cu PackedNode)
   // VF (triangle) and EE (edge) trees kept between calls: later calls refit
   // the cached topology to the new boxes; it is rebuilt every few calls
   struct TreeCache {
     ibf::DevBuf<unsigned long long> keys_sorted;
     ibf::DevBuf<int> left, right, parent, flag;
     ibf::DevBuf<double> lo, hi;
+    ibf::DevBuf<float4> packed;
     int64_t n = -1;
     int uses = 0;
   } tc[2];
   ibf::DevBuf<unsigned char> cub_tmp;
   // candidate / survivor pairs
-  ibf::DevBuf<unsigned long long> pairs, pairs_sorted;
+  ibf::DevBuf<unsigned long long> pairs, pairs2, pairs_sorted;
+  ibf::DevBuf<unsigned long long> vf_order;             // VF query order (Morton keys | query)
+  int64_t vf_order_n = -1;
   ibf::DevBuf<unsigned long long> counters;             // [0] emitted, [1] all candidates
   ibf::DevBuf<double> pair_toi;
   int64_t n_vf = 0, n_ee = 0;                           // candidates of the last call

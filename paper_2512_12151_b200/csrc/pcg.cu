@@ -251,11 +251,9 @@ __device__ __forceinline__ void acc_lower(const double b[9], double x0, double x
 template <class Gather, class Terms = StoredTerms>
 __device__ __forceinline__ void row_product(const Operator& op, const Gather& gp, int pos, int i, double y[3],
                                             const Terms& terms = Terms()) {
-  // storage by position; row i (= row_at(pos)) for the contact incidences
-  // and the padding sentinel: a padded upper slot has col == i past slot 0
-  // (slot 0 is the diagonal), a padded lower entry points at the zero block,
-  // and both sit at the end of the row, so the row stops at its first one —
-  // lanes of shorter rows issue no loads for the slice's longer rows' slots
+  // storage by position (row_at maps positions to rows: internal.cuh); row i
+  // for the contact incidences.  Padding slots are zero blocks whose column
+  // is the position's own row, so they add exact zeros.
   const int s = pos >> 5, lane = pos & 31;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
   {
@@ -266,10 +264,9 @@ __device__ __forceinline__ void row_product(const Operator& op, const Gather& gp
     if (IBF_SPMV_UNROLL >= 2) {
       // column indices are loaded one slot pair ahead, so the p gathers of a
       // pair never wait on an index load (the chain per pair is one level)
-      int n0 = w > 0 ? __ldg(C) : 0, n1 = w > 1 ? __ldg(C + 32) : i;
+      int n0 = w > 0 ? __ldg(C) : 0, n1 = w > 1 ? __ldg(C + 32) : 0;
       for (; k + 2 <= w; k += 2) {
         const int j0 = n0, j1 = n1;
-        if (k > 0 && j0 == i) break;
         if (k + 2 < w) n0 = __ldg(C + 32 * (k + 2));
         if (k + 3 < w) n1 = __ldg(C + 32 * (k + 3));
         const double* B = V + 288 * (size_t)k;
@@ -288,7 +285,6 @@ __device__ __forceinline__ void row_product(const Operator& op, const Gather& gp
     }
     for (; k < w; ++k) {
       const int j = __ldg(C + 32 * k);
-      if (k > 0 && j == i) break;
       const double* B = V + 288 * (size_t)k;
       double b[9];
 #pragma unroll
@@ -301,13 +297,11 @@ __device__ __forceinline__ void row_product(const Operator& op, const Gather& gp
   {
     const int l0 = __ldg(op.low_ptr + s), w = (__ldg(op.low_ptr + s + 1) - l0) >> 5;
     const int2* L = op.low + l0 + lane;
-    const int zq = op.zero_q;
     int t = 0;
     if (IBF_SPMV_UNROLL >= 2) {
-      int2 n0 = w > 0 ? __ldg(L) : make_int2(zq, 0), n1 = w > 1 ? __ldg(L + 32) : make_int2(zq, 0);
+      int2 n0 = w > 0 ? __ldg(L) : make_int2(0, 0), n1 = w > 1 ? __ldg(L + 32) : make_int2(0, 0);
       for (; t + 2 <= w; t += 2) {
         const int2 e0 = n0, e1 = n1;
-        if (e0.x == zq) break;
         if (t + 2 < w) n0 = __ldg(L + 32 * (t + 2));
         if (t + 3 < w) n1 = __ldg(L + 32 * (t + 3));
         const double* B0 = op.val + qel(e0.x, 0);
@@ -327,7 +321,6 @@ __device__ __forceinline__ void row_product(const Operator& op, const Gather& gp
     }
     for (; t < w; ++t) {
       const int2 le = __ldg(L + 32 * t);
-      if (le.x == zq) break;
       const double* B = op.val + qel(le.x, 0);
       double b[9];
 #pragma unroll
@@ -1356,7 +1349,7 @@ int SellPattern::build(int64_t n_, const std::vector<int64_t>& rows_, const std:
 Operator SellPattern::op() const {
   Operator o;
   o.n = (int)n;
-  o.perm = perm.p;
+  o.perm = SELL_WINDOW > 1 ? perm.p : nullptr;   // identity: no lookup
   o.zero_q = zero_q;
   o.slice_ptr = slice_ptr.p;
   o.col = col.p;

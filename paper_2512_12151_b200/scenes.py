@@ -117,7 +117,7 @@ def _sphere_map(c, radius, blend=0.8):
 
 
 def squishy_ball(n=32, shell=2, stem=23, tip=16, pitch=3, cell=0.01, center=(0.0, 0.0, 0.0),
-                 reorder=True) -> TetMesh:
+                 reorder=False) -> TetMesh:
     """Squishy ball: a hollow core with thin strands all over it.
 
     The core is the outer `shell` Kuhn-cell layers of an n^3 grid mapped onto
@@ -333,7 +333,7 @@ def c4_scene(n=42, radius=0.1, gap=0.001, plate_speed=0.1, h=0.01, layers=None, 
 
 
 def squishy_scene(cell=0.02, n=32, stem=23, tip=16, shell=2, gap=None, plate_speed=1.0, plate_stop=None, h=0.01,
-                  walls=True, seed=7, balls=5, reorder=True):
+                  walls=True, seed=7, balls=5, reorder=False):
     """C4, paper-scale: five squishy balls in a box, pressed by a plate.
 
     Each ball is a `squishy_ball` (hollow core + 600 strands; the defaults

@@ -34,11 +34,11 @@ ap.add_argument("--load", default=None)
 ap.add_argument("--dump", default=None)
 ap.add_argument("--iters", type=int, default=200)
 ap.add_argument("--ncu", action="store_true", help="profile one PCG launch (cudaProfilerStart/Stop)")
-ap.add_argument("--no-reorder", action="store_true", help="keep the lattice vertex numbering")
+ap.add_argument("--reorder", action="store_true", help="Morton vertex numbering instead of the lattice's")
 args = ap.parse_args()
 
 system, state, params = scenes.squishy_scene(cell=args.cell, n=args.n, stem=args.stem, tip=args.tip,
-                                             plate_speed=args.plate_speed, reorder=not args.no_reorder)
+                                             plate_speed=args.plate_speed, reorder=args.reorder)
 aset = ActiveSet()
 aset.ensure(system.n_vertices)
 x, v = to_dev(state.x), to_dev(state.v)
