@@ -417,6 +417,9 @@ def run_ours(args):
     if ws > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
+    prof_range = os.environ.get("IBF_BENCH_PROFILE_RANGE") == "1"   # ncu --profile-from-start off
+    if prof_range:
+        torch.cuda.profiler.start()
     with ClockSampler(local) as clocks:
         t0 = time.perf_counter()
         for j in range(args.steps):
@@ -449,6 +452,8 @@ def run_ours(args):
             pass_ms.append(max(r.wall_ms for r in diag.iterations))
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
+    if prof_range:
+        torch.cuda.profiler.stop()
     launches = L.ibf_launch_count() - launches0 - mon_launches
     kclocks = _lib.kernel_clocks(on=0)
     frame_ms = [e[1].elapsed_time(e[2]) for e in evs]

@@ -259,6 +259,28 @@ int ibf_vec_sub(int64_t n, const double* a, const double* b, double* out, ibf_st
 int ibf_velocity_update(int64_t n, const double* x, const double* x_t, double h, double* v,
                         ibf_stream st);
 
+/* ------------------------------------------- row-partitioned PCG (multi-GPU)
+ * Replaces the single-process matvec / pcg_solve (intact/sparse.py:64-73,
+ * :99-150) by a row partition over `world` partitions:
+ * each holds the replicated operator, computes H p for its contiguous row
+ * chunk, and per CG iteration allreduces pAp and (|r|^2, r.z) and allgathers
+ * its z rows.  The reference has no counterpart (it is single-process). */
+typedef struct ibf_dist ibf_dist;
+/* NCCL unique id (128 bytes) for ibf_dist_create; rank 0 makes it and
+ * broadcasts it (e.g. torch.distributed).  NCCL is loaded at run time
+ * (libnccl.so.2, the one torch already loaded); IBF_ERR_CUDA without it. */
+int ibf_dist_unique_id(void* out128);
+/* One rank of a world-rank NCCL communicator on the current device. */
+int ibf_dist_create(int rank, int world, const void* id128, ibf_dist** out);
+/* All `parts` partitions in this process on the current device (exchanges
+ * as device copies, reductions summed in partition order): the single-GPU
+ * check of the partition arithmetic. */
+int ibf_dist_create_local(int parts, ibf_dist** out);
+void ibf_dist_destroy(ibf_dist* d);
+/* Route the system's PCG solves (ibf_system_pcg, ibf_solve_subproblem) through
+ * the partition (NULL: the single-GPU persistent kernel again). */
+int ibf_system_set_dist(ibf_system* s, ibf_dist* d);
+
 /* ---------------------------------------------- standalone sparse matrices */
 typedef struct ibf_bsr ibf_bsr;
 /* BlockSparseMatrix(n, rows, cols, blocks) (intact/sparse.py:49-62): coalesces

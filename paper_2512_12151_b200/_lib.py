@@ -86,6 +86,11 @@ _PROTOS = {
     "ibf_launch_count": (C.c_ulonglong, []),
     "ibf_bsr_export": (_int, [_vp, _vp, _vp, _vp, _vp]),
     "ibf_pcg_tuning": (_int, [_i64, _int]),
+    "ibf_dist_unique_id": (_int, [_vp]),
+    "ibf_dist_create": (_int, [_int, _int, _vp, C.POINTER(_vp)]),
+    "ibf_dist_create_local": (_int, [_int, C.POINTER(_vp)]),
+    "ibf_dist_destroy": (None, [_vp]),
+    "ibf_system_set_dist": (_int, [_vp, _vp]),
     "ibf_pcg_last_shape": (_int, [_vp]),
     "ibf_kernel_clocks": (_int, [_int, _vp, _int]),
     "ibf_system_counts": (_int, [_vp, _vp, _int]),

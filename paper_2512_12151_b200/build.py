@@ -18,7 +18,8 @@ CSRC = os.path.join(HERE, "csrc")
 OUT = os.environ.get("IBF_BUILD_OUT", os.path.join(HERE, "libibf.so"))
 BUILD = os.environ.get("IBF_BUILD_DIR", os.path.join(CSRC, "build"))
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-SOURCES = ["pcg.cu", "system.cu", "contact.cu", "ccd.cu", "newton.cu", "friction.cu", "surface.cu", "export.cpp"]
+SOURCES = ["pcg.cu", "system.cu", "contact.cu", "ccd.cu", "newton.cu", "friction.cu", "surface.cu", "dist.cu",
+           "export.cpp"]
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
@@ -57,7 +58,7 @@ def build(force=False, verbose=False):
         results = list(ex.map(lambda s: _compile(s, verbose), SOURCES))
     objs = [o for o, _ in results]
     tmp = OUT + ".tmp"
-    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs]
+    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs, "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")

@@ -160,6 +160,37 @@ struct PcgWork {
 
 int pcg_solve(const Operator& op, const double* rhs, double* x_out, double rel_tol,
               int64_t max_iters, PcgWork& w, cudaStream_t s);
+
+// ---- row-partitioned PCG (SURVEY.md §8(e), C4 over several GPUs) ----
+// Rows are split into `world` contiguous chunks of `chunk` rows (a multiple
+// of 32); partition r owns rows [r*chunk, min(n, (r+1)*chunk)).  Every
+// partition holds the whole (replicated) operator and full-length z / p
+// vectors, computes q = H p only for its own rows, keeps p valid on its halo
+// (the rows its own rows' blocks and every contact / friction term touch),
+// and exchanges per CG iteration: one allreduce of pAp, one of (|r|^2, r.z),
+// and one allgather of its z rows.  The exchanges go through a DistComm:
+// NCCL across processes (one GPU each), or "local" — all partitions in this
+// process, allgather as device copies — which is how one GPU tests the
+// partition arithmetic against the unpartitioned solve.
+struct PartBuf;
+struct DistWork {
+  std::vector<PartBuf*> parts;         // the partitions this process runs
+  DevBuf<double> gsc;                  // reduced scalars (allreduce result)
+  DevBuf<double> xfull;                // padded full x (restart, result gather)
+  DevBuf<int> counter;
+  DevBuf<unsigned long long> ptrs;     // device copy of the partitions' scalar buffers (local mode)
+  int ptrs_n = -1;
+  HostScratch host;
+  int64_t n = -1, chunk = 0;
+  int world = 0;
+  ~DistWork();
+};
+int pcg_solve_dist(const Operator& op, const std::vector<int64_t>& brows, const std::vector<int64_t>& bcols,
+                   const double* rhs, double* x_out, double rel_tol, int64_t max_iters, PcgWork& w, DistWork& dw,
+                   ibf_dist* d, cudaStream_t s);
+// communicator primitives (dist.cu); in place, on stream s
+int dist_allreduce_sum(ibf_dist* d, double* buf, int count, cudaStream_t s);
+int dist_allgather(ibf_dist* d, const double* send, double* recv, size_t count_per_rank, cudaStream_t s);
 // after pcg_solve: (iterations, converged, rel_residual) on the host (syncs).
 int pcg_info(PcgWork& w, double info[3], cudaStream_t s);
 // host copy of the real blocks (sorted (row, col) order, (nb,9)) of a pattern
@@ -171,6 +202,13 @@ int invert_diag_blocks(int n, const double* val, const int* diag_q, double* pinv
 }  // namespace ibf
 
 // ----------------------------------------------------------- opaque handles
+
+// Row partition of the PCG over `world` partitions (ibf_dist_create*).
+struct ibf_dist {
+  int rank = 0, world = 1;
+  bool local = true;        // all partitions in this process (no NCCL)
+  void* comm = nullptr;     // ncclComm_t when !local
+};
 
 struct ibf_contacts {
   int admit_all = 0;

@@ -376,7 +376,7 @@ extern "C" int ibf_solve_subproblem(ibf_system* s, ibf_contacts* c, const double
     k_neg<<<grid_for(n3), 256, 0, stream>>>(n3, grad, rhs);
     IBF_LAUNCH_CHECK();
     s->t_pcg.begin(stream);
-    IBF_TRY(pcg_solve(s->op(), rhs, p, cg_tol, 10 * n, s->work, stream));
+    IBF_TRY(system_pcg(s, rhs, p, cg_tol, 10 * n, stream));
     s->t_pcg.end(stream);
     tr.mark("pcg", stream);
     k_dot_part<<<dot_parts, 256, 0, stream>>>(n3, grad, p, dpart);

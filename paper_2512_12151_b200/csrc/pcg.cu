@@ -1516,3 +1516,418 @@ extern "C" int ibf_pcg_last_shape(int64_t* out) {
   for (int k = 0; k < 6; ++k) out[k] = ibf::g_last_shape[k].load();
   return IBF_OK;
 }
+
+// ================================================ row-partitioned PCG
+// (internal.cuh: DistWork).  Same arithmetic as k_pcg, split at the points
+// where the partitions exchange data: per CG iteration
+//   A  term dots (all terms: each partition's rows may touch any), q = H p_k
+//      on own rows, p_k on own + halo rows, pAp partial      -> allreduce
+//   B  x, r, z on own rows, |r|^2 and r.z partials           -> allreduce
+//      own z rows                                            -> allgather
+// Host-driven (the exchanges sit between phases); scalars on the host.
+namespace ibf {
+
+struct PartBuf {
+  int64_t r0 = 0, r1 = 0;              // own rows
+  DevBuf<double> z, p[2], q, r, X, t, tf, part, scal;
+  DevBuf<int> halo;                    // rows outside [r0, r1) where p must stay valid
+  DevBuf<uint8_t> hflag;
+  std::vector<int> halo_static;        // structural halo (pattern), built once
+  int n_halo = 0;
+};
+
+DistWork::~DistWork() {
+  for (PartBuf* p : parts) delete p;
+}
+
+constexpr int PD_THREADS = 256;
+
+static int pd_grid(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>(div_up(n, PD_THREADS), 4LL * sm_count())); }
+
+__global__ void k_pd_init(Operator op, int64_t r0, int64_t r1, const double* __restrict__ rhs, double* __restrict__ r,
+                          double* __restrict__ z, double* __restrict__ x, double* __restrict__ part) {
+  __shared__ double red[32];
+  double bb = 0.0, rz = 0.0;
+  for (int64_t i = r0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < r1; i += (int64_t)gridDim.x * blockDim.x) {
+    const double b0 = rhs[3 * i], b1 = rhs[3 * i + 1], b2 = rhs[3 * i + 2];
+    double zv[3];
+    apply_pinv6(op.pinv + PINV_STRIDE * i, b0, b1, b2, zv);
+    r[3 * i] = b0; r[3 * i + 1] = b1; r[3 * i + 2] = b2;
+    z[3 * i] = zv[0]; z[3 * i + 1] = zv[1]; z[3 * i + 2] = zv[2];
+    x[3 * i] = 0.0; x[3 * i + 1] = 0.0; x[3 * i + 2] = 0.0;
+    bb += b0 * b0 + b1 * b1 + b2 * b2;
+    rz += b0 * zv[0] + b1 * zv[1] + b2 * zv[2];
+  }
+  bb = block_sum(bb, red);
+  rz = block_sum(rz, red);
+  if (threadIdx.x == 0) {
+    part[blockIdx.x] = bb;
+    part[gridDim.x + blockIdx.x] = rz;
+  }
+}
+
+// fixed-order sums of `slots` rows of G block partials -> out[slot]
+__global__ void k_pd_sum(const double* __restrict__ part, int G, int slots, double* __restrict__ out) {
+  const int slot = threadIdx.x >> 5;
+  if (slot < slots) {
+    const double v = warp_sum_array(part + (size_t)slot * G, G);
+    if ((threadIdx.x & 31) == 0) out[slot] = v;
+  }
+}
+
+// out[k] = sum over partitions (in partition order) of parts[j][k]
+__global__ void k_pd_sum_parts(const double* const* __restrict__ parts, int np, int count, double* __restrict__ out) {
+  const int k = threadIdx.x;
+  if (k < count) {
+    double v = 0.0;
+    for (int j = 0; j < np; ++j) v += parts[j][k];
+    out[k] = v;
+  }
+}
+
+__global__ void k_pd_dots(Operator op, DirGather gd) { term_dots(op, gd); }
+__global__ void k_pd_dots_plain(Operator op, PlainGather gx) { term_dots(op, gx); }
+
+__global__ void __launch_bounds__(PD_THREADS) k_pd_a(Operator op, DirGather gd, int64_t r0, int64_t r1,
+                                                     double* __restrict__ pk, double* __restrict__ q,
+                                                     const int* __restrict__ halo, int nh, double* __restrict__ part) {
+  __shared__ double red[32];
+  double acc = 0.0;
+  const int64_t S = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = r0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < r1; i += S) {
+    double v[3], pv[3];
+    row_product(op, gd, (int)i, (int)i, v);
+    gd.get((int)i, pv[0], pv[1], pv[2]);
+    pk[3 * i] = pv[0]; pk[3 * i + 1] = pv[1]; pk[3 * i + 2] = pv[2];
+    q[3 * i] = v[0]; q[3 * i + 1] = v[1]; q[3 * i + 2] = v[2];
+    acc += pv[0] * v[0] + pv[1] * v[1] + pv[2] * v[2];
+  }
+  // p_k on the halo: the same fused z + beta p as every reader forms
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nh; k += S) {
+    const int j = halo[k];
+    double pv[3];
+    gd.get(j, pv[0], pv[1], pv[2]);
+    pk[3 * (size_t)j] = pv[0]; pk[3 * (size_t)j + 1] = pv[1]; pk[3 * (size_t)j + 2] = pv[2];
+  }
+  acc = block_sum(acc, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = acc;
+}
+
+__global__ void __launch_bounds__(PD_THREADS) k_pd_b(Operator op, int64_t r0, int64_t r1, double alpha,
+                                                     const double* __restrict__ pk, const double* __restrict__ q,
+                                                     double* __restrict__ r, double* __restrict__ z,
+                                                     const double* __restrict__ xc, double* __restrict__ xn,
+                                                     double* __restrict__ part) {
+  __shared__ double red[32];
+  double rr = 0.0, rz = 0.0;
+  for (int64_t i = r0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < r1; i += (int64_t)gridDim.x * blockDim.x) {
+    double rv[3], zv[3];
+    for (int c = 0; c < 3; ++c) {
+      const size_t e = 3 * (size_t)i + c;
+      xn[e] = xc[e] + alpha * pk[e];
+      rv[c] = r[e] - alpha * q[e];
+      r[e] = rv[c];
+      rr += rv[c] * rv[c];
+    }
+    apply_pinv6(op.pinv + PINV_STRIDE * i, rv[0], rv[1], rv[2], zv);
+    z[3 * i] = zv[0]; z[3 * i + 1] = zv[1]; z[3 * i + 2] = zv[2];
+    rz += rv[0] * zv[0] + rv[1] * zv[1] + rv[2] * zv[2];
+  }
+  rr = block_sum(rr, red);
+  rz = block_sum(rz, red);
+  if (threadIdx.x == 0) {
+    part[blockIdx.x] = rr;
+    part[gridDim.x + blockIdx.x] = rz;
+  }
+}
+
+// restart: r = b - H x (x full), z = P^-1 r, r.z partials
+__global__ void __launch_bounds__(PD_THREADS) k_pd_restart(Operator op, PlainGather gx, int64_t r0, int64_t r1,
+                                                           const double* __restrict__ rhs, double* __restrict__ r,
+                                                           double* __restrict__ z, double* __restrict__ part) {
+  __shared__ double red[32];
+  double rz = 0.0;
+  for (int64_t i = r0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < r1; i += (int64_t)gridDim.x * blockDim.x) {
+    double v[3], zv[3], rv[3];
+    row_product(op, gx, (int)i, (int)i, v);
+    for (int c = 0; c < 3; ++c) {
+      rv[c] = rhs[3 * i + c] - v[c];
+      r[3 * i + c] = rv[c];
+    }
+    apply_pinv6(op.pinv + PINV_STRIDE * i, rv[0], rv[1], rv[2], zv);
+    z[3 * i] = zv[0]; z[3 * i + 1] = zv[1]; z[3 * i + 2] = zv[2];
+    rz += rv[0] * zv[0] + rv[1] * zv[1] + rv[2] * zv[2];
+  }
+  rz = block_sum(rz, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = rz;
+}
+
+// halo of a partition: static (pattern) rows plus every term vertex outside [r0, r1)
+__global__ void k_pd_mark_terms(const int* __restrict__ quad, int64_t nq4, int64_t r0, int64_t r1,
+                                uint8_t* __restrict__ flag) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nq4; k += (int64_t)gridDim.x * blockDim.x) {
+    const int v = quad[k];
+    if (v < r0 || v >= r1) flag[v] = 1;
+  }
+}
+__global__ void k_pd_collect(const uint8_t* __restrict__ flag, int64_t n, int* __restrict__ out, int* __restrict__ cnt) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+    if (flag[v]) out[atomicAdd(cnt, 1)] = (int)v;
+}
+
+__global__ void k_pd_copy_rows(const double* __restrict__ src, double* __restrict__ dst, int64_t r0, int64_t r1) {
+  for (int64_t e = 3 * r0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < 3 * r1; e += (int64_t)gridDim.x * blockDim.x)
+    dst[e] = src[e];
+}
+
+}  // namespace ibf
+
+namespace ibf {
+
+// sum the partitions' scalars: NCCL allreduce of this rank's, or the local
+// partitions' in partition order -> dw.gsc[0..count) -> host
+static int pd_reduce(ibf_dist* d, DistWork& dw, int count, double* host, cudaStream_t s) {
+  if (d->local) {
+    // the partitions' scalar buffers never move after setup: upload their
+    // addresses once
+    if (dw.ptrs_n != (int)dw.parts.size()) {
+      std::vector<unsigned long long> ptrs;
+      for (PartBuf* p : dw.parts) ptrs.push_back((unsigned long long)p->scal.p);
+      IBF_TRY(dw.ptrs.reserve(ptrs.size()));
+      IBF_CUDA(cudaMemcpyAsync(dw.ptrs.p, ptrs.data(), ptrs.size() * sizeof(unsigned long long),
+                               cudaMemcpyHostToDevice, s));
+      IBF_CUDA(cudaStreamSynchronize(s));
+      dw.ptrs_n = (int)dw.parts.size();
+    }
+    k_pd_sum_parts<<<1, 32, 0, s>>>(reinterpret_cast<const double* const*>(dw.ptrs.p), dw.ptrs_n, count, dw.gsc.p);
+    IBF_LAUNCH_CHECK();
+  } else {
+    IBF_CUDA(cudaMemcpyAsync(dw.gsc.p, dw.parts[0]->scal.p, count * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    IBF_TRY(dist_allreduce_sum(d, dw.gsc.p, count, s));
+  }
+  IBF_CUDA(cudaMemcpyAsync(host, dw.gsc.p, count * sizeof(double), cudaMemcpyDeviceToHost, s));
+  IBF_CUDA(cudaStreamSynchronize(s));
+  return IBF_OK;
+}
+
+// every partition's own rows of the full vectors v(part) -> all partitions
+static int pd_allgather(ibf_dist* d, DistWork& dw, DevBuf<double> PartBuf::*vec, cudaStream_t s) {
+  if (d->local) {
+    for (PartBuf* a : dw.parts)
+      for (PartBuf* b : dw.parts)
+        if (a != b && a->r1 > a->r0)
+          IBF_CUDA(cudaMemcpyAsync((b->*vec).p + 3 * a->r0, (a->*vec).p + 3 * a->r0,
+                                   3 * (a->r1 - a->r0) * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    return IBF_OK;
+  }
+  PartBuf* p = dw.parts[0];
+  // the own chunk (padded length) in place: send = recv + rank * chunk
+  double* full = (p->*vec).p;
+  return dist_allgather(d, full + 3 * p->r0, full, 3 * (size_t)dw.chunk, s);
+}
+
+int pcg_solve_dist(const Operator& op, const std::vector<int64_t>& brows, const std::vector<int64_t>& bcols,
+                   const double* rhs, double* x_out, double rel_tol, int64_t max_iters, PcgWork& w, DistWork& dw,
+                   ibf_dist* d, cudaStream_t s) {
+  const int64_t n = op.n;
+  const int W = d->world;
+  if (max_iters <= 0) max_iters = 10LL * n;
+  const int64_t chunk = div_up(div_up(std::max<int64_t>(n, 1), W), 32) * 32;
+  const int64_t npad = chunk * W;
+  // (re)build the partitions: own ranges, buffers, static halos
+  if (dw.n != n || dw.world != W) {
+    for (PartBuf* p : dw.parts) delete p;
+    dw.parts.clear();
+    const int first = d->local ? 0 : d->rank, last = d->local ? W : d->rank + 1;
+    for (int r = first; r < last; ++r) {
+      PartBuf* p = new PartBuf();
+      p->r0 = std::min<int64_t>(n, r * chunk);
+      p->r1 = std::min<int64_t>(n, (r + 1) * chunk);
+      std::vector<uint8_t> f(n, 0);
+      for (size_t b = 0; b < brows.size(); ++b) {
+        const int64_t i = brows[b], j = bcols[b];
+        const bool oi = i >= p->r0 && i < p->r1, oj = j >= p->r0 && j < p->r1;
+        if (oi && !oj) f[j] = 1;
+        if (oj && !oi) f[i] = 1;
+      }
+      for (int64_t v = 0; v < n; ++v)
+        if (f[v]) p->halo_static.push_back((int)v);
+      dw.parts.push_back(p);
+    }
+    dw.n = n;
+    dw.world = W;
+    dw.chunk = chunk;
+    dw.ptrs_n = -1;
+  }
+  IBF_TRY(dw.gsc.reserve(8));
+  IBF_TRY(dw.xfull.reserve(3 * npad));
+  IBF_TRY(dw.host.reserve(16 * sizeof(double)));
+  double* hs = (double*)dw.host.p;
+  const size_t nv = 3 * (size_t)npad;
+  const int G = pd_grid(chunk);
+  for (PartBuf* p : dw.parts) {
+    IBF_TRY(p->z.reserve(nv));
+    IBF_TRY(p->p[0].reserve(nv));
+    IBF_TRY(p->p[1].reserve(nv));
+    IBF_TRY(p->q.reserve(nv));
+    IBF_TRY(p->r.reserve(nv));
+    IBF_TRY(p->X.reserve(3 * nv));
+    IBF_TRY(p->part.reserve(4 * (size_t)G));
+    IBF_TRY(p->scal.reserve(4));
+    IBF_TRY(p->t.reserve(std::max(op.contact.n, 1)));
+    IBF_TRY(p->tf.reserve(3 * (size_t)std::max(op.friction.n, 1)));
+    IBF_TRY(p->hflag.reserve(n));
+    IBF_TRY(p->halo.reserve(n + 1));
+    // halo = static rows | term vertices outside the own range
+    IBF_CUDA(cudaMemsetAsync(p->hflag.p, 0, n, s));
+    if (!p->halo_static.empty()) {
+      std::vector<uint8_t> f(n, 0);
+      for (int v : p->halo_static) f[v] = 1;
+      IBF_CUDA(cudaMemcpyAsync(p->hflag.p, f.data(), n, cudaMemcpyHostToDevice, s));
+      IBF_CUDA(cudaStreamSynchronize(s));    // f is a host temporary
+    }
+    if (op.contact.n)
+      k_pd_mark_terms<<<pd_grid(4LL * op.contact.n), PD_THREADS, 0, s>>>(op.contact.quad, 4LL * op.contact.n, p->r0,
+                                                                         p->r1, p->hflag.p);
+    if (op.friction.n)
+      k_pd_mark_terms<<<pd_grid(4LL * op.friction.n), PD_THREADS, 0, s>>>(op.friction.quad, 4LL * op.friction.n,
+                                                                          p->r0, p->r1, p->hflag.p);
+    IBF_TRY(dw.counter.reserve(2 * dw.parts.size() + 2));
+    IBF_CUDA(cudaMemsetAsync(dw.counter.p, 0, sizeof(int), s));
+    k_pd_collect<<<pd_grid(n), PD_THREADS, 0, s>>>(p->hflag.p, n, p->halo.p, dw.counter.p);
+    IBF_LAUNCH_CHECK();
+    int nh = 0;
+    IBF_CUDA(cudaMemcpyAsync(&nh, dw.counter.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    IBF_CUDA(cudaStreamSynchronize(s));
+    p->n_halo = nh;
+  }
+  auto op_of = [&](PartBuf* p) {
+    Operator o = op;
+    o.contact.t = p->t.p;
+    o.friction.t = p->tf.p;
+    return o;
+  };
+  auto Xb = [&](PartBuf* p, int k) { return p->X.p + (size_t)k * nv; };
+  // ---- r = b, z = P^-1 r, x = 0
+  for (PartBuf* p : dw.parts) {
+    k_pd_init<<<G, PD_THREADS, 0, s>>>(op, p->r0, p->r1, rhs, p->r.p, p->z.p, Xb(p, 0), p->part.p);
+    k_pd_sum<<<1, 64, 0, s>>>(p->part.p, G, 2, p->scal.p);
+    IBF_LAUNCH_CHECK();
+  }
+  IBF_TRY(pd_reduce(d, dw, 2, hs, s));
+  const double bnorm = sqrt(hs[0]);
+  double rz = hs[1];
+  IBF_TRY(pd_allgather(d, dw, &PartBuf::z, s));
+  int cur = 0, best = 0, result = 0;
+  double best_res = bnorm, rel = 0.0, beta = 0.0;
+  int64_t iters = 0;
+  bool conv = false, first = true, done = false;
+  int pb = 0;
+  if (bnorm == 0.0) {
+    conv = true;
+    done = true;
+  }
+  // done: converged or pAp <= 0; otherwise the cap is reached (best iterate)
+  for (int64_t it = 1; !done && it <= max_iters; ++it) {
+    // ---- A
+    for (PartBuf* p : dw.parts) {
+      const Operator o = op_of(p);
+      const DirGather gd{p->z.p, p->p[pb ^ 1].p, beta, first};
+      if (op.contact.n || op.friction.n) k_pd_dots<<<pd_grid(std::max(op.contact.n, op.friction.n)), PD_THREADS, 0, s>>>(o, gd);
+      k_pd_a<<<G, PD_THREADS, 0, s>>>(o, gd, p->r0, p->r1, p->p[pb].p, p->q.p, p->halo.p, p->n_halo, p->part.p);
+      k_pd_sum<<<1, 32, 0, s>>>(p->part.p, G, 1, p->scal.p);
+      IBF_LAUNCH_CHECK();
+    }
+    IBF_TRY(pd_reduce(d, dw, 1, hs, s));
+    const double pap = hs[0];
+    if (pap <= 0.0) {
+      result = best;
+      iters = it - 1;
+      rel = best_res / bnorm;
+      done = true;
+      break;
+    }
+    // ---- B
+    const double alpha = rz / pap;
+    const int nxt = (cur != 0 && best != 0) ? 0 : ((cur != 1 && best != 1) ? 1 : 2);
+    for (PartBuf* p : dw.parts) {
+      k_pd_b<<<G, PD_THREADS, 0, s>>>(op, p->r0, p->r1, alpha, p->p[pb].p, p->q.p, p->r.p, p->z.p, Xb(p, cur),
+                                      Xb(p, nxt), p->part.p);
+      k_pd_sum<<<1, 64, 0, s>>>(p->part.p, G, 2, p->scal.p);
+      IBF_LAUNCH_CHECK();
+    }
+    IBF_TRY(pd_reduce(d, dw, 2, hs, s));
+    const double res = sqrt(hs[0]);
+    double rz_new = hs[1];
+    cur = nxt;
+    if (res < best_res) {
+      best_res = res;
+      best = cur;
+    }
+    if (res <= rel_tol * bnorm) {
+      result = cur;
+      iters = it;
+      conv = true;
+      rel = res / bnorm;
+      done = true;
+      break;
+    }
+    IBF_TRY(pd_allgather(d, dw, &PartBuf::z, s));
+    if (it % 250 == 0) {
+      // restart from the true residual r = b - H x (x gathered in full)
+      for (PartBuf* p : dw.parts) {
+        k_pd_copy_rows<<<G, PD_THREADS, 0, s>>>(Xb(p, cur), p->q.p, p->r0, p->r1);
+        IBF_LAUNCH_CHECK();
+      }
+      IBF_TRY(pd_allgather(d, dw, &PartBuf::q, s));
+      for (PartBuf* p : dw.parts) {
+        const Operator o = op_of(p);
+        const PlainGather gx{p->q.p};
+        if (op.contact.n || op.friction.n) k_pd_dots_plain<<<pd_grid(std::max(op.contact.n, op.friction.n)), PD_THREADS, 0, s>>>(o, gx);
+        k_pd_restart<<<G, PD_THREADS, 0, s>>>(o, gx, p->r0, p->r1, rhs, p->r.p, p->z.p, p->part.p);
+        k_pd_sum<<<1, 32, 0, s>>>(p->part.p, G, 1, p->scal.p);
+        IBF_LAUNCH_CHECK();
+      }
+      IBF_TRY(pd_reduce(d, dw, 1, hs, s));
+      rz = hs[0];
+      IBF_TRY(pd_allgather(d, dw, &PartBuf::z, s));
+      first = true;
+      pb ^= 1;
+      continue;
+    }
+    beta = rz_new / rz;
+    rz = rz_new;
+    first = false;
+    pb ^= 1;
+  }
+  if (!done) {
+    result = best;
+    iters = max_iters;
+    rel = best_res / bnorm;
+  }
+  // ---- x_out = X[result], gathered to every partition
+  if (bnorm == 0.0) {
+    IBF_CUDA(cudaMemsetAsync(x_out, 0, 3 * n * sizeof(double), s));
+  } else if (d->local) {
+    for (PartBuf* p : dw.parts) {
+      k_pd_copy_rows<<<G, PD_THREADS, 0, s>>>(Xb(p, result), x_out, p->r0, p->r1);
+      IBF_LAUNCH_CHECK();
+    }
+  } else {
+    PartBuf* p = dw.parts[0];
+    k_pd_copy_rows<<<G, PD_THREADS, 0, s>>>(Xb(p, result), dw.xfull.p, p->r0, p->r1);
+    IBF_LAUNCH_CHECK();
+    IBF_TRY(dist_allgather(d, dw.xfull.p + 3 * p->r0, dw.xfull.p, 3 * (size_t)chunk, s));
+    IBF_CUDA(cudaMemcpyAsync(x_out, dw.xfull.p, 3 * n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  }
+  IBF_TRY(w.info.reserve(4));
+  hs[8] = (double)iters;
+  hs[9] = conv ? 1.0 : 0.0;
+  hs[10] = rel;
+  IBF_CUDA(cudaMemcpyAsync(w.info.p, hs + 8, 3 * sizeof(double), cudaMemcpyHostToDevice, s));
+  IBF_CUDA(cudaStreamSynchronize(s));
+  ++g_launches;
+  return IBF_OK;
+}
+
+}  // namespace ibf

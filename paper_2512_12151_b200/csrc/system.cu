@@ -688,6 +688,13 @@ int system_assemble(ibf_system* s, ibf_contacts* c, const double* x_hat, const d
   return IBF_OK;
 }
 
+int system_pcg(ibf_system* s, const double* rhs, double* x, double rel_tol, int64_t max_iters, cudaStream_t st) {
+  if (s->dist && s->dist->world > 1)
+    return pcg_solve_dist(s->op(), s->pat.rows, s->pat.cols, rhs, x, rel_tol, max_iters, s->work, s->dwork,
+                          s->dist, st);
+  return pcg_solve(s->op(), rhs, x, rel_tol, max_iters, s->work, st);
+}
+
 int system_energy_launch(ibf_system* s, ibf_contacts* c, const double* x_hat, const double* p, int n_r,
                          const double* r_host, const double* r0_dev, const double* x_tilde, double mu,
                          double offset, double h, double* out_dev, cudaStream_t st) {
@@ -1035,7 +1042,7 @@ extern "C" int ibf_system_pcg(ibf_system* s, const double* rhs, double* x_out, d
                               double* info_host, ibf_stream st) {
   ::ibf::StreamScope ibf_scope_((cudaStream_t)st);
   cudaStream_t stream = (cudaStream_t)st;
-  IBF_TRY(pcg_solve(s->op(), rhs, x_out, rel_tol, max_iters, s->work, stream));
+  IBF_TRY(system_pcg(s, rhs, x_out, rel_tol, max_iters, stream));
   return pcg_info(s->work, info_host, stream);
 }
 

@@ -32,6 +32,8 @@ struct ibf_system {
   ibf::DevBuf<double> vec_a, vec_b, vec_c;   // (n,3) scratch
   ibf::HostScratch host;
   ibf::PcgWork work;
+  ibf_dist* dist = nullptr;      // row partition of the PCG (ibf_system_set_dist), or none
+  ibf::DistWork dwork;
   // phase timers (device time): assembly, PCG, line-search energies, inversion cap
   ibf::PhaseTimer t_asm, t_pcg, t_ls, t_cap;
   long long pcg_iters = 0;       // CG iterations since the last stats reset
@@ -65,4 +67,6 @@ int system_energy_launch(ibf_system* s, ibf_contacts* c, const double* x_hat, co
                          double offset, double h, double* out_dev, cudaStream_t st);
 int system_inversion_cap_launch(ibf_system* s, const double* x, const double* p, double* out_dev,
                                 cudaStream_t st);
+// the system's PCG: the persistent single-GPU kernel, or the row partition
+int system_pcg(ibf_system* s, const double* rhs, double* x, double rel_tol, int64_t max_iters, cudaStream_t st);
 }  // namespace ibf

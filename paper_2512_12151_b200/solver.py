@@ -102,6 +102,14 @@ class DeviceSystem:
                    "solve_subproblem")
         return int(res[0]), int(res[1]), bool(res[2]), float(res[3])
 
+    def set_dist(self, partition):
+        """Row-partition this system's PCG solves over `partition`
+        (dist.Partition; None: the single-GPU kernel again).  Keeps a
+        reference so the communicator outlives the system's use of it."""
+        self._dist = partition
+        _lib.check(_lib.lib().ibf_system_set_dist(self.handle, partition.handle if partition is not None else None),
+                   "ibf_system_set_dist")
+
     def set_friction(self, friction):
         """Frozen friction terms for the following assemble / energy / solve
         calls (None removes them); keeps a reference to the handle."""

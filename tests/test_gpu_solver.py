@@ -704,3 +704,68 @@ def test_press_state_step_limit_and_update_on_identical_inputs(pkg):
           f"admitted/pruned GPU {res_g} oracle {res_o}, set size {len(gk)}")
     assert tuple(res_g) == tuple(res_o)
     assert np.array_equal(gk, np.asarray(o.kind)) and np.array_equal(gq, np.asarray(o.quad))
+
+
+@pytest.mark.parametrize("parts", [2, 3])
+def test_partitioned_pcg_matches_unpartitioned(pkg, parts):
+    """The row-partitioned PCG (csrc/pcg.cu pcg_solve_dist)
+    with `parts` local partitions on one GPU — each partition holds its own
+    z / p / r / x vectors, computes H p on its rows only, keeps p on its
+    halo, and receives the other partitions' z rows by device copies; the
+    scalars are summed in partition order — against the single-GPU
+    persistent kernel on the same assembled operator (reduced squishy-ball
+    press, >= 5k matrix-free contact terms), then through one whole AL
+    subproblem.  Only the reduction order differs, so: equal CG counts (+-1)
+    and solutions within 1e-10 relative; equal Newton counts and x_hat
+    within 1e-9 of the step for the subproblem (intact/sparse.py:99-150,
+    intact/solver.py:178-233)."""
+    from paper_2512_12151_b200 import dist
+    from paper_2512_12151_b200.contact import ActiveSet
+    from paper_2512_12151_b200.device import empty, to_host
+    system, params, aset, x, v, _, frames = _squishy_press_state(0.0, 5000)
+    dev = system.device
+    n = system.n_vertices
+    h = params.h
+    x_tilde = x + h * v
+    mu = params.stiffness_constant * dev.stiffness_diagonal_max(x, h)
+    aset.refresh_anchors(x)
+    g = empty((n, 3))
+    dev.assemble(aset, x, x_tilde, mu, params.offset, h, True, g)
+    rhs = -g
+    x1, x2 = empty((n, 3)), empty((n, 3))
+    it1, conv1, rel1 = dev.pcg(rhs, x1, params.cg_tol)
+    part = dist.Partition.local_parts(parts)
+    dev.set_dist(part)
+    try:
+        it2, conv2, rel2 = dev.pcg(rhs, x2, params.cg_tol)
+    finally:
+        dev.set_dist(None)
+    a, b = to_host(x1), to_host(x2)
+    err = np.abs(a - b).max() / np.abs(a).max()
+    print(f"\n[partitioned PCG x{parts}] rows {n}, ranges {part.row_ranges(n)}, constraints {len(aset)}: "
+          f"CG {it2} vs {it1}, rel residual {rel2:.3e} vs {rel1:.3e}, max rel diff {err:.2e}")
+    assert conv1 and conv2 and abs(it1 - it2) <= 1
+    assert err <= 1e-10
+    # one AL subproblem (Newton loop + dual sweep) through the partition
+    st = aset.export_state()
+    runs = []
+    for use in (None, part):
+        a_set = ActiveSet()
+        a_set.import_state(*st)
+        a_set.ensure(n)
+        xh = x.clone()
+        dev.set_dist(use)
+        try:
+            nw, cg, _, _ = dev.solve_subproblem(a_set, x_tilde, x, xh, mu, params.offset, h, params.cg_tol,
+                                                params.decay)
+        finally:
+            dev.set_dist(None)
+        runs.append((nw, cg, to_host(xh), a_set.export_state()))
+    (n1, c1, xa, sa), (n2, c2, xb, sb) = runs
+    step = np.abs(xa - to_host(x)).max()
+    dx = np.abs(xa - xb).max()
+    print(f"[partitioned subproblem x{parts}] Newton {n2} vs {n1}, CG {c2} vs {c1}, max|dx| {dx:.2e} = "
+          f"{dx / step:.2e} of the step")
+    assert n1 == n2 and abs(c1 - c2) <= n1
+    assert dx <= 1e-9 * step
+    assert np.array_equal(sa[3], sb[3])                        # gamma: same dual branches
