@@ -152,7 +152,7 @@ __device__ __forceinline__ int delta(const unsigned long long* k, int n, int i, 
 
 // internal nodes 0..n-2, leaves n-1..2n-2 (leaf n-1+i holds sorted slot i)
 __global__ void k_build(int n, const unsigned long long* __restrict__ k, int* __restrict__ left,
-                        int* __restrict__ right, int* __restrict__ parent) {
+                        int* __restrict__ right, int* __restrict__ parent, int* __restrict__ last) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n - 1; i += gridDim.x * blockDim.x) {
     const int d = (delta(k, n, i, i + 1) - delta(k, n, i, i - 1)) >= 0 ? 1 : -1;
     const int dmin = delta(k, n, i, i - d);
@@ -178,6 +178,7 @@ __global__ void k_build(int n, const unsigned long long* __restrict__ k, int* __
     right[i] = rc;
     parent[lc] = i;
     parent[rc] = i;
+    last[i] = max(i, j);   // the node covers sorted slots [min(i, j), max(i, j)]
   }
 }
 
@@ -192,7 +193,7 @@ struct __align__(16) PackedNode {
   float4 a;  // lo_L.xyz, hi_L.x
   float4 b;  // hi_L.yz, lo_R.xy
   float4 c;  // lo_R.z, hi_R.xyz
-  int4 d;    // left, right, -, -
+  int4 d;    // left, right, last sorted slot under left, last sorted slot under right
 };
 
 // write node `node`'s FP64 box (lo, hi) into its parent's packed record
@@ -248,6 +249,57 @@ __global__ void k_refit(int n, const unsigned long long* __restrict__ k, const d
       __threadfence();
       if (node == 0) break;
       node = parent[node];
+    }
+  }
+}
+
+// Refit of the packed records alone (no FP64 node boxes): a leaf writes its
+// primitive's FP64 box rounded outward into its parent's record; the second
+// arrival at a node takes the union of the two float child boxes in its own
+// record and writes it into its parent's.  A union of outward-rounded boxes
+// contains the exact FP64 union, so the tree stays conservative; the leaves
+// are still tested exactly (k_traverse), so the candidate set is unchanged.
+__device__ __forceinline__ int slot_last(int c, int nl, const int* __restrict__ last) {
+  return c >= nl ? c - nl : last[c];
+}
+__global__ void k_refit_packed(int n, const unsigned long long* __restrict__ k, const double* __restrict__ plo,
+                               const double* __restrict__ phi, const int* __restrict__ left,
+                               const int* __restrict__ right, const int* __restrict__ parent,
+                               const int* __restrict__ last, int* __restrict__ flag, PackedNode* __restrict__ packed) {
+  const int nl = n - 1;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int prim = (int)(k[i] & 0xffffffffull);
+    int node = nl + i;
+    {
+      const double lo[3] = {plo[3 * prim], plo[3 * prim + 1], plo[3 * prim + 2]};
+      const double hi[3] = {phi[3 * prim], phi[3 * prim + 1], phi[3 * prim + 2]};
+      const int par = parent[node];
+      pack_child(packed, par, left[par] == node, lo, hi);
+    }
+    __threadfence();
+    node = parent[node];
+    while (true) {
+      const int old = atomicAdd(flag + node, 1);
+      if (old == 0) break;  // first arrival: the sibling finishes this node
+      const int a = left[node], b = right[node];
+      const float* f = reinterpret_cast<const float*>(packed + node);
+      float lo[3], hi[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        lo[c] = fminf(__ldcg(f + c), __ldcg(f + 6 + c));
+        hi[c] = fmaxf(__ldcg(f + 3 + c), __ldcg(f + 9 + c));
+      }
+      packed[node].d = make_int4(a, b, slot_last(a, nl, last), slot_last(b, nl, last));
+      if (node == 0) break;
+      const int par = parent[node];
+      float* g = reinterpret_cast<float*>(packed + par) + (left[par] == node ? 0 : 6);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        g[c] = lo[c];
+        g[3 + c] = hi[c];
+      }
+      __threadfence();
+      node = par;
     }
   }
 }
@@ -414,6 +466,108 @@ __global__ void __launch_bounds__(128) k_traverse(TraverseArgs a) {
   if (n_cand) atomicAdd(a.counters + 1, n_cand);
 }
 
+// Packed-tree traversal with dynamic query fetching.  Query walks differ in
+// length by an order of magnitude, so a warp that takes 32 queries and runs
+// until the longest ends keeps ~8 of its lanes busy (ncu: 8.2-9.0 threads
+// per executed instruction).  Here a lane whose walk ends takes the next
+// query at once: each warp claims chunks of TRAV_CHUNK queries with one
+// global atomic and deals them to its idle lanes by ballot rank, so the
+// lanes stay busy until the queries run out.
+//
+// SELF (EE, triangle-triangle): the queries are the tree's own leaves in
+// sorted order, query t sitting at sorted slot t.  Each unordered pair is
+// found once, from the leaf with the smaller slot: a child whose last slot is
+// <= t is skipped (PackedNode.d.zw), which halves the walks, and the pair is
+// emitted in the canonical (smaller id, larger id) orientation the per-query
+// `qi < pi` test gave — the same set (intact/ccd.py:131-138).
+constexpr int TRAV_CHUNK = 64;
+template <bool FILTER, bool SELF>
+__global__ void __launch_bounds__(128) k_traverse_dyn(TraverseArgs a) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  const int nl = a.tree.n - 1;
+  const long long nq = a.nq;
+  unsigned long long n_cand = 0;
+  long long pool = 0, pool_end = 0;   // warp-uniform: this warp's unclaimed queries
+  bool exhausted = false;             // warp-uniform
+  long long t = -1;                   // this lane's query (slot), -1: idle
+  int qi = 0;
+  double ql[3], qh[3];
+  float qlf[3], qhf[3];
+  int stack[64];
+  int sp = 0, node = 0;
+  while (true) {
+    unsigned need = __ballot_sync(0xffffffffu, t < 0);
+    while (need && !exhausted) {
+      if (pool == pool_end) {
+        long long b = 0;
+        if (lane == 0) b = (long long)atomicAdd(a.counters + 3, (unsigned long long)TRAV_CHUNK);
+        b = __shfl_sync(0xffffffffu, b, 0);
+        if (b >= nq) {
+          exhausted = true;
+          break;
+        }
+        pool = b;
+        pool_end = b + TRAV_CHUNK < nq ? b + TRAV_CHUNK : nq;
+      }
+      const long long take = min((long long)__popc(need), pool_end - pool);
+      const int rank = __popc(need & lt);
+      if (t < 0 && rank < take) {
+        t = pool + rank;
+        qi = a.qorder ? (int)(a.qorder[t] & 0xffffffffull) : (int)t;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          ql[c] = a.qlo[3 * (int64_t)qi + c];
+          qh[c] = a.qhi[3 * (int64_t)qi + c];
+          qlf[c] = __double2float_rd(ql[c]);
+          qhf[c] = __double2float_ru(qh[c]);
+        }
+        sp = 0;
+        node = 0;
+      }
+      pool += take;
+      need = __ballot_sync(0xffffffffu, t < 0);
+    }
+    if (__ballot_sync(0xffffffffu, t >= 0) == 0) break;
+    if (t < 0) continue;
+    // one node of this lane's walk
+    const PackedNode* P = a.tree.packed + node;
+    const float4 A = __ldg(&P->a), B = __ldg(&P->b), Cq = __ldg(&P->c);
+    const int4 D = __ldg(&P->d);
+    bool hl = overlap_f(qlf, qhf, A.x, A.y, A.z, A.w, B.x, B.y);
+    bool hr = overlap_f(qlf, qhf, B.z, B.w, Cq.x, Cq.y, Cq.z, Cq.w);
+    if (SELF) {
+      hl = hl && D.z > t;
+      hr = hr && D.w > t;
+    }
+    if (hl && D.x >= nl) {
+      const int pi = (int)(a.tree.keys[D.x - nl] & 0xffffffffull);
+      if (overlap(ql, qh, a.tree.plo + 3 * pi, a.tree.phi + 3 * pi))
+        traverse_leaf<FILTER>(a, SELF ? min(qi, pi) : qi, SELF ? max(qi, pi) : pi, n_cand);
+      hl = false;
+    }
+    if (hr && D.y >= nl) {
+      const int pi = (int)(a.tree.keys[D.y - nl] & 0xffffffffull);
+      if (overlap(ql, qh, a.tree.plo + 3 * pi, a.tree.phi + 3 * pi))
+        traverse_leaf<FILTER>(a, SELF ? min(qi, pi) : qi, SELF ? max(qi, pi) : pi, n_cand);
+      hr = false;
+    }
+    if (hl && hr) {
+      stack[sp++] = D.y;
+      node = D.x;
+    } else if (hl) {
+      node = D.x;
+    } else if (hr) {
+      node = D.y;
+    } else if (sp > 0) {
+      node = stack[--sp];
+    } else {
+      t = -1;   // walk done
+    }
+  }
+  if (n_cand) atomicAdd(a.counters + 1, n_cand);
+}
+
 // Second stage of the filtered broad phase: the traversal emits every
 // candidate (no FP64 work inside the tree walk, so it keeps ~40 % of the
 // registers and its warps stay converged between leaves), then one thread
@@ -515,6 +669,10 @@ static int grid_for(int64_t n, int threads = 256) {
 #ifndef IBF_CCD_VF_ORDER
 #define IBF_CCD_VF_ORDER 0
 #endif
+// packed traversal with dynamic query fetching (1) or one query per thread (0)
+#ifndef IBF_CCD_DYNAMIC
+#define IBF_CCD_DYNAMIC 1
+#endif
 // filtered broad phase as traversal + a separate prefilter pass (1) or with
 // the prefilter inside the traversal (0)
 #ifndef IBF_CCD_SPLIT
@@ -523,7 +681,7 @@ static int grid_for(int64_t n, int threads = 256) {
 static int build_tree(ibf_ccd* c, int64_t n, cudaStream_t s, Tree& t, ibf_ccd::TreeCache* cache = nullptr) {
   const int64_t nn = std::max<int64_t>(2 * n - 1, 1);
   unsigned long long* keys_sorted = c->keys_sorted.p;
-  int *left, *right, *parent, *flag;
+  int *left, *right, *parent, *flag, *last;
   double *lo, *hi;
   float4* packed4;
   bool refit_only = false;
@@ -533,12 +691,16 @@ static int build_tree(ibf_ccd* c, int64_t n, cudaStream_t s, Tree& t, ibf_ccd::T
     IBF_TRY(cache->right.reserve(nn));
     IBF_TRY(cache->parent.reserve(nn));
     IBF_TRY(cache->flag.reserve(nn));
-    IBF_TRY(cache->lo.reserve(3 * nn));
-    IBF_TRY(cache->hi.reserve(3 * nn));
+    IBF_TRY(cache->last.reserve(nn));
+    if (!IBF_CCD_PACKED) {
+      IBF_TRY(cache->lo.reserve(3 * nn));
+      IBF_TRY(cache->hi.reserve(3 * nn));
+    }
     IBF_TRY(cache->packed.reserve(4 * nn));
     refit_only = cache->n == n && cache->uses < IBF_CCD_REBUILD;
     keys_sorted = cache->keys_sorted.p;
     left = cache->left.p, right = cache->right.p, parent = cache->parent.p, flag = cache->flag.p;
+    last = cache->last.p;
     lo = cache->lo.p, hi = cache->hi.p;
     packed4 = cache->packed.p;
   } else {
@@ -547,11 +709,13 @@ static int build_tree(ibf_ccd* c, int64_t n, cudaStream_t s, Tree& t, ibf_ccd::T
     IBF_TRY(c->node_right.reserve(nn));
     IBF_TRY(c->node_parent.reserve(nn));
     IBF_TRY(c->node_flag.reserve(nn));
+    IBF_TRY(c->node_last.reserve(nn));
     IBF_TRY(c->node_lo.reserve(3 * nn));
     IBF_TRY(c->node_hi.reserve(3 * nn));
     IBF_TRY(c->node_packed.reserve(4 * nn));
     keys_sorted = c->keys_sorted.p;
     left = c->node_left.p, right = c->node_right.p, parent = c->node_parent.p, flag = c->node_flag.p;
+    last = c->node_last.p;
     lo = c->node_lo.p, hi = c->node_hi.p;
     packed4 = c->node_packed.p;
   }
@@ -570,7 +734,7 @@ static int build_tree(ibf_ccd* c, int64_t n, cudaStream_t s, Tree& t, ibf_ccd::T
     size_t have = c->cub_tmp.cap;
     IBF_CUDA(cub::DeviceRadixSort::SortKeys(c->cub_tmp.p, have, c->keys.p, keys_sorted, (int)n, 0, 64, s));
     if (n > 1) {
-      k_build<<<grid_for(n - 1), 256, 0, s>>>((int)n, keys_sorted, left, right, parent);
+      k_build<<<grid_for(n - 1), 256, 0, s>>>((int)n, keys_sorted, left, right, parent, last);
       IBF_LAUNCH_CHECK();
     }
     if (cache) {
@@ -580,8 +744,18 @@ static int build_tree(ibf_ccd* c, int64_t n, cudaStream_t s, Tree& t, ibf_ccd::T
   }
   if (cache) ++cache->uses;
   IBF_CUDA(cudaMemsetAsync(flag, 0, nn * sizeof(int), s));
-  k_refit<<<grid_for(n), 256, 0, s>>>((int)n, keys_sorted, c->box_lo.p, c->box_hi.p, left, right, parent, flag, lo,
-                                       hi, packed);
+  if (packed && n > 1) {
+    k_refit_packed<<<grid_for(n), 256, 0, s>>>((int)n, keys_sorted, c->box_lo.p, c->box_hi.p, left, right, parent,
+                                                last, flag, packed);
+  } else {
+    if (cache && IBF_CCD_PACKED) {
+      IBF_TRY(cache->lo.reserve(3 * nn));
+      IBF_TRY(cache->hi.reserve(3 * nn));
+      lo = cache->lo.p, hi = cache->hi.p;
+    }
+    k_refit<<<grid_for(n), 256, 0, s>>>((int)n, keys_sorted, c->box_lo.p, c->box_hi.p, left, right, parent, flag,
+                                         lo, hi, nullptr);
+  }
   IBF_LAUNCH_CHECK();
   t.packed = n > 1 ? packed : nullptr;
   t.plo = c->box_lo.p;
@@ -662,6 +836,7 @@ static int broad_pass(ibf_ccd* c, int kind, const double* x0, const double* x1, 
   TraverseArgs a;
   for (int attempt = 0; attempt < 3; ++attempt) {
     IBF_CUDA(cudaMemsetAsync(c->counters.p, 0, 2 * sizeof(unsigned long long), s));
+    IBF_CUDA(cudaMemsetAsync(c->counters.p + 3, 0, sizeof(unsigned long long), s));
     a.tree = tree;
     a.qorder = qorder;
     a.nq = nq;
@@ -683,9 +858,23 @@ static int broad_pass(ibf_ccd* c, int kind, const double* x0, const double* x1, 
       // read once) + 16 B per candidate pair out (booked after the count)
       KernelClock kc(KC_TRAVERSE, s, 48.0 * (nq + tree.n), 0.0, 0.0);
       const bool packed = tree.packed != nullptr;
-      auto kern = a.filter ? (packed ? k_traverse<true, true> : k_traverse<true, false>)
-                           : (packed ? k_traverse<false, true> : k_traverse<false, false>);
-      kern<<<grid_for(nq, 128), 128, 0, s>>>(a);
+      if (packed && IBF_CCD_DYNAMIC) {
+        // self-queries walk the tree's own leaves in sorted order
+        const bool self = kind != 0 && a.qorder == tree.keys;
+        auto kern = a.filter ? (self ? k_traverse_dyn<true, true> : k_traverse_dyn<true, false>)
+                             : (self ? k_traverse_dyn<false, true> : k_traverse_dyn<false, false>);
+        static int blocks_per_sm = 0;
+        if (!blocks_per_sm) {
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_traverse_dyn<false, true>, 128, 0);
+          blocks_per_sm = std::max(blocks_per_sm, 1);
+        }
+        const int64_t want = div_up(nq, 128);
+        kern<<<(int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)blocks_per_sm * sm_count())), 128, 0, s>>>(a);
+      } else {
+        auto kern = a.filter ? (packed ? k_traverse<true, true> : k_traverse<true, false>)
+                             : (packed ? k_traverse<false, true> : k_traverse<false, false>);
+        kern<<<grid_for(nq, 128), 128, 0, s>>>(a);
+      }
       IBF_LAUNCH_CHECK();
       IBF_CUDA(cudaMemcpyAsync(h, c->counters.p, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
       IBF_CUDA(cudaStreamSynchronize(s));

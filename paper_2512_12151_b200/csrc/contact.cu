@@ -470,6 +470,7 @@ int contact_build_incidence(ibf_contacts* c, int64_t n_verts, cudaStream_t s) {
   }
   IBF_TRY(exclusive_scan(c, c->v_count.p, c->vc_ptr.p, n_verts + 1, s));
   c->vc_nverts = n_verts;
+  c->trec_nverts = -1;
   return IBF_OK;
 }
 
@@ -482,6 +483,50 @@ int contact_prepare(ibf_contacts* c, const double* x_hat, double mu, double offs
   return IBF_OK;
 }
 
+// Per-row term records for the PCG (k_pcg's warp-cooperative term pass):
+// the incidences of every unmasked row, in vc order, as 32-byte records
+// {g_c[slot] (3 doubles), c}, with masked (Dirichlet) rows given none — a
+// pinned plate vertex can sit in 10^4 constraints, which a warp sharing its
+// incidence range would otherwise walk.
+__global__ void k_term_counts(int64_t n, const int* __restrict__ vc_ptr, const uint8_t* __restrict__ mask,
+                              int* __restrict__ cnt) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    cnt[i] = (mask && mask[i]) ? 0 : vc_ptr[i + 1] - vc_ptr[i];
+}
+__global__ void k_term_records(int64_t n, const int* __restrict__ vc_ptr, const int* __restrict__ vc_src,
+                               const int* __restrict__ ip_ptr, const double* __restrict__ grad,
+                               double4* __restrict__ rec) {
+  // one warp per row: its lanes copy the row's records
+  const int lane = threadIdx.x & 31;
+  for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < n;
+       i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int o = ip_ptr[i], m = ip_ptr[i + 1] - o, e0 = vc_ptr[i];
+    for (int k = lane; k < m; k += 32) {
+      const int src = vc_src[e0 + k];
+      const double* g = grad + 12 * (size_t)(src >> 2) + 3 * (src & 3);
+      // meta: constraint (bits 0-31), slot (32-33), the row's lane in its 32-row slice (34-38)
+      const long long meta = (long long)(src >> 2) | ((long long)(src & 3) << 32) | ((long long)(i & 31) << 34);
+      rec[o + k] = make_double4(g[0], g[1], g[2], __longlong_as_double(meta));
+    }
+  }
+}
+
+int contact_pack_terms(ibf_contacts* c, int64_t n_verts, const uint8_t* mask, cudaStream_t s) {
+  if (!c->n) return IBF_OK;
+  IBF_TRY(c->ip_ptr.reserve(n_verts + 1));
+  IBF_TRY(c->v_count.reserve(n_verts + 1));
+  k_term_counts<<<grid_for(n_verts), 256, 0, s>>>(n_verts, c->vc_ptr.p, mask, c->v_count.p);
+  IBF_LAUNCH_CHECK();
+  IBF_CUDA(cudaMemsetAsync(c->v_count.p + n_verts, 0, sizeof(int), s));
+  IBF_TRY(exclusive_scan(c, c->v_count.p, c->ip_ptr.p, n_verts + 1, s));
+  IBF_TRY(c->trec.reserve(std::max<int64_t>(4 * c->n, 1)));
+  k_term_records<<<(int)std::max<int64_t>(1, std::min<int64_t>(div_up(32 * n_verts, 256), 148LL * 16)), 256, 0, s>>>(
+      n_verts, c->vc_ptr.p, c->vc_src.p, c->ip_ptr.p, c->anchor_grad.p, c->trec.p);
+  IBF_LAUNCH_CHECK();
+  c->trec_nverts = n_verts;
+  return IBF_OK;
+}
+
 ContactView contact_view(ibf_contacts* c) {
   ContactView v;
   v.n = (int)c->n;
@@ -491,6 +536,10 @@ ContactView contact_view(ibf_contacts* c) {
   v.vc_ptr = c->vc_ptr.p;
   v.vc_src = c->vc_src.p;
   v.t = c->tdot.p;
+  if (c->trec_nverts >= 0) {
+    v.ip_ptr = c->ip_ptr.p;
+    v.rec = c->trec.p;
+  }
   return v;
 }
 

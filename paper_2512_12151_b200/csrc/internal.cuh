@@ -15,6 +15,12 @@ struct RegionDev {
   double lam;
 };
 
+// k_pcg applies the contact terms of a warp's 32 rows cooperatively (lanes
+// over the rows' concatenated term records) instead of one row per lane
+#ifndef IBF_PCG_WARP_TERMS
+#define IBF_PCG_WARP_TERMS 1
+#endif
+
 // Matrix-free contact operator: H_c = sum_c coef_c g_c g_c^T over the 12-dof
 // clique of constraint c, with DBC masking applied on both sides.
 struct ContactView {
@@ -25,6 +31,9 @@ struct ContactView {
   const int* vc_ptr = nullptr;        // (N+1) vertex -> incidences
   const int* vc_src = nullptr;        // c*4 + slot, ordered by c
   double* t = nullptr;                // (C) workspace coef_c * g_c . p
+  // per-row term records of the unmasked rows (contact_pack_terms), or null
+  const int* ip_ptr = nullptr;        // (N+1)
+  const double4* rec = nullptr;       // {g_c[slot], c}, in vc order
 };
 
 // Symmetric 3x3-block matrix (diagonal + strict upper, the reference's
@@ -154,6 +163,7 @@ struct PcgWork {
   DevBuf<int> counter;               // dynamic phase-A chunk counters
   DevBuf<double> part_chunk;         // dynamic phase-A per-chunk partials
   DevBuf<unsigned> ready;            // term-dot ready counter
+  DevBuf<double> zdot, pdot;         // zdot mode: per-record z and previous-direction products
   int grid = 0;
   int n_alloc = -1;
 };
@@ -221,6 +231,9 @@ struct ibf_contacts {
   ibf::DevBuf<double> coef_h, coef_g, cval;   // mu*gamma, gradient coefficient, c
   ibf::DevBuf<double> tdot;                   // SpMV workspace (C)
   ibf::DevBuf<int> vc_ptr, vc_src;
+  ibf::DevBuf<int> ip_ptr;                    // PCG term records (contact_pack_terms)
+  ibf::DevBuf<double4> trec;
+  int64_t trec_nverts = -1;
   ibf::DevBuf<int> sort_keys, sort_vals, sort_keys2, sort_vals2;
   ibf::DevBuf<unsigned char> cub_tmp;
   int64_t vc_nverts = -1;
@@ -259,14 +272,14 @@ struct ibf_ccd {
   ibf::DevBuf<double> box_lo, box_hi, qlo, qhi;        // primitive boxes / query boxes (n,3)
   ibf::DevBuf<unsigned long long> keys, keys_sorted;
   ibf::DevBuf<int> order;                               // sorted primitive order
-  ibf::DevBuf<int> node_left, node_right, node_parent, node_flag;
+  ibf::DevBuf<int> node_left, node_right, node_parent, node_flag, node_last;
   ibf::DevBuf<double> node_lo, node_hi;
   ibf::DevBuf<float4> node_packed;                      // 4 per internal node (ccd.cu PackedNode)
   // VF (triangle) and EE (edge) trees kept between calls: later calls refit
   // the cached topology to the new boxes; it is rebuilt every few calls
   struct TreeCache {
     ibf::DevBuf<unsigned long long> keys_sorted;
-    ibf::DevBuf<int> left, right, parent, flag;
+    ibf::DevBuf<int> left, right, parent, flag, last;
     ibf::DevBuf<double> lo, hi;
     ibf::DevBuf<float4> packed;
     int64_t n = -1;
@@ -277,7 +290,8 @@ struct ibf_ccd {
   ibf::DevBuf<unsigned long long> pairs, pairs2, pairs_sorted;
   ibf::DevBuf<unsigned long long> vf_order;             // VF query order (Morton keys | query)
   int64_t vf_order_n = -1;
-  ibf::DevBuf<unsigned long long> counters;             // [0] emitted, [1] all candidates
+  ibf::DevBuf<unsigned long long> counters;             // [0] emitted, [1] all candidates, [2] min-distance
+                                                        // pair, [3] traversal query fetch
   ibf::DevBuf<double> pair_toi;
   int64_t n_vf = 0, n_ee = 0;                           // candidates of the last call
   // blocking set

@@ -82,6 +82,10 @@ constexpr int PCG_SMEM_BYTES = IBF_PCG_SMEM_KB * 1024;
 #ifndef IBF_PCG_LANES_MAX_N
 #define IBF_PCG_LANES_MAX_N 16384
 #endif
+// contact dots by linearity from per-row z products (no dot phase; see warp_zdot)
+#ifndef IBF_PCG_ZDOT
+#define IBF_PCG_ZDOT 1
+#endif
 // matrix-free term dots behind a ready counter instead of a grid barrier
 #ifndef IBF_PCG_READY
 #define IBF_PCG_READY 1
@@ -194,9 +198,10 @@ __device__ __forceinline__ void friction_dot(const Operator& op, const Gather& g
 
 // the matrix-free terms' per-term dots (contact and friction) over this thread's share
 template <class Gather>
-__device__ __forceinline__ void term_dots(const Operator& op, const Gather& gp) {
+__device__ __forceinline__ void term_dots(const Operator& op, const Gather& gp, bool contacts = true) {
   const int S = gridDim.x * blockDim.x;
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < op.contact.n; c += S) contact_dot(op, gp, c);
+  if (contacts)
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < op.contact.n; c += S) contact_dot(op, gp, c);
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < op.friction.n; k += S) friction_dot(op, gp, k);
 }
 
@@ -248,7 +253,7 @@ __device__ __forceinline__ void acc_lower(const double b[9], double x0, double x
 // row's blocks in storage order.  Two slots are in flight per iteration
 // (18 matrix entries, 2 indices, 6 p entries): the product is latency-bound
 // otherwise.
-template <class Gather, class Terms = StoredTerms>
+template <class Gather, class Terms = StoredTerms, bool CONTACT = true>
 __device__ __forceinline__ void row_product(const Operator& op, const Gather& gp, int pos, int i, double y[3],
                                             const Terms& terms = Terms()) {
   // storage by position (row_at maps positions to rows: internal.cuh); row i
@@ -330,7 +335,7 @@ __device__ __forceinline__ void row_product(const Operator& op, const Gather& gp
       acc_lower(b, x0, x1, x2, a0, a1, a2);
     }
   }
-  if (op.contact.n && !(op.mask && op.mask[i])) {
+  if (CONTACT && op.contact.n && !(op.mask && op.mask[i])) {
     const ContactView& cv = op.contact;
     const int e0 = cv.vc_ptr[i], e1 = cv.vc_ptr[i + 1];
     if (e0 < e1) terms.ready();
@@ -360,6 +365,117 @@ __device__ __forceinline__ void row_product(const Operator& op, const Gather& gp
   y[0] = a0;
   y[1] = a1;
   y[2] = a2;
+}
+
+// Contact terms of the warp's 32 consecutive rows r0 .. r0+31 (all lanes
+// call this, converged): the rows' term records are one contiguous range of
+// ContactView::rec, so the lanes walk it together, TERM_CHUNK records at a
+// time, each forming t_c g_c[slot] into shared memory; then each row adds
+// its own records' products in record order.  Rows take 0-50 terms (p50 3,
+// p99 17 on the squishy press), so one row per lane kept ~1/6 of the lanes
+// busy through the term loop (the slowest row of a warp sets its length).
+constexpr int TERM_CHUNK = 32;
+template <class Terms>
+__device__ __forceinline__ void warp_terms(const ContactView& cv, const Terms& terms, int r0, int n, double* buf,
+                                           double& a0, double& a1, double& a2) {
+  const int lane = threadIdx.x & 31;
+  const int rl = min(r0 + 32, n);
+  const int E0 = __ldg(cv.ip_ptr + r0), E1 = __ldg(cv.ip_ptr + rl);
+  if (E0 == E1) return;
+  terms.ready();
+  const int i = r0 + lane;
+  const int s0 = i < rl ? __ldg(cv.ip_ptr + i) : 0, s1 = i < rl ? __ldg(cv.ip_ptr + i + 1) : 0;
+  for (int base = E0; base < E1; base += TERM_CHUNK) {
+    const int m = min(TERM_CHUNK, E1 - base);
+    for (int k = lane; k < m; k += 32) {
+      const double2* rp = reinterpret_cast<const double2*>(cv.rec + base + k);
+      const double2 ra = __ldg(rp), rb = __ldg(rp + 1);
+      const double4 r = make_double4(ra.x, ra.y, rb.x, rb.y);
+      const double t = terms.contact(cv, (int)(__double_as_longlong(r.w) & 0xffffffffll));
+      buf[k] = t * r.x;
+      buf[TERM_CHUNK + k] = t * r.y;
+      buf[2 * TERM_CHUNK + k] = t * r.z;
+    }
+    __syncwarp();
+    const int lo = max(s0, base), hi = min(s1, base + m);
+    for (int e = lo - base; e < hi - base; ++e) {
+      a0 += buf[e];
+      a1 += buf[TERM_CHUNK + e];
+      a2 += buf[2 * TERM_CHUNK + e];
+    }
+    __syncwarp();
+  }
+}
+
+// Contact dots without a dot phase (k_pcg "zdot" mode).  By linearity
+// g_c . p_k = sum_slots g_c[slot] . z_k[v_slot] + beta_k (g_c . p_{k-1}):
+// where a row's z is formed (init, phase B, restart) its warp writes
+// g_c[slot] . z_i into zdot[4c + slot] for each of the row's records, and in
+// phase A each record sums its constraint's 4 zdot entries in slot order and
+// adds beta times its own copy of the previous dot (pdot[4c + slot]; the
+// copies of one constraint are formed from identical inputs, so they stay
+// bit-identical).  Masked slots have no records and keep zdot = 0, as the
+// masked gathers of contact_dot contribute nothing.  No CTA waits for
+// another's term dots inside phase A, and the z / p gathers of the dot
+// phase (quad -> vertex -> value chains) are gone.
+__device__ __forceinline__ double4 ld_rec(const double4* p) {
+  const double2* rp = reinterpret_cast<const double2*>(p);
+  const double2 ra = __ldg(rp), rb = __ldg(rp + 1);
+  return make_double4(ra.x, ra.y, rb.x, rb.y);
+}
+__device__ __forceinline__ void warp_zdot(const ContactView& cv, int r0, int n, const double z[3], double* zs,
+                                          double* zdot) {
+  const int lane = threadIdx.x & 31;
+  const int rl = min(r0 + 32, n);
+  const int E0 = __ldg(cv.ip_ptr + r0), E1 = __ldg(cv.ip_ptr + rl);
+  if (E0 == E1) return;
+  zs[lane] = z[0];
+  zs[32 + lane] = z[1];
+  zs[64 + lane] = z[2];
+  __syncwarp();
+  for (int e = E0 + lane; e < E1; e += 32) {
+    const double4 r = ld_rec(cv.rec + e);
+    const long long m = __double_as_longlong(r.w);
+    const int c = (int)(m & 0xffffffffll), slot = (int)((m >> 32) & 3), ol = (int)((m >> 34) & 31);
+    zdot[4 * (size_t)c + slot] = r.x * zs[ol] + r.y * zs[32 + ol] + r.z * zs[64 + ol];
+  }
+  __syncwarp();
+}
+__device__ __forceinline__ void warp_terms_z(const ContactView& cv, int r0, int n, double* buf, bool first,
+                                             double beta, const double* zdot, double* pdot, double& a0, double& a1,
+                                             double& a2) {
+  const int lane = threadIdx.x & 31;
+  const int rl = min(r0 + 32, n);
+  const int E0 = __ldg(cv.ip_ptr + r0), E1 = __ldg(cv.ip_ptr + rl);
+  if (E0 == E1) return;
+  const int i = r0 + lane;
+  const int s0 = i < rl ? __ldg(cv.ip_ptr + i) : 0, s1 = i < rl ? __ldg(cv.ip_ptr + i + 1) : 0;
+  for (int base = E0; base < E1; base += TERM_CHUNK) {
+    const int m = min(TERM_CHUNK, E1 - base);
+    for (int k = lane; k < m; k += 32) {
+      const double4 r = ld_rec(cv.rec + base + k);
+      const long long mt = __double_as_longlong(r.w);
+      const int c = (int)(mt & 0xffffffffll), slot = (int)((mt >> 32) & 3);
+      const double2* Zd = reinterpret_cast<const double2*>(zdot + 4 * (size_t)c);
+      const double2 z01 = Zd[0], z23 = Zd[1];
+      const double zsum = ((z01.x + z01.y) + z23.x) + z23.y;
+      double* pd = pdot + 4 * (size_t)c + slot;
+      const double dot = first ? zsum : __fma_rn(beta, *pd, zsum);
+      *pd = dot;
+      const double t = __ldg(cv.coef + c) * dot;
+      buf[k] = t * r.x;
+      buf[TERM_CHUNK + k] = t * r.y;
+      buf[2 * TERM_CHUNK + k] = t * r.z;
+    }
+    __syncwarp();
+    const int lo = max(s0, base), hi = min(s1, base + m);
+    for (int e = lo - base; e < hi - base; ++e) {
+      a0 += buf[e];
+      a1 += buf[TERM_CHUNK + e];
+      a2 += buf[2 * TERM_CHUNK + e];
+    }
+    __syncwarp();
+  }
 }
 
 // Row i's product split over L lanes of one warp (lane sub takes slots,
@@ -633,6 +749,9 @@ struct PcgArgs {
   unsigned* bar;        // split-barrier arrival counter (phase B), or null: grid barrier
   int lanes;            // lanes per row in phase A (1: one thread per row)
   unsigned n_home;      // CTAs that compute term dots (each adds 1 per iteration)
+  double* zdot;         // zdot mode (contacts without a dot phase): (C,4) g_c[slot] . z
+  double* pdot;         // (C,4) each record's copy of g_c . p_{k-1}
+  int zmode;
 };
 
 // all CTAs compute the same fixed-order total of part[slot*G .. slot*G+G)
@@ -678,6 +797,10 @@ __global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
   extern __shared__ double dyn[];
   __shared__ double red[32];
   __shared__ double bc[1];
+  __shared__ double term_buf[(PCG_THREADS / 32) * 3 * TERM_CHUNK];
+  double* wbuf = term_buf + (threadIdx.x >> 5) * 3 * TERM_CHUNK;
+  const bool zmode = a.zmode != 0;
+  double dummy[3] = {0.0, 0.0, 0.0};
   const Operator& op = a.op;
   const int n = op.n;
   const int S = gridDim.x * blockDim.x;          // rows per sweep
@@ -707,11 +830,21 @@ __global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
   double acc_b = 0.0, acc_rz = 0.0;
   for (int k = 0; k < R; ++k) {
     const int pos = row_of(k);
-    if (pos >= n) break;
+    if (zmode) {
+      if (__all_sync(0xffffffffu, pos >= n)) break;
+      if (pos >= n) {
+        const double z0[3] = {0.0, 0.0, 0.0};
+        warp_zdot(op.contact, pos & ~31, n, z0, wbuf, a.zdot);
+        continue;
+      }
+    } else if (pos >= n) {
+      break;
+    }
     const int i = row_at(op, pos);
     const double r0 = a.rhs[3 * (size_t)i], r1 = a.rhs[3 * (size_t)i + 1], r2 = a.rhs[3 * (size_t)i + 2];
     double zv[3];
     apply_pinv6(op.pinv + PINV_STRIDE * (size_t)i, r0, r1, r2, zv);
+    if (zmode) warp_zdot(op.contact, pos & ~31, n, zv, wbuf, a.zdot);
     double* zi = a.z + 3 * (size_t)i;
     double* xi = Xb(0) + 3 * (size_t)i;
     r_ref(k, i, 0) = r0;
@@ -757,10 +890,10 @@ __global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
         else
           row_product(op, gd, pos, i, v);
       };
-      if (op.contact.n || op.friction.n) {
+      if ((op.contact.n && !zmode) || op.friction.n) {
         if (counted) {
           if (blockIdx.x < a.n_home) {
-            term_dots(op, gd);
+            term_dots(op, gd, !zmode);
             __syncthreads();
             if (threadIdx.x == 0) {
               __threadfence();
@@ -768,7 +901,7 @@ __global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
             }
           }
         } else {
-          term_dots(op, gd);
+          term_dots(op, gd, !zmode);
           grid.sync();
         }
       }
@@ -843,12 +976,46 @@ __global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
             }
           }
         }
+        // warp-cooperative contact terms: positions are rows (no SELL
+        // window permutation) and the records exist for this operator
+        const bool wterms = IBF_PCG_WARP_TERMS && op.contact.n && op.contact.rec && !op.perm;
         for (int k = 0; k < R && a.lanes == 1; ++k) {
           const int pos = row_of(k);
-          if (pos >= n) break;
+          if (wterms) {
+            // the warp's 32 positions are one aligned slice: exit together
+            if (__all_sync(0xffffffffu, pos >= n)) break;
+          } else if (pos >= n) {
+            break;
+          }
+          if (pos >= n) {
+            if (zmode)
+              warp_terms_z(op.contact, pos & ~31, n, wbuf, first, beta, a.zdot, a.pdot, dummy[0], dummy[1],
+                           dummy[2]);
+            else if (counted)
+              warp_terms(op.contact, sterms, pos & ~31, n, wbuf, dummy[0], dummy[1], dummy[2]);
+            else
+              warp_terms(op.contact, StoredTerms(), pos & ~31, n, wbuf, dummy[0], dummy[1], dummy[2]);
+            continue;
+          }
           const int i = row_at(op, pos);
           double v[3], pv[3];
-          product(pos, i, v);
+          if (zmode) {
+            if (counted)
+              row_product<DirGather, CountedTerms, false>(op, gd, pos, i, v, sterms);
+            else
+              row_product<DirGather, StoredTerms, false>(op, gd, pos, i, v);
+            warp_terms_z(op.contact, pos & ~31, n, wbuf, first, beta, a.zdot, a.pdot, v[0], v[1], v[2]);
+          } else if (wterms) {
+            if (counted) {
+              row_product<DirGather, CountedTerms, false>(op, gd, pos, i, v, sterms);
+              warp_terms(op.contact, sterms, pos & ~31, n, wbuf, v[0], v[1], v[2]);
+            } else {
+              row_product<DirGather, StoredTerms, false>(op, gd, pos, i, v);
+              warp_terms(op.contact, StoredTerms(), pos & ~31, n, wbuf, v[0], v[1], v[2]);
+            }
+          } else {
+            product(pos, i, v);
+          }
           const double* Z = a.z + 3 * (size_t)i;
           if (first) {
             pv[0] = Z[0]; pv[1] = Z[1]; pv[2] = Z[2];
@@ -896,7 +1063,16 @@ __global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
       const bool split = a.bar != nullptr && !qp_smem;
       for (int k = 0; k < R; ++k) {
         const int pos = row_of(k);
-        if (pos >= n) break;
+        if (zmode) {
+          if (__all_sync(0xffffffffu, pos >= n)) break;
+          if (pos >= n) {
+            const double z0[3] = {0.0, 0.0, 0.0};
+            warp_zdot(op.contact, pos & ~31, n, z0, wbuf, a.zdot);
+            continue;
+          }
+        } else if (pos >= n) {
+          break;
+        }
         const int i = row_at(op, pos);
         double qv[3], pv[3], rv[3], zv[3];
         if (qp_smem) {
@@ -920,6 +1096,7 @@ __global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
         apply_pinv6(op.pinv + PINV_STRIDE * (size_t)i, rv[0], rv[1], rv[2], zv);
         double* zi = a.z + 3 * (size_t)i;
         zi[0] = zv[0]; zi[1] = zv[1]; zi[2] = zv[2];
+        if (zmode) warp_zdot(op.contact, pos & ~31, n, zv, wbuf, a.zdot);
         acc_rz += rv[0] * zv[0] + rv[1] * zv[1] + rv[2] * zv[2];
       }
       PCG_PT(3)
@@ -975,7 +1152,16 @@ __global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
         acc_rz = 0.0;
         for (int k = 0; k < R; ++k) {
           const int pos = row_of(k);
-          if (pos >= n) break;
+          if (zmode) {
+            if (__all_sync(0xffffffffu, pos >= n)) break;
+            if (pos >= n) {
+              const double z0[3] = {0.0, 0.0, 0.0};
+              warp_zdot(op.contact, pos & ~31, n, z0, wbuf, a.zdot);
+              continue;
+            }
+          } else if (pos >= n) {
+            break;
+          }
           const int i = row_at(op, pos);
           double v[3], zv[3];
           row_product(op, gx, pos, i, v);
@@ -988,6 +1174,7 @@ __global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
           r_ref(k, i, 1) = r1;
           r_ref(k, i, 2) = r2;
           zi[0] = zv[0]; zi[1] = zv[1]; zi[2] = zv[2];
+          if (zmode) warp_zdot(op.contact, pos & ~31, n, zv, wbuf, a.zdot);
           acc_rz += r0 * zv[0] + r1 * zv[1] + r2 * zv[2];
         }
         put_partials(a.part, 1, acc_rz, red);
@@ -1044,6 +1231,14 @@ struct PcgShape {
 // sweeps per thread on systems the oracle solves in seconds.
 static std::atomic<long long> g_lanes_max_n{IBF_PCG_LANES_MAX_N};
 static std::atomic<int> g_max_ctas{0};
+// zdot mode on (IBF_PCG_ZDOT builds) unless the environment sets IBF_PCG_ZDOT=0 (A/B runs)
+static int zdot_enabled() {
+  static const int on = [] {
+    const char* e = getenv("IBF_PCG_ZDOT");
+    return (e && e[0] == '0') ? 0 : 1;
+  }();
+  return on;
+}
 // shape of the last PCG launch in the process (ibf_pcg_last_shape)
 static std::atomic<long long> g_last_shape[6];
 
@@ -1175,9 +1370,24 @@ int pcg_solve(const Operator& op, const double* rhs, double* x_out, double rel_t
   IBF_CUDA(cudaMemsetAsync(w.ready.p, 0, 2 * sizeof(unsigned), s));
   a.bar = IBF_PCG_SPLIT_BAR ? w.ready.p + 1 : nullptr;
   a.lanes = lanes;
-  if (IBF_PCG_READY && (op.contact.n || op.friction.n)) {
+  // contacts without a dot phase: one thread per row, rows = positions, term records built
+  a.zmode = (IBF_PCG_ZDOT && IBF_PCG_WARP_TERMS && lanes == 1 && !a.n_chunks && op.contact.n && op.contact.rec &&
+             !op.perm && zdot_enabled())
+                ? 1
+                : 0;
+  a.zdot = a.pdot = nullptr;
+  if (a.zmode) {
+    const size_t nc4 = 4 * (size_t)op.contact.n;
+    IBF_TRY(w.zdot.reserve(nc4));
+    IBF_TRY(w.pdot.reserve(nc4));
+    IBF_CUDA(cudaMemsetAsync(w.zdot.p, 0, nc4 * sizeof(double), s));
+    a.zdot = w.zdot.p;
+    a.pdot = w.pdot.p;
+  }
+  const int64_t n_dot_terms = std::max<int64_t>(a.zmode ? 0 : op.contact.n, op.friction.n);
+  if (IBF_PCG_READY && n_dot_terms) {
     a.ready = w.ready.p;
-    a.n_home = (unsigned)std::min<int64_t>(sh.grid, div_up(std::max(op.contact.n, op.friction.n), sh.threads));
+    a.n_home = (unsigned)std::min<int64_t>(sh.grid, div_up(n_dot_terms, sh.threads));
   }
   a.prof = nullptr;
   if (IBF_PCG_PROFILE) {

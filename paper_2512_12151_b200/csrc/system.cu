@@ -662,6 +662,7 @@ int system_assemble(ibf_system* s, ibf_contacts* c, const double* x_hat, const d
       IBF_TRY(contact_build_incidence(c, s->n, st));
     }
     IBF_TRY(contact_prepare(c, x_hat, mu, offset, st));
+    if (IBF_PCG_WARP_TERMS) IBF_TRY(contact_pack_terms(c, s->n, mask, st));
     cv = contact_view(c);
     coef_g = c->coef_g.p;
   }

@@ -52,6 +52,8 @@ namespace ibf {
 int contact_prepare(ibf_contacts* c, const double* x_hat, double mu, double offset, cudaStream_t s);
 int contact_build_incidence(ibf_contacts* c, int64_t n_verts, cudaStream_t s);
 ContactView contact_view(ibf_contacts* c);
+// per-row PCG term records of the unmasked rows (mask: the assembled DBC mask or null)
+int contact_pack_terms(ibf_contacts* c, int64_t n_verts, const uint8_t* mask, cudaStream_t s);
 
 // friction.cu
 int friction_build_incidence(ibf_friction* f, int64_t n_verts, cudaStream_t s);

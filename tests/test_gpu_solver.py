@@ -350,8 +350,8 @@ def test_contact_heavy_subproblem_parity(pkg, n, layers, frames):
                                             dbc=system.dbc_mask)
     # the oracle's own rounding sensitivity: same solve from x_tilde perturbed by 1e-15 relative
     pert = x_tilde * (1.0 + 1e-15 * np.random.default_rng(1).standard_normal(x_tilde.shape))
-    _, _, cgo2, _, _ = newton.subproblem(pert, xt, x_hat0, system.masses, regions, o2, mu, params.offset, h,
-                                         dbc=system.dbc_mask)
+    xo2, _, cgo2, _, _ = newton.subproblem(pert, xt, x_hat0, system.masses, regions, o2, mu, params.offset, h,
+                                           dbc=system.dbc_mask)
     xh = to_dev(x_hat0)
     nw, cg, _, w = dev.solve_subproblem(aset, to_dev(x_tilde), x, xh, mu, params.offset, h, params.cg_tol,
                                         params.decay)
@@ -366,6 +366,16 @@ def test_contact_heavy_subproblem_parity(pkg, n, layers, frames):
     # by up to ~cond * 1e-4 of the step, so a bound relative to the step
     # would test rounding luck, not parity.
     assert np.abs(xg - xo).max() <= 1e-5 * np.abs(xo).max()
+    # ... and against the oracle's own spread: the GPU's deviation from the
+    # oracle must be of the size the oracle moves by under a 1e-15 relative
+    # input perturbation (its CG stops on a rounding-sensitive test too)
+    err = np.abs(xg - xo).max()
+    spread = np.abs(xo2 - xo).max()
+    step = np.abs(xo - xt).max()
+    print(f"\n[parity] n={n}: C={len(aset)} newton {nw}/{nwo} cg {cg}/{cgo} (perturbed oracle {cgo2}); "
+          f"max|dx| {err:.3e} = {err / step:.3e} of the step = {err / params.offset:.3e} of delta; "
+          f"oracle spread {spread:.3e}")
+    assert err <= max(10.0 * spread, 1e-12 * np.abs(xo).max()), (err, spread)
     sg = aset.export_state()
     assert np.array_equal(sg[3], o.gamma)
     # lambda <- lambda - mu c with c = d + grad_d . (x_hat - anchor) - offset
