@@ -304,6 +304,90 @@ __global__ void k_refit_packed(int n, const unsigned long long* __restrict__ k, 
   }
 }
 
+// 4-wide traversal records (IBF_CCD_WIDE): the binary tree collapsed two
+// levels at a time.  The record of an even-depth internal node holds its
+// grandchildren (or a leaf child itself, with an empty slot beside it):
+// four float boxes (SoA across the slots), the child ids (>= n-1: leaf,
+// else an even-depth internal node with its own record, -1: empty) and each
+// child's last sorted slot.  128 bytes, one L2 line, per visited node — a
+// walk takes about half the dependent fetches of the binary records.
+struct __align__(128) WideNode {
+  float4 lx, ly, lz, hx, hy, hz;
+  int4 child;
+  int4 last;
+};
+
+// depth parity of every internal node (1: odd), once per topology
+__global__ void k_depth_parity(int n, const int* __restrict__ parent, uint8_t* __restrict__ odd) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n - 1; i += gridDim.x * blockDim.x) {
+    int x = i, d = 0;
+    while (x != 0) {
+      x = parent[x];
+      d ^= 1;
+    }
+    odd[i] = (uint8_t)d;
+  }
+}
+
+// wide records of the even-depth internal nodes from the refitted binary records
+__global__ void k_widen(int n, const uint8_t* __restrict__ odd, const PackedNode* __restrict__ packed,
+                        WideNode* __restrict__ wide) {
+  const int nl = n - 1;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nl; i += gridDim.x * blockDim.x) {
+    if (odd[i]) continue;
+    const float* P = reinterpret_cast<const float*>(packed + i);
+    const int4 D = packed[i].d;
+    float lo[4][3], hi[4][3];
+    int ch[4], la[4];
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+      const int cid = side ? D.y : D.x;
+      const int clast = side ? D.w : D.z;
+      const int s0 = 2 * side;
+      if (cid >= nl) {
+        ch[s0] = cid;
+        la[s0] = clast;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          lo[s0][c] = P[6 * side + c];
+          hi[s0][c] = P[6 * side + 3 + c];
+        }
+        ch[s0 + 1] = -1;
+        la[s0 + 1] = -1;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          lo[s0 + 1][c] = INFINITY;
+          hi[s0 + 1][c] = -INFINITY;
+        }
+      } else {
+        const float* Q = reinterpret_cast<const float*>(packed + cid);
+        const int4 E = packed[cid].d;
+        ch[s0] = E.x;
+        ch[s0 + 1] = E.y;
+        la[s0] = E.z;
+        la[s0 + 1] = E.w;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          lo[s0][c] = Q[c];
+          hi[s0][c] = Q[3 + c];
+          lo[s0 + 1][c] = Q[6 + c];
+          hi[s0 + 1][c] = Q[9 + c];
+        }
+      }
+    }
+    WideNode w;
+    w.lx = make_float4(lo[0][0], lo[1][0], lo[2][0], lo[3][0]);
+    w.ly = make_float4(lo[0][1], lo[1][1], lo[2][1], lo[3][1]);
+    w.lz = make_float4(lo[0][2], lo[1][2], lo[2][2], lo[3][2]);
+    w.hx = make_float4(hi[0][0], hi[1][0], hi[2][0], hi[3][0]);
+    w.hy = make_float4(hi[0][1], hi[1][1], hi[2][1], hi[3][1]);
+    w.hz = make_float4(hi[0][2], hi[1][2], hi[2][2], hi[3][2]);
+    w.child = make_int4(ch[0], ch[1], ch[2], ch[3]);
+    w.last = make_int4(la[0], la[1], la[2], la[3]);
+    wide[i] = w;
+  }
+}
+
 struct Tree {
   int n;
   const unsigned long long* keys;  // sorted
@@ -312,6 +396,7 @@ struct Tree {
   const double* lo;
   const double* hi;
   const PackedNode* packed;        // internal-node records (null: FP64 node arrays only)
+  const WideNode* wide;            // 4-wide records of the even-depth internal nodes, or null
   const double* plo;               // primitive boxes (exact leaf test with `packed`)
   const double* phi;
 };
@@ -481,6 +566,9 @@ __global__ void __launch_bounds__(128) k_traverse(TraverseArgs a) {
 // emitted in the canonical (smaller id, larger id) orientation the per-query
 // `qi < pi` test gave — the same set (intact/ccd.py:131-138).
 constexpr int TRAV_CHUNK = 64;
+#ifndef IBF_CCD_PREFETCH
+#define IBF_CCD_PREFETCH 0
+#endif
 template <bool FILTER, bool SELF>
 __global__ void __launch_bounds__(128) k_traverse_dyn(TraverseArgs a) {
   const int lane = threadIdx.x & 31;
@@ -555,6 +643,9 @@ __global__ void __launch_bounds__(128) k_traverse_dyn(TraverseArgs a) {
     if (hl && hr) {
       stack[sp++] = D.y;
       node = D.x;
+      // the deferred child's record: start its fetch now (IBF_CCD_PREFETCH)
+      if (IBF_CCD_PREFETCH == 1) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.tree.packed + D.y));
+      if (IBF_CCD_PREFETCH == 2) asm volatile("prefetch.global.L1 [%0];" ::"l"(a.tree.packed + D.y));
     } else if (hl) {
       node = D.x;
     } else if (hr) {
@@ -563,6 +654,93 @@ __global__ void __launch_bounds__(128) k_traverse_dyn(TraverseArgs a) {
       node = stack[--sp];
     } else {
       t = -1;   // walk done
+    }
+  }
+  if (n_cand) atomicAdd(a.counters + 1, n_cand);
+}
+
+// k_traverse_dyn over the 4-wide records: same query fetching, slot pruning
+// and leaf handling; up to three internal children are pushed per step.
+template <bool FILTER, bool SELF>
+__global__ void __launch_bounds__(128) k_traverse_wide(TraverseArgs a) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  const int nl = a.tree.n - 1;
+  const long long nq = a.nq;
+  unsigned long long n_cand = 0;
+  long long pool = 0, pool_end = 0;
+  bool exhausted = false;
+  long long t = -1;
+  int qi = 0;
+  double ql[3], qh[3];
+  float qlf[3], qhf[3];
+  int stack[100];
+  int sp = 0, node = 0;
+  while (true) {
+    unsigned need = __ballot_sync(0xffffffffu, t < 0);
+    while (need && !exhausted) {
+      if (pool == pool_end) {
+        long long b = 0;
+        if (lane == 0) b = (long long)atomicAdd(a.counters + 3, (unsigned long long)TRAV_CHUNK);
+        b = __shfl_sync(0xffffffffu, b, 0);
+        if (b >= nq) {
+          exhausted = true;
+          break;
+        }
+        pool = b;
+        pool_end = b + TRAV_CHUNK < nq ? b + TRAV_CHUNK : nq;
+      }
+      const long long take = min((long long)__popc(need), pool_end - pool);
+      const int rank = __popc(need & lt);
+      if (t < 0 && rank < take) {
+        t = pool + rank;
+        qi = a.qorder ? (int)(a.qorder[t] & 0xffffffffull) : (int)t;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          ql[c] = a.qlo[3 * (int64_t)qi + c];
+          qh[c] = a.qhi[3 * (int64_t)qi + c];
+          qlf[c] = __double2float_rd(ql[c]);
+          qhf[c] = __double2float_ru(qh[c]);
+        }
+        sp = 0;
+        node = 0;
+      }
+      pool += take;
+      need = __ballot_sync(0xffffffffu, t < 0);
+    }
+    if (__ballot_sync(0xffffffffu, t >= 0) == 0) break;
+    if (t < 0) continue;
+    const WideNode* W = a.tree.wide + node;
+    const float4 lx = __ldg(&W->lx), ly = __ldg(&W->ly), lz = __ldg(&W->lz);
+    const float4 hx = __ldg(&W->hx), hy = __ldg(&W->hy), hz = __ldg(&W->hz);
+    const int4 ch = __ldg(&W->child), la = __ldg(&W->last);
+    const int cid[4] = {ch.x, ch.y, ch.z, ch.w};
+    const int cl[4] = {la.x, la.y, la.z, la.w};
+    const float Lx[4] = {lx.x, lx.y, lx.z, lx.w}, Ly[4] = {ly.x, ly.y, ly.z, ly.w}, Lz[4] = {lz.x, lz.y, lz.z, lz.w};
+    const float Hx[4] = {hx.x, hx.y, hx.z, hx.w}, Hy[4] = {hy.x, hy.y, hy.z, hy.w}, Hz[4] = {hz.x, hz.y, hz.z, hz.w};
+    int next = -1;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      bool h = overlap_f(qlf, qhf, Lx[k], Ly[k], Lz[k], Hx[k], Hy[k], Hz[k]);
+      if (SELF) h = h && cl[k] > t;
+      if (!h) continue;
+      const int c = cid[k];
+      if (c >= nl) {
+        const int pi = (int)(a.tree.keys[c - nl] & 0xffffffffull);
+        if (overlap(ql, qh, a.tree.plo + 3 * pi, a.tree.phi + 3 * pi))
+          traverse_leaf<FILTER>(a, SELF ? min(qi, pi) : qi, SELF ? max(qi, pi) : pi, n_cand);
+      } else if (next < 0) {
+        next = c;
+      } else {
+        stack[sp++] = c;
+      }
+    }
+    if (next >= 0) {
+      node = next;
+    } else if (sp > 0) {
+      node = stack[--sp];
+    } else {
+      t = -1;
     }
   }
   if (n_cand) atomicAdd(a.counters + 1, n_cand);
@@ -669,6 +847,10 @@ static int grid_for(int64_t n, int threads = 256) {
 #ifndef IBF_CCD_VF_ORDER
 #define IBF_CCD_VF_ORDER 0
 #endif
+// 4-wide traversal records (1) or the binary packed records (0)
+#ifndef IBF_CCD_WIDE
+#define IBF_CCD_WIDE 1
+#endif
 // packed traversal with dynamic query fetching (1) or one query per thread (0)
 #ifndef IBF_CCD_DYNAMIC
 #define IBF_CCD_DYNAMIC 1
@@ -684,6 +866,8 @@ static int build_tree(ibf_ccd* c, int64_t n, cudaStream_t s, Tree& t, ibf_ccd::T
   int *left, *right, *parent, *flag, *last;
   double *lo, *hi;
   float4* packed4;
+  WideNode* wide = nullptr;
+  uint8_t* odd = nullptr;
   bool refit_only = false;
   if (cache) {
     IBF_TRY(cache->keys_sorted.reserve(n));
@@ -697,6 +881,12 @@ static int build_tree(ibf_ccd* c, int64_t n, cudaStream_t s, Tree& t, ibf_ccd::T
       IBF_TRY(cache->hi.reserve(3 * nn));
     }
     IBF_TRY(cache->packed.reserve(4 * nn));
+    if (IBF_CCD_WIDE && IBF_CCD_PACKED && n > 1) {
+      IBF_TRY(cache->wide.reserve(8 * (size_t)(n - 1)));
+      IBF_TRY(cache->odd.reserve(n - 1));
+      wide = reinterpret_cast<WideNode*>(cache->wide.p);
+      odd = cache->odd.p;
+    }
     refit_only = cache->n == n && cache->uses < IBF_CCD_REBUILD;
     keys_sorted = cache->keys_sorted.p;
     left = cache->left.p, right = cache->right.p, parent = cache->parent.p, flag = cache->flag.p;
@@ -713,6 +903,12 @@ static int build_tree(ibf_ccd* c, int64_t n, cudaStream_t s, Tree& t, ibf_ccd::T
     IBF_TRY(c->node_lo.reserve(3 * nn));
     IBF_TRY(c->node_hi.reserve(3 * nn));
     IBF_TRY(c->node_packed.reserve(4 * nn));
+    if (IBF_CCD_WIDE && IBF_CCD_PACKED && n > 1) {
+      IBF_TRY(c->node_wide.reserve(8 * (size_t)(n - 1)));
+      IBF_TRY(c->node_odd.reserve(n - 1));
+      wide = reinterpret_cast<WideNode*>(c->node_wide.p);
+      odd = c->node_odd.p;
+    }
     keys_sorted = c->keys_sorted.p;
     left = c->node_left.p, right = c->node_right.p, parent = c->node_parent.p, flag = c->node_flag.p;
     last = c->node_last.p;
@@ -736,6 +932,10 @@ static int build_tree(ibf_ccd* c, int64_t n, cudaStream_t s, Tree& t, ibf_ccd::T
     if (n > 1) {
       k_build<<<grid_for(n - 1), 256, 0, s>>>((int)n, keys_sorted, left, right, parent, last);
       IBF_LAUNCH_CHECK();
+      if (odd) {
+        k_depth_parity<<<grid_for(n - 1), 256, 0, s>>>((int)n, parent, odd);
+        IBF_LAUNCH_CHECK();
+      }
     }
     if (cache) {
       cache->n = n;
@@ -757,6 +957,11 @@ static int build_tree(ibf_ccd* c, int64_t n, cudaStream_t s, Tree& t, ibf_ccd::T
                                          lo, hi, nullptr);
   }
   IBF_LAUNCH_CHECK();
+  if (wide && packed && n > 1) {
+    k_widen<<<grid_for(n - 1), 256, 0, s>>>((int)n, odd, packed, wide);
+    IBF_LAUNCH_CHECK();
+  }
+  t.wide = (packed && n > 1) ? wide : nullptr;
   t.packed = n > 1 ? packed : nullptr;
   t.plo = c->box_lo.p;
   t.phi = c->box_hi.p;
@@ -863,6 +1068,9 @@ static int broad_pass(ibf_ccd* c, int kind, const double* x0, const double* x1, 
         const bool self = kind != 0 && a.qorder == tree.keys;
         auto kern = a.filter ? (self ? k_traverse_dyn<true, true> : k_traverse_dyn<true, false>)
                              : (self ? k_traverse_dyn<false, true> : k_traverse_dyn<false, false>);
+        if (tree.wide)
+          kern = a.filter ? (self ? k_traverse_wide<true, true> : k_traverse_wide<true, false>)
+                          : (self ? k_traverse_wide<false, true> : k_traverse_wide<false, false>);
         static int blocks_per_sm = 0;
         if (!blocks_per_sm) {
           cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_traverse_dyn<false, true>, 128, 0);

@@ -164,6 +164,7 @@ struct PcgWork {
   DevBuf<double> part_chunk;         // dynamic phase-A per-chunk partials
   DevBuf<unsigned> ready;            // term-dot ready counter
   DevBuf<double> zdot, pdot;         // zdot mode: per-record z and previous-direction products
+  DevBuf<double> tprev;              // linear-recursion contact dots: g_c . p_{k-1}
   int grid = 0;
   int n_alloc = -1;
 };
@@ -275,6 +276,8 @@ struct ibf_ccd {
   ibf::DevBuf<int> node_left, node_right, node_parent, node_flag, node_last;
   ibf::DevBuf<double> node_lo, node_hi;
   ibf::DevBuf<float4> node_packed;                      // 4 per internal node (ccd.cu PackedNode)
+  ibf::DevBuf<float4> node_wide;                        // 8 per internal node (ccd.cu WideNode)
+  ibf::DevBuf<uint8_t> node_odd;
   // VF (triangle) and EE (edge) trees kept between calls: later calls refit
   // the cached topology to the new boxes; it is rebuilt every few calls
   struct TreeCache {
@@ -282,6 +285,8 @@ struct ibf_ccd {
     ibf::DevBuf<int> left, right, parent, flag, last;
     ibf::DevBuf<double> lo, hi;
     ibf::DevBuf<float4> packed;
+    ibf::DevBuf<float4> wide;                            // 4-wide records (8 float4 per internal node)
+    ibf::DevBuf<uint8_t> odd;                            // internal-node depth parity
     int64_t n = -1;
     int uses = 0;
   } tc[2];

