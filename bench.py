@@ -19,9 +19,11 @@ is needed between frames.
 --workload c4ball is the round-1 solid-ball proxy (same tet count, 0.40M
 vertices, 0.11M surface triangles); --workload c5 the scene-parallel batch.
 
-Multi-GPU (torchrun): one scene per rank ("replicas only", DESIGN.md §(e));
-value = the slowest rank's ms/frame, and `replica_scene_frames_per_s` the
-replicas' throughput.
+Multi-GPU (torchrun): by default one scene with its PCG rows split over the
+ranks (--mode partition: NCCL allreduce / allgather inside each CG
+iteration, assembly / CCD / line search replicated, "scaling": "strong",
+DESIGN.md §(e)); --mode replicas runs one scene per rank instead (value = the
+slowest rank's ms/frame, `replica_scene_frames_per_s` their throughput).
 
 --impl reference times the reference's CPU path as the oracle port (oracle/,
 single-threaded numpy) on bounded samples of the same scene
@@ -184,7 +186,7 @@ def _scene(args):
     from paper_2512_12151_b200 import scenes
     if args.workload == "c4ball":
         return scenes.c4_scene(n=args.n, plate_speed=0.5, plate_stop=0.05)
-    return scenes.squishy_scene(cell=args.cell, plate_speed=args.plate_speed)
+    return scenes.squishy_scene(cell=args.cell, plate_speed=args.plate_speed, numbering=args.numbering)
 
 
 def workload(args):
@@ -195,8 +197,8 @@ def workload(args):
         return (f"C4 solid-ball proxy: five COR balls n={args.n} ({5 * 6 * args.n ** 3} ball tets) pressed by a "
                 f"plate at 0.5 m/s down to 0.05 m; {frames}")
     return (f"C4 squishy balls: five COR squishy balls (hollow core + 600 strands each, scenes.squishy_scene "
-            f"cell={args.cell} m: 2.30M tets, 0.90M vertices, 1.62M surface triangles) in a pinned box, pressed "
-            f"by a plate at {args.plate_speed} m/s under gravity; {frames}")
+            f"cell={args.cell} m: 2.30M tets, 0.90M vertices, 1.62M surface triangles; {args.numbering} vertex "
+            f"numbering) in a pinned box, pressed by a plate at {args.plate_speed} m/s under gravity; {frames}")
 
 
 def _oracle_counts(counts_path=None):
@@ -380,6 +382,21 @@ def run_ours(args):
     system, state, params = _scene(args)
     dev = system.device
     ccd = system.ccd
+    # N > 1: one scene, its PCG rows split over the ranks (NCCL allreduce /
+    # allgather inside the solve, csrc/dist.cu); assembly, CCD and line search
+    # run replicated on every rank (the ranks' states stay bit-identical).
+    # --mode replicas runs N independent copies instead.
+    mode = "single-gpu"
+    part = None
+    if ws > 1:
+        mode = args.mode
+        if mode == "partition":
+            from paper_2512_12151_b200 import dist as pdist
+            try:
+                part = pdist.Partition.from_torch()
+                dev.set_dist(part)
+            except Exception as exc:      # no NCCL communicator: say so and run replicas
+                part, mode = None, f"replicas (partition unavailable: {exc})"[:200]
     aset = ActiveSet()
     aset.ensure(system.n_vertices)
     n = system.n_vertices
@@ -459,10 +476,20 @@ def run_ours(args):
     frame_ms = [e[1].elapsed_time(e[2]) for e in evs]
     e2e_ms = [e[0].elapsed_time(e[3]) for e in evs]
     tot_dev, tot_e2e = float(np.sum(frame_ms)), float(np.sum(e2e_ms))
+    consistent = None
     if ws > 1:
         t = torch.tensor([tot_dev, tot_e2e], dtype=torch.float64, device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         tot_dev, tot_e2e = float(t[0]), float(t[1])
+        if part is not None:
+            # the partitioned solve hands every rank the same solution: the
+            # ranks' final states must agree bit for bit
+            ck = torch.tensor([float(xn.double().sum()), float(vn.double().sum())], dtype=torch.float64,
+                              device="cuda")
+            lo, hi = ck.clone(), ck.clone()
+            torch.distributed.all_reduce(lo, op=torch.distributed.ReduceOp.MIN)
+            torch.distributed.all_reduce(hi, op=torch.distributed.ReduceOp.MAX)
+            consistent = bool(torch.equal(lo, hi))
     L.ibf_system_stats(dev.handle, _lib.host_ptr(stats), 0)
     L.ibf_ccd_stats(ccd.handle, _lib.host_ptr(cst), 0)
     L.ibf_system_counts(dev.handle, _lib.host_ptr(cnt), 0)
@@ -492,7 +519,8 @@ def run_ours(args):
     counts = {"newton": newton / args.steps, "cg": cg / args.steps, "passes": passes / args.steps,
               "energy": cnt[1] / args.steps}
     line = {"metric": METRIC, "value": value, "unit": "ms/frame", "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": value, "higher_is_better": False, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": value, "higher_is_better": False,
+            "scaling": "strong" if part is not None else "weak",
             # value / the paper's 5,367 ms/frame (RTX 4090, FP64, the authors' own mesh)
             "vs_baseline": round(value / 5367.0, 4) if value > 0 else None,
             "vs_baseline_note": "value / 5367 ms/frame (paper Table 1, RTX 4090, its own squishy-ball mesh); "
@@ -502,7 +530,9 @@ def run_ours(args):
                        "system": f"{sum(len(r.tets) for r in system.regions)} tets, {n} vertices "
                                  f"({int(system.dbc_mask.sum())} pinned), {len(system.surface_triangles)} surface "
                                  f"triangles",
-                       "parallelism": f"replicas x{ws} (one scene per GPU)" if ws > 1 else "single-gpu",
+                       "parallelism": (f"row-partitioned PCG x{ws} (one scene; assembly, CCD and line search "
+                                       f"replicated per rank)" if part is not None else
+                                       f"replicas x{ws} (one scene per GPU): {mode}" if ws > 1 else "single-gpu"),
                        "l2": "inputs > L2 (matrix ~%.0f MB, no flush needed)" % (spmv_bytes / 1e6)},
             "ms_per_newton_iter": tot_dev / max(newton, 1),
             "newton_per_frame": counts["newton"], "cg_per_frame": counts["cg"], "passes_per_frame": counts["passes"],
@@ -524,8 +554,10 @@ def run_ours(args):
             "frames_constraints": n_constraints,
             "slowest_pass_wall_ms": [round(t, 1) for t in pass_ms], "wall_s": wall, "setup_s": setup_s,
             "precompress_s": pre_s}
-    if ws > 1:
+    if ws > 1 and part is None:
         line["replica_scene_frames_per_s"] = ws * args.steps / (tot_dev * 1e-3)
+    if consistent is not None:
+        line["ranks_bit_identical"] = consistent
     if cert:
         line["penetration_free"] = {
             "frames_checked": len(cert), "min_distance": min(c[0] for c in cert),
@@ -642,9 +674,13 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cell", type=float, default=0.02, help="c4: squishy-ball cell edge (m)")
     ap.add_argument("--plate-speed", type=float, default=2.0, help="c4: plate speed (m/s)")
+    ap.add_argument("--numbering", default="lattice", choices=["sell", "lattice", "morton"],
+                    help="c4: squishy-ball vertex numbering (mesh.sell_numbering / lattice / Morton)")
     ap.add_argument("--n", type=int, default=42, help="c4ball: ball resolution (42 -> 2.22M tets)")
     ap.add_argument("--precompress", type=int, default=40,
                     help="untimed frames of the press before warm-up (reaches the contact-heavy regime)")
+    ap.add_argument("--mode", default="partition", choices=["partition", "replicas"],
+                    help="N > 1: row-partitioned PCG of one scene (strong scaling) or N independent replicas")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-certify", action="store_true", help="skip the per-frame penetration certificate")
     ap.add_argument("--workload", default="c4", choices=["c4", "c4ball", "c5"],

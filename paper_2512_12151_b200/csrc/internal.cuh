@@ -165,6 +165,8 @@ struct PcgWork {
   DevBuf<unsigned> ready;            // term-dot ready counter
   DevBuf<double> zdot, pdot;         // zdot mode: per-record z and previous-direction products
   DevBuf<double> tprev;              // linear-recursion contact dots: g_c . p_{k-1}
+  DevBuf<int> wcounter;              // warp-dynamic phase A: slice counters + group counts
+  DevBuf<double> part_unit;          // warp-dynamic phase A: slice and group partials
   int grid = 0;
   int n_alloc = -1;
 };

@@ -52,6 +52,22 @@ int dev_alloc(void** p, size_t bytes) {
     IBF_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
     uint64_t keep = UINT64_MAX;
     IBF_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    // Prime the pool: map one large block up front and return it, so buffer
+    // growth mid-press is carved from memory the pool already holds.  Growth
+    // that had to map new memory stalled single passes by 0.1-0.7 s on the
+    // squishy press (bench "slowest_pass_wall_ms").  IBF_POOL_PRIME_GB
+    // overrides the size (default: 20 % of free memory, at most 24 GB).
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
+      size_t prime = std::min<size_t>(free_b / 5, (size_t)24 << 30);
+      if (const char* e = getenv("IBF_POOL_PRIME_GB")) prime = (size_t)(atof(e) * (double)(1ull << 30));
+      void* q = nullptr;
+      if (prime && cudaMallocAsync(&q, prime, 0) == cudaSuccess) {
+        cudaFreeAsync(q, 0);
+        cudaStreamSynchronize(0);
+      }
+      cudaGetLastError();
+    }
     pools_ready.fetch_or(1u << dev);
   }
   const cudaStream_t s = tl_stream;

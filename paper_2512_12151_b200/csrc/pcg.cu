@@ -98,10 +98,24 @@ constexpr int PCG_SMEM_BYTES = IBF_PCG_SMEM_KB * 1024;
 
 // ---------------------------------------------------------------- gathers
 
+// Diagnostic builds for the DRAM-traffic breakdown (never the product):
+// IBF_DIAG_NO_GATHER replaces the SpMV's vector gathers by constants,
+// IBF_DIAG_NO_LOWER skips the transposed (lower) entries.
+#ifndef IBF_DIAG_NO_GATHER
+#define IBF_DIAG_NO_GATHER 0
+#endif
+#ifndef IBF_DIAG_NO_LOWER
+#define IBF_DIAG_NO_LOWER 0
+#endif
+
 // p at vertex j: a plain vector ...
 struct PlainGather {
   const double* __restrict__ p;
   __device__ __forceinline__ void get(int j, double& x0, double& x1, double& x2) const {
+    if (IBF_DIAG_NO_GATHER) {
+      x0 = x1 = x2 = 1e-3 * (double)(j & 7);
+      return;
+    }
     const double* P = p + 3 * (size_t)j;
     x0 = P[0];
     x1 = P[1];
@@ -128,6 +142,10 @@ struct DirGather {
   double beta;
   bool first;
   __device__ __forceinline__ void get(int j, double& x0, double& x1, double& x2) const {
+    if (IBF_DIAG_NO_GATHER) {
+      x0 = x1 = x2 = 1e-3 * (double)(j & 7);
+      return;
+    }
     const double* Z = z + 3 * (size_t)j;
     if (first) {
       x0 = Z[0];
@@ -334,7 +352,7 @@ __device__ __forceinline__ void row_product(const Operator& op, const Gather& gp
       acc_upper(b, x0, x1, x2, a0, a1, a2);
     }
   }
-  {
+  if (!IBF_DIAG_NO_LOWER) {
     const int l0 = __ldg(op.low_ptr + s), w = (__ldg(op.low_ptr + s + 1) - l0) >> 5;
     const int2* L = op.low + l0 + lane;
     int t = 0;
@@ -788,6 +806,12 @@ struct PcgArgs {
   double* pdot;         // (C,4) each record's copy of g_c . p_{k-1}
   int zmode;
   double* tprev;        // (C) g_c . p_{k-1} for the linear-recursion dots, or null
+  int wdyn;             // warp-granular dynamic phase A (IBF_PCG_WARPDYN)
+  int n_units, n_groups;
+  int* wcounter;        // (2) slice counters, alternating iterations
+  int* gcount;          // (n_groups) finished slices per group
+  double* part_unit;    // (n_units) per-slice p.q partials
+  double* part_group;   // (n_groups) per-group sums
 };
 
 // all CTAs compute the same fixed-order total of part[slot*G .. slot*G+G)
@@ -982,6 +1006,86 @@ __global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
           double v = 0.0;
           for (int c = threadIdx.x; c < a.n_chunks; c += blockDim.x) v += a.part_chunk[c];
           pap = block_sum(v, red);
+        }
+        PCG_PT(2)
+      } else if (a.wdyn) {
+        // Warp-granular dynamic phase A (IBF_PCG_WARPDYN): each warp takes
+        // the next 32-row slice with one atomic, in ascending order, so the
+        // CTAs that run fast (locality, memory-latency luck: measured
+        // per-CTA spread +-11 %, weakly tied to their nnz) absorb the slow
+        // ones' share and the barrier waits shrink.  p.q stays deterministic:
+        // a slice's partial is the warp's fixed tree sum, stored by slice;
+        // the last warp to finish a group of 64 slices sums the group's 64
+        // partials in slice order, and every CTA sums the group partials in
+        // group order after the barrier.
+        const int lane = threadIdx.x & 31;
+        if (blockIdx.x == 0 && threadIdx.x == 0) a.wcounter[(it + 1) & 1] = 0;
+        const bool wt = IBF_PCG_WARP_TERMS && op.contact.n && op.contact.rec && !op.perm;
+        while (true) {
+          int u = 0;
+          if (lane == 0) u = atomicAdd(a.wcounter + (it & 1), 1);
+          u = __shfl_sync(0xffffffffu, u, 0);
+          if (u >= a.n_units) break;
+          const int pos = 32 * u + lane;
+          double pq = 0.0;
+          if (pos < n) {
+            const int i = row_at(op, pos);
+            double v[3], pv[3];
+            if (wt) {
+              if (counted)
+                row_product<DirGather, CountedTerms, false>(op, gd, pos, i, v, sterms);
+              else
+                row_product<DirGather, StoredTerms, false>(op, gd, pos, i, v);
+              if (counted)
+                warp_terms(op.contact, sterms, pos & ~31, n, wbuf, v[0], v[1], v[2]);
+              else
+                warp_terms(op.contact, StoredTerms(), pos & ~31, n, wbuf, v[0], v[1], v[2]);
+            } else {
+              product(pos, i, v);
+            }
+            gd.get(i, pv[0], pv[1], pv[2]);
+            double* pki = pk + 3 * (size_t)i;
+            pki[0] = pv[0]; pki[1] = pv[1]; pki[2] = pv[2];
+            double* qi = a.hp + 3 * (size_t)i;
+            qi[0] = v[0]; qi[1] = v[1]; qi[2] = v[2];
+            pq = pv[0] * v[0] + pv[1] * v[1] + pv[2] * v[2];
+          } else if (wt) {
+            if (counted)
+              warp_terms(op.contact, sterms, pos & ~31, n, wbuf, dummy[0], dummy[1], dummy[2]);
+            else
+              warp_terms(op.contact, StoredTerms(), pos & ~31, n, wbuf, dummy[0], dummy[1], dummy[2]);
+          }
+          pq = warp_sum(pq);
+          int last = 0;
+          const int g = u >> 6, gsize = min(64, a.n_units - (g << 6));
+          if (lane == 0) {
+            a.part_unit[u] = pq;
+            __threadfence();
+            last = (atomicAdd(a.gcount + g, 1) == gsize - 1);
+          }
+          last = __shfl_sync(0xffffffffu, last, 0);
+          if (last) {
+            __threadfence();
+            const double* P = a.part_unit + (g << 6);
+            double v = (lane < gsize ? __ldcg(P + lane) : 0.0) + (lane + 32 < gsize ? __ldcg(P + lane + 32) : 0.0);
+            v = warp_sum(v);
+            if (lane == 0) {
+              a.part_group[g] = v;
+              a.gcount[g] = 0;
+            }
+          }
+        }
+        PCG_PT(1)
+        grid.sync();
+        {
+          double v = 0.0;
+          if (threadIdx.x < 32) {
+            v = warp_sum_array(a.part_group, a.n_groups);
+            if (threadIdx.x == 0) bc[0] = v;
+          }
+          __syncthreads();
+          pap = bc[0];
+          __syncthreads();
         }
         PCG_PT(2)
       } else {
@@ -1271,6 +1375,18 @@ struct PcgShape {
 // sweeps per thread on systems the oracle solves in seconds.
 static std::atomic<long long> g_lanes_max_n{IBF_PCG_LANES_MAX_N};
 static std::atomic<int> g_max_ctas{0};
+// warp-granular dynamic phase A: IBF_PCG_WARPDYN default, the environment
+// variable of the same name overrides (0 / 1) for A/B runs
+#ifndef IBF_PCG_WARPDYN
+#define IBF_PCG_WARPDYN 0
+#endif
+static int warpdyn_enabled() {
+  static const int on = [] {
+    const char* e = getenv("IBF_PCG_WARPDYN");
+    return e ? (e[0] == '1' ? 1 : 0) : IBF_PCG_WARPDYN;
+  }();
+  return on;
+}
 // zdot mode on (IBF_PCG_ZDOT builds) unless the environment sets IBF_PCG_ZDOT=0 (A/B runs)
 static int zdot_enabled() {
   static const int on = [] {
@@ -1435,6 +1551,22 @@ int pcg_solve(const Operator& op, const double* rhs, double* x_out, double rel_t
     IBF_CUDA(cudaMemsetAsync(w.zdot.p, 0, nc4 * sizeof(double), s));
     a.zdot = w.zdot.p;
     a.pdot = w.pdot.p;
+  }
+  a.wdyn = 0;
+  a.n_units = a.n_groups = 0;
+  a.wcounter = a.gcount = nullptr;
+  a.part_unit = a.part_group = nullptr;
+  if (warpdyn_enabled() && lanes == 1 && !a.n_chunks && !IBF_PCG_CARRY_QP && !a.zmode) {
+    a.wdyn = 1;
+    a.n_units = (int)div_up(std::max(n, 1), 32);
+    a.n_groups = (int)div_up(a.n_units, 64);
+    IBF_TRY(w.wcounter.reserve(2 + (size_t)a.n_groups));
+    IBF_TRY(w.part_unit.reserve((size_t)a.n_units + a.n_groups));
+    IBF_CUDA(cudaMemsetAsync(w.wcounter.p, 0, (2 + (size_t)a.n_groups) * sizeof(int), s));
+    a.wcounter = w.wcounter.p;
+    a.gcount = w.wcounter.p + 2;
+    a.part_unit = w.part_unit.p;
+    a.part_group = w.part_unit.p + a.n_units;
   }
   a.tprev = nullptr;
   if (IBF_PCG_DOT_REC && op.contact.n && !a.zmode) {

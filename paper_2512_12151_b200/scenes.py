@@ -28,7 +28,7 @@ from __future__ import annotations
 import numpy as np
 
 from .elasticity import Material, MaterialModel
-from .mesh import SimState, TetMesh, build_tet_mesh, compute_rest_data, reorder_for_locality
+from .mesh import SimState, TetMesh, build_tet_mesh, compute_rest_data, reorder_for_locality, reorder_for_sell
 from .solver import ElasticRegion
 from .stepper import BoundaryCondition, StepParams, System
 
@@ -117,7 +117,7 @@ def _sphere_map(c, radius, blend=0.8):
 
 
 def squishy_ball(n=32, shell=2, stem=23, tip=16, pitch=3, cell=0.01, center=(0.0, 0.0, 0.0),
-                 reorder=False) -> TetMesh:
+                 reorder=False, numbering="lattice") -> TetMesh:
     """Squishy ball: a hollow core with thin strands all over it.
 
     The core is the outer `shell` Kuhn-cell layers of an n^3 grid mapped onto
@@ -200,7 +200,11 @@ def squishy_ball(n=32, shell=2, stem=23, tip=16, pitch=3, cell=0.01, center=(0.0
     shift = np.where(tipv[:, None], 0.5 * (bw - bc), bw - bc)
     pos[out] = bc + shift + (l * cell)[:, None] * axis
     mesh = build_tet_mesh(pos + np.asarray(center, dtype=np.float64), tets)
-    return reorder_for_locality(mesh) if reorder else mesh
+    if reorder or numbering == "morton":
+        return reorder_for_locality(mesh)
+    if numbering == "sell":
+        return reorder_for_sell(mesh)
+    return mesh
 
 
 def squishy_extent(n=32, stem=23, tip=16, cell=0.01):
@@ -333,7 +337,7 @@ def c4_scene(n=42, radius=0.1, gap=0.001, plate_speed=0.1, h=0.01, layers=None, 
 
 
 def squishy_scene(cell=0.02, n=32, stem=23, tip=16, shell=2, gap=None, plate_speed=1.0, plate_stop=None, h=0.01,
-                  walls=True, seed=7, balls=5, reorder=False):
+                  walls=True, seed=7, balls=5, reorder=False, numbering="lattice"):
     """C4, paper-scale: five squishy balls in a box, pressed by a plate.
 
     Each ball is a `squishy_ball` (hollow core + 600 strands; the defaults
@@ -349,9 +353,12 @@ def squishy_scene(cell=0.02, n=32, stem=23, tip=16, shell=2, gap=None, plate_spe
     height, PAPER.md:596).  Physical scale: `cell` is the strand cell edge;
     2 cm puts block-Jacobi PCG at ~90-110 CG iterations per solve (the
     paper's average is 28, its peak 146), see DESIGN.md.
+    `numbering` = the ball's vertex numbering: "lattice" (default), "sell"
+    (lattice order with 1024-vertex windows sorted for even sliced-ELL
+    slices, mesh.sell_numbering; measured slower) or "morton".
     """
     rng = np.random.default_rng(seed)
-    base = squishy_ball(n=n, shell=shell, stem=stem, tip=tip, cell=cell, reorder=reorder)
+    base = squishy_ball(n=n, shell=shell, stem=stem, tip=tip, cell=cell, reorder=reorder, numbering=numbering)
     R = float(np.linalg.norm(base.rest_positions, axis=1).max())
     gap = 2.0 * cell if gap is None else gap
     mat = Material(MaterialModel.COR, 1e4, 0.4)

@@ -25,6 +25,7 @@ from paper_2512_12151_b200.stepper import step_device
 ap = argparse.ArgumentParser()
 ap.add_argument("--frames", type=int, default=45)
 ap.add_argument("--cell", type=float, default=0.02)
+ap.add_argument("--numbering", default="lattice", choices=["sell", "lattice", "morton"])
 ap.add_argument("--plate-speed", type=float, default=2.0)
 ap.add_argument("--load", default=None)
 ap.add_argument("--dump", default=None)
@@ -33,7 +34,7 @@ ap.add_argument("--scale", type=float, default=1.0)
 ap.add_argument("--ncu", action="store_true", help="profile the last call (cudaProfilerStart/Stop)")
 args = ap.parse_args()
 
-system, state, params = scenes.squishy_scene(cell=args.cell, plate_speed=args.plate_speed)
+system, state, params = scenes.squishy_scene(numbering=args.numbering, cell=args.cell, plate_speed=args.plate_speed)
 aset = ActiveSet()
 aset.ensure(system.n_vertices)
 x, v = to_dev(state.x), to_dev(state.v)

@@ -29,6 +29,7 @@ ap.add_argument("--cell", type=float, default=0.02)
 ap.add_argument("--n", type=int, default=32)
 ap.add_argument("--stem", type=int, default=23)
 ap.add_argument("--tip", type=int, default=16)
+ap.add_argument("--numbering", default="lattice", choices=["sell", "lattice", "morton"])
 ap.add_argument("--plate-speed", type=float, default=2.0)
 ap.add_argument("--load", default=None)
 ap.add_argument("--dump", default=None)
@@ -37,7 +38,7 @@ ap.add_argument("--ncu", action="store_true", help="profile one PCG launch (cuda
 ap.add_argument("--reorder", action="store_true", help="Morton vertex numbering instead of the lattice's")
 args = ap.parse_args()
 
-system, state, params = scenes.squishy_scene(cell=args.cell, n=args.n, stem=args.stem, tip=args.tip,
+system, state, params = scenes.squishy_scene(numbering=args.numbering, cell=args.cell, n=args.n, stem=args.stem, tip=args.tip,
                                              plate_speed=args.plate_speed, reorder=args.reorder)
 aset = ActiveSet()
 aset.ensure(system.n_vertices)

@@ -27,6 +27,7 @@ ap.add_argument("--stem", type=int, default=23)
 ap.add_argument("--tip", type=int, default=16)
 ap.add_argument("--shell", type=int, default=2)
 ap.add_argument("--balls", type=int, default=5)
+ap.add_argument("--numbering", default="lattice", choices=["sell", "lattice", "morton"])
 ap.add_argument("--plate-speed", type=float, default=1.0)
 ap.add_argument("--plate-stop", type=float, default=None)
 ap.add_argument("--certify", action="store_true")
@@ -39,7 +40,7 @@ ap.add_argument("--profile-frames", type=int, default=0,
 args = ap.parse_args()
 
 t = time.perf_counter()
-system, state, params = scenes.squishy_scene(cell=args.cell, n=args.n, stem=args.stem, tip=args.tip,
+system, state, params = scenes.squishy_scene(numbering=args.numbering, cell=args.cell, n=args.n, stem=args.stem, tip=args.tip,
                                              shell=args.shell, balls=args.balls, plate_speed=args.plate_speed,
                                              plate_stop=args.plate_stop)
 info = dict(system.scene_info, n_vertices=system.n_vertices, tets=int(sum(len(r.tets) for r in system.regions)),
