@@ -423,6 +423,11 @@ struct TraverseArgs {
   // (its sorted keys), so a warp's 32 traversals follow nearly the same path
   const unsigned long long* qorder;
   unsigned long long* counters;  // [0] emitted, [1] all candidates
+  // 1: leaves are tested exactly (FP64 primitive boxes) inside the walk;
+  // 0: the walk emits every leaf whose float box overlaps and k_prefilter
+  // runs the exact test (it recomputes both swept boxes from the vertex
+  // positions it loads anyway, bit-identically to k_swept_boxes)
+  int exact_leaf;
 };
 
 __device__ __forceinline__ bool make_quad(const TraverseArgs& a, int qi, int pi, int q[4]) {
@@ -727,7 +732,7 @@ __global__ void __launch_bounds__(128) k_traverse_wide(TraverseArgs a) {
       const int c = cid[k];
       if (c >= nl) {
         const int pi = (int)(a.tree.keys[c - nl] & 0xffffffffull);
-        if (overlap(ql, qh, a.tree.plo + 3 * pi, a.tree.phi + 3 * pi))
+        if (!a.exact_leaf || overlap(ql, qh, a.tree.plo + 3 * pi, a.tree.phi + 3 * pi))
           traverse_leaf<FILTER>(a, SELF ? min(qi, pi) : qi, SELF ? max(qi, pi) : pi, n_cand);
       } else if (next < 0) {
         next = c;
@@ -750,7 +755,27 @@ __global__ void __launch_bounds__(128) k_traverse_wide(TraverseArgs a) {
 // candidate (no FP64 work inside the tree walk, so it keeps ~40 % of the
 // registers and its warps stay converged between leaves), then one thread
 // per candidate runs the ACCD prefilter and appends the survivors.
+// swept box of vertices X0/X1[k0 .. k0+K) exactly as k_swept_boxes forms it
+__device__ __forceinline__ void quad_box(const V3* X0, const V3* X1, int k0, int K, double pad, double lo[3],
+                                         double hi[3]) {
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    double l0 = INFINITY, h0 = -INFINITY, l1 = INFINITY, h1 = -INFINITY;
+    for (int k = k0; k < k0 + K; ++k) {
+      const double av = c == 0 ? X0[k].x : (c == 1 ? X0[k].y : X0[k].z);
+      const double bv = c == 0 ? X1[k].x : (c == 1 ? X1[k].y : X1[k].z);
+      l0 = geo::np_min(l0, av);
+      h0 = geo::np_max(h0, av);
+      l1 = geo::np_min(l1, bv);
+      h1 = geo::np_max(h1, bv);
+    }
+    lo[c] = geo::sub(geo::np_min(l0, l1), pad);
+    hi[c] = geo::add(geo::np_max(h0, h1), pad);
+  }
+}
+
 __global__ void __launch_bounds__(256) k_prefilter(TraverseArgs a, int64_t n, const unsigned long long* __restrict__ cand) {
+  unsigned long long n_exact = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const unsigned long long e = cand[i];
     const int qi = (int)(e >> 32), pi = (int)(e & 0xffffffffull);
@@ -761,7 +786,22 @@ __global__ void __launch_bounds__(256) k_prefilter(TraverseArgs a, int64_t n, co
       X0[k] = geo::ld3(a.x0 + 3 * (int64_t)q[k]);
       X1[k] = geo::ld3(a.x1 + 3 * (int64_t)q[k]);
     }
-    if (geo::accd_class(a.kind, X0, X1, a.min_gap) != 1) {
+    bool cand_ok = true;
+    if (!a.exact_leaf) {
+      // the exact FP64 swept-box overlap the walk skipped: VF = vertex (pad 0)
+      // vs triangle (pad min_gap), EE = both edges (pad min_gap / 2)
+      double la[3], ha[3], lb[3], hb[3];
+      if (a.kind == 0) {
+        quad_box(X0, X1, 0, 1, 0.0, la, ha);
+        quad_box(X0, X1, 1, 3, a.min_gap, lb, hb);
+      } else {
+        quad_box(X0, X1, 0, 2, 0.5 * a.min_gap, la, ha);
+        quad_box(X0, X1, 2, 2, 0.5 * a.min_gap, lb, hb);
+      }
+      cand_ok = overlap(la, ha, lb, hb);
+      n_exact += cand_ok ? 1 : 0;
+    }
+    if (cand_ok && geo::accd_class(a.kind, X0, X1, a.min_gap) != 1) {
       const unsigned grp = __activemask();
       const int lane = threadIdx.x & 31;
       const int leader = __ffs(grp) - 1;
@@ -771,6 +811,7 @@ __global__ void __launch_bounds__(256) k_prefilter(TraverseArgs a, int64_t n, co
       a.out[base + __popc(grp & ((1u << lane) - 1u))] = e;
     }
   }
+  if (n_exact) atomicAdd(a.counters + 1, n_exact);
 }
 
 __global__ void k_pair_toi(int64_t n, int kind, const unsigned long long* __restrict__ pairs,
@@ -846,6 +887,10 @@ static int grid_for(int64_t n, int threads = 256) {
 // 15.7 vs 15.2 ms per CCD pass on the squishy press (the sort costs more)
 #ifndef IBF_CCD_VF_ORDER
 #define IBF_CCD_VF_ORDER 0
+#endif
+// exact leaf box test moved from the walk into k_prefilter (1) or kept in the walk (0)
+#ifndef IBF_CCD_DEFER_EXACT
+#define IBF_CCD_DEFER_EXACT 0
 #endif
 // 4-wide traversal records (1) or the binary packed records (0)
 #ifndef IBF_CCD_WIDE
@@ -1054,6 +1099,7 @@ static int broad_pass(ibf_ccd* c, int kind, const double* x0, const double* x1, 
     a.x1 = x1;
     a.min_gap = min_gap;
     a.filter = (filter && !split) ? 1 : 0;
+    a.exact_leaf = (split && IBF_CCD_DEFER_EXACT) ? 0 : 1;
     a.out = c->pairs.p;
     a.cap = c->pairs.cap;
     a.counters = c->counters.p;
@@ -1105,7 +1151,7 @@ static int broad_pass(ibf_ccd* c, int kind, const double* x0, const double* x1, 
   if (split && *count) {
     const int64_t n_all = *count;
     IBF_TRY(c->pairs2.reserve(n_all));
-    IBF_CUDA(cudaMemsetAsync(c->counters.p, 0, sizeof(unsigned long long), s));
+    IBF_CUDA(cudaMemsetAsync(c->counters.p, 0, (a.exact_leaf ? 1 : 2) * sizeof(unsigned long long), s));
     a.out = c->pairs2.p;
     a.cap = c->pairs2.cap;
     unsigned long long* h = (unsigned long long*)c->host.p;
@@ -1114,11 +1160,12 @@ static int broad_pass(ibf_ccd* c, int kind, const double* x0, const double* x1, 
       KernelClock kc(KC_PREFILTER, s, 200.0 * (double)n_all, 0.0, (double)n_all);
       k_prefilter<<<grid_for(n_all, 256), 256, 0, s>>>(a, n_all, c->pairs.p);
       IBF_LAUNCH_CHECK();
-      IBF_CUDA(cudaMemcpyAsync(h, c->counters.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+      IBF_CUDA(cudaMemcpyAsync(h, c->counters.p, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
       IBF_CUDA(cudaStreamSynchronize(s));
       kc.bytes += 8.0 * (double)h[0];
     }
     *count = (int64_t)h[0];
+    if (!a.exact_leaf) *n_candidates = (int64_t)h[1];   // the exact candidates (the walk counted float overlaps)
     unsorted = c->pairs2.p;
     tr.mark("prefilter", s, *count);
   }

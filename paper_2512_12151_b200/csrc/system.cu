@@ -628,11 +628,13 @@ __global__ void k_diag_max(int64_t n, const int* __restrict__ diag_q, const doub
 
 // ------------------------------------------------------------ host side
 
-// FP64 flops per tet of k_elem, frozen from ncu (2 x DFMA + DMUL + DADD
-// thread instructions per tet, COR model; profiles/).
-// The reference's own counter gives 927 multiplies per tet for the 10-block
-// PSD part alone (tests/test_elasticity.py:381-420).
-constexpr double kFlopPerTet = 0.0;
+// FP64 flops per tet of k_elem, frozen from ncu: 2 x DFMA + DMUL + DADD
+// thread instructions per tet = 2 x 1273.2 + 846.6 + 66.5 = 3459.5 on the
+// COR squishy-ball C4 assembly (profiles/r2v_k_elem_flops.json).  The
+// reference's own counter gives 927 multiplies per tet for the 10-block PSD
+// part alone (tests/test_elasticity.py:381-420); F, PK1, the rotation-variant
+// SVD and the eigensystem make up the rest.
+constexpr double kFlopPerTet = 3459.5;
 
 int system_assemble(ibf_system* s, ibf_contacts* c, const double* x_hat, const double* x_tilde, double mu,
                     double offset, double h, bool apply_dbc, double* grad, bool contacts_ready,

@@ -1,8 +1,10 @@
-O=gpurun_out/r2u; mkdir -p $O
-timeout 600 python bench.py > $O/bench.json 2> $O/bench.err
+O=gpurun_out/r2w; mkdir -p $O
+timeout 1200 python tools/long_parity.py c1 50 1e-15 > $O/c1_parity.log 2>&1 &
+P1=$!
+timeout 900 python -m pytest tests -m gpu -x -q -s -rA > $O/tests.log 2>&1
 timeout 500 python tools/squishy_run.py --frames 52 --plate-speed 2.0 --every 4 --dump /tmp/sq52.npz > $O/press.log 2>&1
-timeout 900 ncu --set full --import-source on --clock-control none --profile-from-start off -k regex:k_pcg -c 1 -o $O/k_pcg python tools/pcg_contact_bench.py --load /tmp/sq52.npz --frames 0 --iters 60 --ncu > $O/ncu_pcg.log 2>&1
-timeout 900 ncu --set full --import-source on --clock-control none --profile-from-start off -k regex:k_traverse -c 2 -o $O/k_traverse python tools/ccd_bench.py --load /tmp/sq52.npz --frames 0 --reps 2 --ncu > $O/ncu_trav.log 2>&1
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_elem -c 1 -o $O/k_elem python tools/pcg_contact_bench.py --load /tmp/sq52.npz --frames 0 --iters 5 > $O/ncu_elem.log 2>&1
-IBF_BENCH_PROFILE_RANGE=1 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv --log-file $O/launches_bench.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-certify > $O/bench_under_ncu.log 2>&1
-gzip -f $O/launches_bench.csv
+for v in base minb5 base2; do
+  L=""; [ $v = minb5 ] && L=tools/variants/libibf_minb5.so
+  IBF_LIB=$L timeout 300 python tools/pcg_contact_bench.py --load /tmp/sq52.npz --frames 0 --iters 200 > $O/pcg_$v.log 2>&1
+done
+wait $P1
