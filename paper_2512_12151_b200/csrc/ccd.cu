@@ -265,7 +265,8 @@ __device__ __forceinline__ int slot_last(int c, int nl, const int* __restrict__ 
 __global__ void k_refit_packed(int n, const unsigned long long* __restrict__ k, const double* __restrict__ plo,
                                const double* __restrict__ phi, const int* __restrict__ left,
                                const int* __restrict__ right, const int* __restrict__ parent,
-                               const int* __restrict__ last, int* __restrict__ flag, PackedNode* __restrict__ packed) {
+                               const int* __restrict__ last, int* __restrict__ flag, PackedNode* __restrict__ packed,
+                               double4* __restrict__ lbox) {
   const int nl = n - 1;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const int prim = (int)(k[i] & 0xffffffffull);
@@ -273,6 +274,11 @@ __global__ void k_refit_packed(int n, const unsigned long long* __restrict__ k, 
     {
       const double lo[3] = {plo[3 * prim], plo[3 * prim + 1], plo[3 * prim + 2]};
       const double hi[3] = {phi[3 * prim], phi[3 * prim + 1], phi[3 * prim + 2]};
+      if (lbox) {
+        // the exact leaf record in sorted-slot order: {lo, hi.x}, {hi.yz, prim, -}
+        lbox[2 * (size_t)i] = make_double4(lo[0], lo[1], lo[2], hi[0]);
+        lbox[2 * (size_t)i + 1] = make_double4(hi[1], hi[2], __longlong_as_double((long long)prim), 0.0);
+      }
       const int par = parent[node];
       pack_child(packed, par, left[par] == node, lo, hi);
     }
@@ -397,6 +403,7 @@ struct Tree {
   const double* hi;
   const PackedNode* packed;        // internal-node records (null: FP64 node arrays only)
   const WideNode* wide;            // 4-wide records of the even-depth internal nodes, or null
+  const double4* lbox;             // exact leaf records by sorted slot (2 double4 each), or null
   const double* plo;               // primitive boxes (exact leaf test with `packed`)
   const double* phi;
 };
@@ -731,9 +738,21 @@ __global__ void __launch_bounds__(128) k_traverse_wide(TraverseArgs a) {
       if (!h) continue;
       const int c = cid[k];
       if (c >= nl) {
-        const int pi = (int)(a.tree.keys[c - nl] & 0xffffffffull);
-        if (!a.exact_leaf || overlap(ql, qh, a.tree.plo + 3 * pi, a.tree.phi + 3 * pi))
-          traverse_leaf<FILTER>(a, SELF ? min(qi, pi) : qi, SELF ? max(qi, pi) : pi, n_cand);
+        int pi;
+        bool hit;
+        if (a.tree.lbox) {
+          // one 64-byte record per leaf, sibling leaves in adjacent slots
+          const double2* L = reinterpret_cast<const double2*>(a.tree.lbox + 2 * (size_t)(c - nl));
+          const double2 l0 = __ldg(L), l1 = __ldg(L + 1), l2 = __ldg(L + 2), l3 = __ldg(L + 3);
+          const double4 b0 = make_double4(l0.x, l0.y, l1.x, l1.y), b1 = make_double4(l2.x, l2.y, l3.x, l3.y);
+          pi = (int)__double_as_longlong(b1.z);
+          hit = !a.exact_leaf || (ql[0] <= b0.w && ql[1] <= b1.x && ql[2] <= b1.y && qh[0] >= b0.x &&
+                                  qh[1] >= b0.y && qh[2] >= b0.z);
+        } else {
+          pi = (int)(a.tree.keys[c - nl] & 0xffffffffull);
+          hit = !a.exact_leaf || overlap(ql, qh, a.tree.plo + 3 * pi, a.tree.phi + 3 * pi);
+        }
+        if (hit) traverse_leaf<FILTER>(a, SELF ? min(qi, pi) : qi, SELF ? max(qi, pi) : pi, n_cand);
       } else if (next < 0) {
         next = c;
       } else {
@@ -892,6 +911,11 @@ static int grid_for(int64_t n, int threads = 256) {
 #ifndef IBF_CCD_DEFER_EXACT
 #define IBF_CCD_DEFER_EXACT 0
 #endif
+// exact leaf boxes in sorted-slot records for the wide walk's leaf test (1),
+// or through the primitive index and the primitive box arrays (0)
+#ifndef IBF_CCD_LEAF_RECORDS
+#define IBF_CCD_LEAF_RECORDS 1
+#endif
 // 4-wide traversal records (1) or the binary packed records (0)
 #ifndef IBF_CCD_WIDE
 #define IBF_CCD_WIDE 1
@@ -913,6 +937,7 @@ static int build_tree(ibf_ccd* c, int64_t n, cudaStream_t s, Tree& t, ibf_ccd::T
   float4* packed4;
   WideNode* wide = nullptr;
   uint8_t* odd = nullptr;
+  double4* lbox = nullptr;
   bool refit_only = false;
   if (cache) {
     IBF_TRY(cache->keys_sorted.reserve(n));
@@ -931,6 +956,10 @@ static int build_tree(ibf_ccd* c, int64_t n, cudaStream_t s, Tree& t, ibf_ccd::T
       IBF_TRY(cache->odd.reserve(n - 1));
       wide = reinterpret_cast<WideNode*>(cache->wide.p);
       odd = cache->odd.p;
+      if (IBF_CCD_LEAF_RECORDS) {
+        IBF_TRY(cache->lbox.reserve(2 * (size_t)n));
+        lbox = cache->lbox.p;
+      }
     }
     refit_only = cache->n == n && cache->uses < IBF_CCD_REBUILD;
     keys_sorted = cache->keys_sorted.p;
@@ -953,6 +982,10 @@ static int build_tree(ibf_ccd* c, int64_t n, cudaStream_t s, Tree& t, ibf_ccd::T
       IBF_TRY(c->node_odd.reserve(n - 1));
       wide = reinterpret_cast<WideNode*>(c->node_wide.p);
       odd = c->node_odd.p;
+      if (IBF_CCD_LEAF_RECORDS) {
+        IBF_TRY(c->node_lbox.reserve(2 * (size_t)n));
+        lbox = c->node_lbox.p;
+      }
     }
     keys_sorted = c->keys_sorted.p;
     left = c->node_left.p, right = c->node_right.p, parent = c->node_parent.p, flag = c->node_flag.p;
@@ -991,7 +1024,7 @@ static int build_tree(ibf_ccd* c, int64_t n, cudaStream_t s, Tree& t, ibf_ccd::T
   IBF_CUDA(cudaMemsetAsync(flag, 0, nn * sizeof(int), s));
   if (packed && n > 1) {
     k_refit_packed<<<grid_for(n), 256, 0, s>>>((int)n, keys_sorted, c->box_lo.p, c->box_hi.p, left, right, parent,
-                                                last, flag, packed);
+                                                last, flag, packed, lbox);
   } else {
     if (cache && IBF_CCD_PACKED) {
       IBF_TRY(cache->lo.reserve(3 * nn));
@@ -1007,6 +1040,7 @@ static int build_tree(ibf_ccd* c, int64_t n, cudaStream_t s, Tree& t, ibf_ccd::T
     IBF_LAUNCH_CHECK();
   }
   t.wide = (packed && n > 1) ? wide : nullptr;
+  t.lbox = (packed && n > 1) ? lbox : nullptr;
   t.packed = n > 1 ? packed : nullptr;
   t.plo = c->box_lo.p;
   t.phi = c->box_hi.p;

@@ -280,6 +280,7 @@ struct ibf_ccd {
   ibf::DevBuf<float4> node_packed;                      // 4 per internal node (ccd.cu PackedNode)
   ibf::DevBuf<float4> node_wide;                        // 8 per internal node (ccd.cu WideNode)
   ibf::DevBuf<uint8_t> node_odd;
+  ibf::DevBuf<double4> node_lbox;
   // VF (triangle) and EE (edge) trees kept between calls: later calls refit
   // the cached topology to the new boxes; it is rebuilt every few calls
   struct TreeCache {
@@ -289,6 +290,7 @@ struct ibf_ccd {
     ibf::DevBuf<float4> packed;
     ibf::DevBuf<float4> wide;                            // 4-wide records (8 float4 per internal node)
     ibf::DevBuf<uint8_t> odd;                            // internal-node depth parity
+    ibf::DevBuf<double4> lbox;                           // exact leaf records by sorted slot
     int64_t n = -1;
     int uses = 0;
   } tc[2];

@@ -87,6 +87,12 @@ constexpr int PCG_SMEM_BYTES = IBF_PCG_SMEM_KB * 1024;
 #ifndef IBF_PCG_ZDOT
 #define IBF_PCG_ZDOT 0
 #endif
+// contact_dot_rec issues its 4 z gathers unconditionally, mask applied after (1;
+// measured equal, 225.3 vs 226.2 us per CG iteration, with a 28-byte spill), or
+// behind the mask (0)
+#ifndef IBF_PCG_DOT_UNCOND
+#define IBF_PCG_DOT_UNCOND 0
+#endif
 // contact dots g.p_k = g.z_k + beta g.p_{k-1} (z gathers only; contact_dot_rec)
 #ifndef IBF_PCG_DOT_REC
 #define IBF_PCG_DOT_REC 1
@@ -202,19 +208,45 @@ __device__ __forceinline__ void contact_dot(const Operator& op, const Gather& gp
 // iteration and after a restart: p_k = z_k).
 __device__ __forceinline__ void contact_dot_rec(const Operator& op, const DirGather& gd, int c, double* tprev) {
   const ContactView& cv = op.contact;
-  const int* q = cv.quad + 4 * c;
-  const double* g = cv.grad + 12 * c;
-  double acc = 0.0;
+#if !IBF_PCG_DOT_UNCOND
+  const int* qq = cv.quad + 4 * c;
+  const double* gg = cv.grad + 12 * c;
+  double acc0 = 0.0;
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    const int v = q[k];
-    if (op.mask && op.mask[v]) continue;
-    const double* Z = gd.z + 3 * (size_t)v;
-    acc += g[3 * k] * Z[0] + g[3 * k + 1] * Z[1] + g[3 * k + 2] * Z[2];
+    const int vv = qq[k];
+    if (op.mask && op.mask[vv]) continue;
+    const double* Z = gd.z + 3 * (size_t)vv;
+    acc0 += gg[3 * k] * Z[0] + gg[3 * k + 1] * Z[1] + gg[3 * k + 2] * Z[2];
   }
+  const double dot0 = gd.first ? acc0 : __fma_rn(gd.beta, tprev[c], acc0);
+  tprev[c] = dot0;
+  cv.t[c] = cv.coef[c] * dot0;
+#else
+  const int4 q = *reinterpret_cast<const int4*>(cv.quad + 4 * (size_t)c);
+  const int v[4] = {q.x, q.y, q.z, q.w};
+  const double* g = cv.grad + 12 * (size_t)c;
+  // the z gathers are issued unconditionally and masked slots dropped after
+  // (z is finite everywhere): the chain is quad -> (mask, z), not quad ->
+  // mask -> z
+  double z[4][3];
+  bool m[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const double* Z = gd.z + 3 * (size_t)v[k];
+    z[k][0] = Z[0];
+    z[k][1] = Z[1];
+    z[k][2] = Z[2];
+    m[k] = op.mask && op.mask[v[k]];
+  }
+  double acc = 0.0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if (!m[k]) acc += g[3 * k] * z[k][0] + g[3 * k + 1] * z[k][1] + g[3 * k + 2] * z[k][2];
   const double dot = gd.first ? acc : __fma_rn(gd.beta, tprev[c], acc);
   tprev[c] = dot;
   cv.t[c] = cv.coef[c] * dot;
+#endif
 }
 
 // friction term k: t_k = Hw_k sum_j w_j p_j over unmasked j
@@ -248,6 +280,9 @@ __device__ __forceinline__ void term_dots(const Operator& op, const Gather& gp, 
   if (contacts) {
     if constexpr (std::is_same<Gather, DirGather>::value) {
       if (tprev) {
+        // two constraints per step, all their loads issued before any use:
+        // the dot phase is a chain quad -> z gathers per constraint, and the
+        // ready counter holds every row with terms until it ends
         for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < op.contact.n; c += S) contact_dot_rec(op, gp, c, tprev);
         contacts = false;
       }
