@@ -246,6 +246,22 @@ int ibf_solve_subproblem(ibf_system* s, ibf_contacts* c, const double* x_tilde,
                          const double* x, double* x_hat, double mu, double offset, double h,
                          double cg_tol, double decay, double* result_host, ibf_stream st);
 
+/* The outer passes of Alg. 1 (intact/stepper.py:283-347) in native code:
+ * per pass solve_subproblem, ActiveSet.update with the previous pass's
+ * blocking pairs (none on the first pass), the NH inversion cap on x_hat - x
+ * (p_scratch: 3n doubles, or null when no region is NH), max_step_size with
+ * min_gap = 0.1 offset, clamp_state, the beta update from pass 1 on, and the
+ * stagnation escape (mu x2, offset /2 after 50 passes with alpha < 1e-4);
+ * stops when beta <= epsilon or after outer_cap passes.  x and x_hat are
+ * updated in place.  records_host: outer_cap x 6 doubles per pass (alpha,
+ * beta, constraints, newton iterations, CG iterations, wall ms).  out_host:
+ * (passes, terminated, mu, offset, stagnation triggers, blocking pairs of the
+ * last pass). */
+int ibf_outer_loop(ibf_system* s, ibf_contacts* c, ibf_ccd* ccd, const double* x_tilde, double* x,
+                   double* x_hat, double* p_scratch, double mu, double offset, double h, double cg_tol,
+                   double decay, double epsilon, int min_iterations, int outer_cap, double* records_host,
+                   double* out_host, ibf_stream st);
+
 /* ------------------------------------------------------- step glue kernels */
 /* x_tilde = x + h v + h^2 g (intact/stepper.py:263) */
 int ibf_inertia_target(int64_t n, const double* x, const double* v, double h,

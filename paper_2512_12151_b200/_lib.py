@@ -72,6 +72,8 @@ _PROTOS = {
     "ibf_solve_subproblem": (_int, [_vp, _vp, _vp, _vp, _vp, _dbl, _dbl, _dbl, _dbl, _dbl, _vp, _vp]),
     "ibf_inertia_target": (_int, [_i64, _vp, _vp, _dbl, _vp, _vp, _vp]),
     "ibf_clamp_state": (_int, [_i64, _vp, _vp, _dbl, _vp]),
+    "ibf_outer_loop": (_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _dbl, _dbl, _dbl, _dbl, _dbl, _dbl, _int, _int,
+                              _vp, _vp, _vp]),
     "ibf_velocity_update": (_int, [_i64, _vp, _vp, _dbl, _vp, _vp]),
     "ibf_bsr_create": (_int, [_i64, _i64, _vp, _vp, _vp, C.POINTER(_vp)]),
     "ibf_bsr_destroy": (None, [_vp]),
@@ -114,6 +116,8 @@ def lib():
                 "(there is no CPU fallback)")
         h = C.CDLL(LIB_PATH)
         for name, (res, args) in _PROTOS.items():
+            if os.environ.get("IBF_LIB") and not hasattr(h, name):
+                continue     # an older A/B build without this entry point
             fn = getattr(h, name)
             fn.restype = res
             fn.argtypes = args

@@ -253,6 +253,22 @@ __global__ void k_refit(int n, const unsigned long long* __restrict__ k, const d
   }
 }
 
+// The ids half of the leaf records: {prim | v0 << 32, v1 | v2 << 32} with the
+// primitive's vertex ids (-1 past its arity), so the walk's shared-vertex
+// test loads nothing.  Once per topology (the sorted order changes only on
+// a rebuild).
+__global__ void k_leaf_ids(int n, const unsigned long long* __restrict__ k, const int* __restrict__ prims, int arity,
+                           double4* __restrict__ lbox) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int prim = (int)(k[i] & 0xffffffffull);
+    int v[3] = {-1, -1, -1};
+    for (int j = 0; j < arity; ++j) v[j] = prims[arity * (size_t)prim + j];
+    const long long w0 = (long long)(unsigned)prim | ((long long)(unsigned)v[0] << 32);
+    const long long w1 = (long long)(unsigned)v[1] | ((long long)(unsigned)v[2] << 32);
+    reinterpret_cast<double2*>(lbox)[4 * (size_t)i + 3] = make_double2(__longlong_as_double(w0), __longlong_as_double(w1));
+  }
+}
+
 // Refit of the packed records alone (no FP64 node boxes): a leaf writes its
 // primitive's FP64 box rounded outward into its parent's record; the second
 // arrival at a node takes the union of the two float child boxes in its own
@@ -275,9 +291,10 @@ __global__ void k_refit_packed(int n, const unsigned long long* __restrict__ k, 
       const double lo[3] = {plo[3 * prim], plo[3 * prim + 1], plo[3 * prim + 2]};
       const double hi[3] = {phi[3 * prim], phi[3 * prim + 1], phi[3 * prim + 2]};
       if (lbox) {
-        // the exact leaf record in sorted-slot order: {lo, hi.x}, {hi.yz, prim, -}
+        // the exact leaf record in sorted-slot order: {lo, hi.x}, {hi.yz,
+        // ids}; the ids half is written once per topology (k_leaf_ids)
         lbox[2 * (size_t)i] = make_double4(lo[0], lo[1], lo[2], hi[0]);
-        lbox[2 * (size_t)i + 1] = make_double4(hi[1], hi[2], __longlong_as_double((long long)prim), 0.0);
+        reinterpret_cast<double2*>(lbox)[4 * (size_t)i + 2] = make_double2(hi[1], hi[2]);
       }
       const int par = parent[node];
       pack_child(packed, par, left[par] == node, lo, hi);
@@ -686,6 +703,7 @@ __global__ void __launch_bounds__(128) k_traverse_wide(TraverseArgs a) {
   int qi = 0;
   double ql[3], qh[3];
   float qlf[3], qhf[3];
+  int qv[3] = {-2, -2, -2};   // the query primitive's vertex ids (-2: none)
   int stack[100];
   int sp = 0, node = 0;
   while (true) {
@@ -714,6 +732,9 @@ __global__ void __launch_bounds__(128) k_traverse_wide(TraverseArgs a) {
           qlf[c] = __double2float_rd(ql[c]);
           qhf[c] = __double2float_ru(qh[c]);
         }
+        const int ar = a.kind == 0 ? 1 : (a.kind == 1 ? 2 : 3);
+#pragma unroll
+        for (int j = 0; j < 3; ++j) qv[j] = j < ar ? a.qprim[ar * (int64_t)qi + j] : -2;
         sp = 0;
         node = 0;
       }
@@ -745,9 +766,31 @@ __global__ void __launch_bounds__(128) k_traverse_wide(TraverseArgs a) {
           const double2* L = reinterpret_cast<const double2*>(a.tree.lbox + 2 * (size_t)(c - nl));
           const double2 l0 = __ldg(L), l1 = __ldg(L + 1), l2 = __ldg(L + 2), l3 = __ldg(L + 3);
           const double4 b0 = make_double4(l0.x, l0.y, l1.x, l1.y), b1 = make_double4(l2.x, l2.y, l3.x, l3.y);
-          pi = (int)__double_as_longlong(b1.z);
+          const long long w0 = __double_as_longlong(b1.z), w1 = __double_as_longlong(b1.w);
+          pi = (int)(w0 & 0xffffffffll);
           hit = !a.exact_leaf || (ql[0] <= b0.w && ql[1] <= b1.x && ql[2] <= b1.y && qh[0] >= b0.x &&
                                   qh[1] >= b0.y && qh[2] >= b0.z);
+          if (hit && !FILTER) {
+            // the candidate filter of make_quad on the ids in hand: no shared
+            // vertex (and, for self-queries, each pair once: done by the slot
+            // pruning); then the warp-aggregated append
+            const int tv0 = (int)(w0 >> 32), tv1 = (int)(w1 & 0xffffffffll), tv2 = (int)(w1 >> 32);
+            bool shared = false;
+#pragma unroll
+            for (int j = 0; j < 3; ++j) shared |= qv[j] >= 0 && (qv[j] == tv0 || qv[j] == tv1 || qv[j] == tv2);
+            if (!shared) {
+              ++n_cand;
+              const int lo_i = SELF ? min(qi, pi) : qi, hi_i = SELF ? max(qi, pi) : pi;
+              const unsigned grp = __activemask();
+              const int leader = __ffs(grp) - 1;
+              unsigned long long base = 0;
+              if (lane == leader) base = atomicAdd(a.counters, (unsigned long long)__popc(grp));
+              base = __shfl_sync(grp, base, leader);
+              const unsigned long long slot = base + __popc(grp & lt);
+              if (slot < a.cap) a.out[slot] = ((unsigned long long)lo_i << 32) | (unsigned long long)hi_i;
+            }
+            continue;
+          }
         } else {
           pi = (int)(a.tree.keys[c - nl] & 0xffffffffull);
           hit = !a.exact_leaf || overlap(ql, qh, a.tree.plo + 3 * pi, a.tree.phi + 3 * pi);
@@ -929,7 +972,8 @@ static int grid_for(int64_t n, int threads = 256) {
 #ifndef IBF_CCD_SPLIT
 #define IBF_CCD_SPLIT 1
 #endif
-static int build_tree(ibf_ccd* c, int64_t n, cudaStream_t s, Tree& t, ibf_ccd::TreeCache* cache = nullptr) {
+static int build_tree(ibf_ccd* c, int64_t n, cudaStream_t s, Tree& t, ibf_ccd::TreeCache* cache = nullptr,
+                      const int* prims = nullptr, int arity = 0) {
   const int64_t nn = std::max<int64_t>(2 * n - 1, 1);
   unsigned long long* keys_sorted = c->keys_sorted.p;
   int *left, *right, *parent, *flag, *last;
@@ -1014,6 +1058,10 @@ static int build_tree(ibf_ccd* c, int64_t n, cudaStream_t s, Tree& t, ibf_ccd::T
         k_depth_parity<<<grid_for(n - 1), 256, 0, s>>>((int)n, parent, odd);
         IBF_LAUNCH_CHECK();
       }
+      if (lbox && prims) {
+        k_leaf_ids<<<grid_for(n), 256, 0, s>>>((int)n, keys_sorted, prims, arity, lbox);
+        IBF_LAUNCH_CHECK();
+      }
     }
     if (cache) {
       cache->n = n;
@@ -1024,7 +1072,7 @@ static int build_tree(ibf_ccd* c, int64_t n, cudaStream_t s, Tree& t, ibf_ccd::T
   IBF_CUDA(cudaMemsetAsync(flag, 0, nn * sizeof(int), s));
   if (packed && n > 1) {
     k_refit_packed<<<grid_for(n), 256, 0, s>>>((int)n, keys_sorted, c->box_lo.p, c->box_hi.p, left, right, parent,
-                                                last, flag, packed, lbox);
+                                                last, flag, packed, prims ? lbox : nullptr);
   } else {
     if (cache && IBF_CCD_PACKED) {
       IBF_TRY(cache->lo.reserve(3 * nn));
@@ -1040,7 +1088,7 @@ static int build_tree(ibf_ccd* c, int64_t n, cudaStream_t s, Tree& t, ibf_ccd::T
     IBF_LAUNCH_CHECK();
   }
   t.wide = (packed && n > 1) ? wide : nullptr;
-  t.lbox = (packed && n > 1) ? lbox : nullptr;
+  t.lbox = (packed && n > 1 && prims) ? lbox : nullptr;
   t.packed = n > 1 ? packed : nullptr;
   t.plo = c->box_lo.p;
   t.phi = c->box_hi.p;
@@ -1087,7 +1135,8 @@ static int broad_pass(ibf_ccd* c, int kind, const double* x0, const double* x1, 
   }
   tr.mark("boxes", s, nt);
   Tree tree;
-  IBF_TRY(build_tree(c, nt, s, tree, (kind < 2 && IBF_CCD_REBUILD > 1) ? &c->tc[kind] : nullptr));
+  IBF_TRY(build_tree(c, nt, s, tree, (kind < 2 && IBF_CCD_REBUILD > 1) ? &c->tc[kind] : nullptr,
+                     kind == 1 ? c->edges.p : c->tris.p, kind == 1 ? 2 : 3));
   tr.mark("tree", s);
   // VF queries (surface vertices) in Morton order of their boxes, so the 32
   // walks of a warp follow nearly the same path (EE and TT self-queries use

@@ -521,6 +521,78 @@ __global__ void k_sub(int64_t n, const double* __restrict__ a, const double* __r
 }
 }  // namespace ibf
 
+// Alg. 1's outer passes (stepper._outer_loop, intact/stepper.py:283-347):
+// the same calls in the same order, the scalar logic in C++, so a pass costs
+// no Python round trips.  The scalar helpers mirror beta_update,
+// stagnation_advance and adaptive_mu (intact/stepper.py:178-213).
+extern "C" int ibf_outer_loop(ibf_system* s, ibf_contacts* c, ibf_ccd* ccd, const double* x_tilde, double* x,
+                              double* x_hat, double* p_scratch, double mu, double offset, double h, double cg_tol,
+                              double decay, double epsilon, int min_iterations, int outer_cap, double* records_host,
+                              double* out_host, ibf_stream st) {
+  if (!s || !c || !ccd || !x_tilde || !x || !x_hat || !records_host || !out_host || outer_cap < 0) {
+    set_error("ibf_outer_loop: bad arguments");
+    return IBF_ERR_BAD_ARG;
+  }
+  const int64_t n = s->n;
+  constexpr double kStagnationAlpha = 1e-4;   // stepper.STAGNATION_ALPHA
+  constexpr int kStagnationLimit = 50;         // stepper.STAGNATION_LIMIT
+  constexpr double kGapFraction = 0.1;         // stepper.CCD_GAP_FRACTION
+  double beta = 1.0;
+  int counter = 0, triggers = 0, passes = 0;
+  int64_t last_block = 0;
+  bool have_blocking = false, terminated = false;
+  for (int k = 0; k < outer_cap; ++k) {
+    const double t0 = wall_now();
+    double res[4];
+    IBF_TRY(ibf_solve_subproblem(s, c, x_tilde, x, x_hat, mu, offset, h, cg_tol, decay, res, st));
+    int64_t adm = 0, pr = 0;
+    if (have_blocking)
+      IBF_TRY(ibf_contacts_update(c, ccd, &adm, &pr, st));
+    else
+      IBF_TRY(ibf_contacts_update_host(c, 0, nullptr, nullptr, nullptr, &adm, &pr, st));
+    double cap = 1.0;
+    if (p_scratch) {
+      IBF_TRY(ibf_vec_sub(3 * n, x_hat, x, p_scratch, st));
+      double a_nh = 1.0;
+      IBF_TRY(ibf_inversion_safe_step(s, x, p_scratch, &a_nh, st));
+      cap = std::min(cap, a_nh);
+    }
+    double alpha = 0.0;
+    int64_t n_block = 0;
+    IBF_TRY(ibf_max_step_size(ccd, x, x_hat, kGapFraction * offset, cap, &alpha, &n_block, st));
+    last_block = n_block;
+    have_blocking = true;
+    IBF_TRY(ibf_clamp_state(n, x, x_hat, alpha, st));
+    if ((k - 1) + 1 >= min_iterations) beta = (1.0 - alpha) * beta;
+    double* r = records_host + 6 * (size_t)k;
+    r[0] = alpha;
+    r[1] = beta;
+    r[2] = (double)ibf_contacts_size(c);
+    r[3] = res[0];
+    r[4] = res[1];
+    r[5] = (wall_now() - t0) * 1e3;
+    passes = k + 1;
+    counter = alpha < kStagnationAlpha ? counter + 1 : 0;
+    if (counter >= kStagnationLimit) {
+      mu = 2.0 * mu;
+      offset = 0.5 * offset;
+      counter = 0;
+      ++triggers;
+    }
+    if (beta <= epsilon) {
+      terminated = true;
+      break;
+    }
+  }
+  out_host[0] = passes;
+  out_host[1] = terminated ? 1.0 : 0.0;
+  out_host[2] = mu;
+  out_host[3] = offset;
+  out_host[4] = triggers;
+  out_host[5] = (double)last_block;
+  return IBF_OK;
+}
+
 extern "C" int ibf_vec_sub(int64_t n, const double* a, const double* b, double* out, ibf_stream st) {
   ::ibf::StreamScope ibf_scope_((cudaStream_t)st);
   if (n <= 0) return IBF_OK;

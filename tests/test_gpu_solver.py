@@ -788,3 +788,43 @@ def test_partitioned_pcg_matches_unpartitioned(pkg, parts):
     assert n1 == n2 and abs(c1 - c2) <= n1
     assert dx <= 1e-9 * step
     assert np.array_equal(sa[3], sb[3])                        # gamma: same dual branches
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("scene", ["c5", "squishy"])
+def test_native_outer_loop_matches_python(pkg, scene, monkeypatch):
+    """Alg. 1's outer passes in native code (ibf_outer_loop) against the
+    Python loop over the same native calls (stepper._outer_loop,
+    intact/stepper.py:283-347): bit-identical states and identical per-pass
+    records (alpha, beta, constraints, Newton and CG counts) over several
+    frames of a C5 drop and of a reduced squishy-ball press."""
+    import torch
+    from paper_2512_12151_b200 import scenes
+    from paper_2512_12151_b200.contact import ActiveSet
+    from paper_2512_12151_b200.stepper import step_device
+    if scene == "c5":
+        system, state, params = scenes.c5_scene(3)
+        frames = 12
+    else:
+        system, state, params = scenes.squishy_scene(cell=0.01, n=12, stem=10, tip=6, plate_speed=2.0,
+                                                     plate_stop=0.16)
+        frames = 14
+    runs = []
+    for py in (False, True):
+        if py:
+            monkeypatch.setenv("IBF_PY_OUTER", "1")
+        else:
+            monkeypatch.delenv("IBF_PY_OUTER", raising=False)
+        aset = ActiveSet()
+        aset.ensure(system.n_vertices)
+        x = torch.from_numpy(state.x).cuda()
+        v = torch.from_numpy(state.v).cuda()
+        recs = []
+        for k in range(frames):
+            x, v, d = step_device(x, v, system, aset, params, step_index=k)
+            recs.append([(r.alpha, r.beta, r.n_constraints, r.newton_iters, r.cg_iters) for r in d.iterations])
+        runs.append((x.cpu().numpy(), v.cpu().numpy(), recs, len(aset)))
+    (xn, vn, rn, cn), (xp, vp, rp, cp) = runs
+    print(f"\n[native outer loop, {scene}] {frames} frames, passes {sum(len(r) for r in rn)}, constraints {cn}")
+    assert np.array_equal(xn, xp) and np.array_equal(vn, vp)
+    assert rn == rp and cn == cp
