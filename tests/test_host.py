@@ -139,3 +139,32 @@ def test_scene_generators_match_reference_primitives():
     system, state, params = scenes.c1_scene()
     assert sum(len(r.tets) for r in system.regions) == 4800 + 24
     assert params.min_iterations == 2
+
+
+def test_sell_numbering_is_a_padding_reducing_permutation():
+    """mesh.sell_numbering (the optional squishy-ball numbering):
+    a permutation of the vertices that keeps the mesh (same tets up to
+    renumbering) and lowers the sliced-ELL padding of the upper slots."""
+    import numpy as np
+    from paper_2512_12151_b200 import scenes
+    from paper_2512_12151_b200.mesh import reorder_for_sell, sell_numbering
+
+    ball = scenes.squishy_ball(n=8, shell=2, stem=4, tip=3, cell=0.02)
+    n = ball.n_verts
+    new_of = sell_numbering(n, ball.tets, window=128)
+    assert np.array_equal(np.sort(new_of), np.arange(n))
+
+    def upper_padding(tets):
+        pairs = np.concatenate([tets[:, [i, j]] for i in range(4) for j in range(i + 1, 4)])
+        key = np.unique(pairs.min(axis=1) * n + pairs.max(axis=1))
+        up = np.bincount(key // n, minlength=n) + 1
+        w = np.maximum.reduceat(up, np.arange(0, n, 32))
+        return 1.0 - up.sum() / (32.0 * w.sum())
+
+    re = reorder_for_sell(ball, window=128)
+    assert re.n_verts == n and re.n_tets == ball.n_tets
+    # same geometry: the renumbered positions are a permutation of the originals
+    perm = np.empty_like(new_of)
+    perm[new_of] = np.arange(n)
+    assert np.array_equal(re.rest_positions, ball.rest_positions[perm])
+    assert upper_padding(re.tets) < upper_padding(ball.tets)
