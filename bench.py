@@ -293,6 +293,19 @@ def run_reference_c5(args):
     print(json.dumps(line), flush=True)
 
 
+def _full_size_check():
+    """The committed one-off timing of the oracle's stages at the full C4
+    size against the same slice extrapolation (tools/oracle_full_stages.py):
+    how far the model is from a measurement, stage by stage."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r2_oracle_full_stages.json")) as f:
+            d = json.load(f)
+        return {"source": "profiles/r2_oracle_full_stages.json", "measured_full_s": d["measured_full_s"],
+                "extrapolated_over_measured": d["ratio_extrapolated_over_measured"]}
+    except Exception:
+        return None
+
+
 def run_reference(args):
     """--impl reference: the oracle port of the reference's CPU path (oracle/,
     single-threaded numpy like the reference), no GPU.  Each step times one
@@ -341,6 +354,7 @@ def run_reference(args):
             "sample_wall_s": {"mean": float(np.mean(walls)), "total": float(np.sum(walls))},
             "extrapolation": "ms/frame = sum over stages of (sample stage time x scene/sample size) x per-frame "
                              "op count; the sampled stage times are measured, the multiplication is the model",
+            "full_size_check": _full_size_check(),
             "spread_ms": {"min": float(np.min(vals)), "max": float(np.max(vals))}}
     print(json.dumps(line), flush=True)
 

@@ -594,7 +594,10 @@ __global__ void __launch_bounds__(128) k_traverse(TraverseArgs a) {
 // <= t is skipped (PackedNode.d.zw), which halves the walks, and the pair is
 // emitted in the canonical (smaller id, larger id) orientation the per-query
 // `qi < pi` test gave — the same set (intact/ccd.py:131-138).
-constexpr int TRAV_CHUNK = 64;
+#ifndef IBF_TRAV_CHUNK
+#define IBF_TRAV_CHUNK 32
+#endif
+constexpr int TRAV_CHUNK = IBF_TRAV_CHUNK;
 #ifndef IBF_CCD_PREFETCH
 #define IBF_CCD_PREFETCH 0
 #endif

@@ -211,9 +211,11 @@ def sell_numbering(n_verts: int, tets: np.ndarray, window: int = 1024, rounds: i
     return new_of
 
 
-def reorder_for_sell(mesh: TetMesh, window: int = 1024, rounds: int = 4) -> TetMesh:
+def reorder_for_sell(mesh: TetMesh, window: int = 0, rounds: int = 4) -> TetMesh:
     """The same mesh with its vertices renumbered by `sell_numbering`
-    (tets keep their order)."""
+    (tets keep their order).  window 0: IBF_SELL_NUMBERING_WINDOW or 1024."""
+    import os
+    window = window or int(os.environ.get("IBF_SELL_NUMBERING_WINDOW", "1024"))
     new_of = sell_numbering(mesh.n_verts, mesh.tets, window, rounds)
     perm = np.empty_like(new_of)
     perm[new_of] = np.arange(len(new_of))
