@@ -635,6 +635,10 @@ __global__ void k_diag_max(int64_t n, const int* __restrict__ diag_q, const doub
 // part alone (tests/test_elasticity.py:381-420); F, PK1, the rotation-variant
 // SVD and the eigensystem make up the rest.
 constexpr double kFlopPerTet = 3459.5;
+// FP64 flops per tet and trial point of k_energy's elastic part, frozen the
+// same way: 2 x 3.470e9 + 1.673e9 + 0.284e9 = 8.90e9 per launch of 2 trial
+// points over the 2.30M COR tets (profiles/r2ah_k_energy_flops.json)
+constexpr double kEnergyFlopPerTetPoint = 1937.0;
 
 int system_assemble(ibf_system* s, ibf_contacts* c, const double* x_hat, const double* x_tilde, double mu,
                     double offset, double h, bool apply_dbc, double* grad, bool contacts_ready,
@@ -750,7 +754,8 @@ int system_energy_launch(ibf_system* s, ibf_contacts* c, const double* x_hat, co
   {
     // algorithmic: 120 B/tet + x_hat, p, x_tilde, mass (80 B/vertex) + 232 B per
     // constraint, read once for all n_r trial points
-    KernelClock kc(KC_ENERGY, st, 120.0 * s->m + 80.0 * s->n + 232.0 * a.nc, 0.0, (double)n_r);
+    KernelClock kc(KC_ENERGY, st, 120.0 * s->m + 80.0 * s->n + 232.0 * a.nc,
+                   kEnergyFlopPerTetPoint * (double)s->m * n_r, (double)n_r);
     k_energy<<<a.bv + a.bt + a.bc + a.bf, 256, 0, st>>>(a);
     IBF_LAUNCH_CHECK();
   }
