@@ -87,6 +87,10 @@ constexpr int PCG_SMEM_BYTES = IBF_PCG_SMEM_KB * 1024;
 #ifndef IBF_PCG_ZDOT
 #define IBF_PCG_ZDOT 0
 #endif
+// materialise p_k behind a third grid barrier (1) or form it on the fly where gathered (0)
+#ifndef IBF_PCG_PMAT
+#define IBF_PCG_PMAT 0
+#endif
 // contact_dot_rec issues its 4 z gathers unconditionally, mask applied after (1;
 // measured equal, 225.3 vs 226.2 us per CG iteration, with a 28-byte spill), or
 // behind the mask (0)
@@ -973,6 +977,22 @@ __global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
       const DirGather gd{a.z, a.p[pb ^ 1], beta, first};
       double* pk = a.p[pb];
       PCG_PT(5)
+      // materialised direction (IBF_PCG_PMAT): p_k = z + beta p_{k-1} for the
+      // own rows, a grid barrier, then phase A gathers p_k alone
+      const bool pmat = IBF_PCG_PMAT && a.lanes == 1 && !a.n_chunks && !a.wdyn && !zmode && !qp_smem;
+      if (pmat) {
+        for (int k = 0; k < R; ++k) {
+          const int pos = row_of(k);
+          if (pos >= n) break;
+          const int i = row_at(op, pos);
+          double pv[3];
+          gd.get(i, pv[0], pv[1], pv[2]);
+          double* pki = pk + 3 * (size_t)i;
+          pki[0] = pv[0]; pki[1] = pv[1]; pki[2] = pv[2];
+        }
+        grid.sync();
+      }
+      const PlainGather gpk{pk};
       // ---- A: contact dots on p_k, then q = H p_k, pAp.  With the ready
       // counter, the CTAs holding term dots compute them first and count
       // themselves in; rows touching terms wait for the count just before
@@ -988,7 +1008,10 @@ __global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
       if ((op.contact.n && !zmode) || op.friction.n) {
         if (counted) {
           if (blockIdx.x < a.n_home) {
-            term_dots(op, gd, !zmode, a.tprev);
+            if (pmat)
+              term_dots(op, gpk, true);
+            else
+              term_dots(op, gd, !zmode, a.tprev);
             __syncthreads();
             if (threadIdx.x == 0) {
               __threadfence();
@@ -996,7 +1019,10 @@ __global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
             }
           }
         } else {
-          term_dots(op, gd, !zmode, a.tprev);
+          if (pmat)
+            term_dots(op, gpk, true);
+          else
+            term_dots(op, gd, !zmode, a.tprev);
           grid.sync();
         }
       }
@@ -1180,6 +1206,19 @@ __global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
             else
               row_product<DirGather, StoredTerms, false>(op, gd, pos, i, v);
             warp_terms_z(op.contact, pos & ~31, n, wbuf, first, beta, a.zdot, a.pdot, v[0], v[1], v[2]);
+          } else if (wterms && pmat) {
+            if (counted) {
+              row_product<PlainGather, CountedTerms, false>(op, gpk, pos, i, v, sterms);
+              warp_terms(op.contact, sterms, pos & ~31, n, wbuf, v[0], v[1], v[2]);
+            } else {
+              row_product<PlainGather, StoredTerms, false>(op, gpk, pos, i, v);
+              warp_terms(op.contact, StoredTerms(), pos & ~31, n, wbuf, v[0], v[1], v[2]);
+            }
+          } else if (pmat) {
+            if (counted)
+              row_product(op, gpk, pos, i, v, sterms);
+            else
+              row_product(op, gpk, pos, i, v);
           } else if (wterms) {
             if (counted) {
               row_product<DirGather, CountedTerms, false>(op, gd, pos, i, v, sterms);
@@ -1191,17 +1230,21 @@ __global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
           } else {
             product(pos, i, v);
           }
-          const double* Z = a.z + 3 * (size_t)i;
-          if (first) {
-            pv[0] = Z[0]; pv[1] = Z[1]; pv[2] = Z[2];
-          } else {
-            const double* P = gd.pold + 3 * (size_t)i;
-            pv[0] = cg_dir(beta, P[0], Z[0]);
-            pv[1] = cg_dir(beta, P[1], Z[1]);
-            pv[2] = cg_dir(beta, P[2], Z[2]);
-          }
           double* pki = pk + 3 * (size_t)i;
-          pki[0] = pv[0]; pki[1] = pv[1]; pki[2] = pv[2];
+          if (pmat) {
+            pv[0] = pki[0]; pv[1] = pki[1]; pv[2] = pki[2];
+          } else {
+            const double* Z = a.z + 3 * (size_t)i;
+            if (first) {
+              pv[0] = Z[0]; pv[1] = Z[1]; pv[2] = Z[2];
+            } else {
+              const double* P = gd.pold + 3 * (size_t)i;
+              pv[0] = cg_dir(beta, P[0], Z[0]);
+              pv[1] = cg_dir(beta, P[1], Z[1]);
+              pv[2] = cg_dir(beta, P[2], Z[2]);
+            }
+            pki[0] = pv[0]; pki[1] = pv[1]; pki[2] = pv[2];
+          }
           if (qp_smem) {
             for (int c = 0; c < 3; ++c) {
               sq[slot(k, c)] = v[c];
