@@ -89,7 +89,7 @@ constexpr int PCG_SMEM_BYTES = IBF_PCG_SMEM_KB * 1024;
 #endif
 // materialise p_k behind a third grid barrier (1) or form it on the fly where gathered (0)
 #ifndef IBF_PCG_PMAT
-#define IBF_PCG_PMAT 0
+#define IBF_PCG_PMAT 1
 #endif
 // contact_dot_rec issues its 4 z gathers unconditionally, mask applied after (1;
 // measured equal, 225.3 vs 226.2 us per CG iteration, with a 28-byte spill), or
@@ -844,6 +844,7 @@ struct PcgArgs {
   double* zdot;         // zdot mode (contacts without a dot phase): (C,4) g_c[slot] . z
   double* pdot;         // (C,4) each record's copy of g_c . p_{k-1}
   int zmode;
+  int pmat;             // materialised direction this solve (IBF_PCG_PMAT and enough contact terms)
   double* tprev;        // (C) g_c . p_{k-1} for the linear-recursion dots, or null
   int wdyn;             // warp-granular dynamic phase A (IBF_PCG_WARPDYN)
   int n_units, n_groups;
@@ -979,7 +980,7 @@ __global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
       PCG_PT(5)
       // materialised direction (IBF_PCG_PMAT): p_k = z + beta p_{k-1} for the
       // own rows, a grid barrier, then phase A gathers p_k alone
-      const bool pmat = IBF_PCG_PMAT && a.lanes == 1 && !a.n_chunks && !a.wdyn && !zmode && !qp_smem;
+      const bool pmat = IBF_PCG_PMAT && a.pmat && a.lanes == 1 && !a.n_chunks && !a.wdyn && !zmode && !qp_smem;
       if (pmat) {
         for (int k = 0; k < R; ++k) {
           const int pos = row_of(k);
@@ -1622,6 +1623,16 @@ int pcg_solve(const Operator& op, const double* rhs, double* x_out, double rel_t
                 ? 1
                 : 0;
   a.zdot = a.pdot = nullptr;
+  // The materialised direction pays a third grid barrier and saves the
+  // dot phase's second gather and the direction's on-the-fly registers:
+  // measured 220.0 vs 224.4 us per CG iteration at 0.35 contact terms per
+  // row and 192.5 vs 184.8 us without contacts, so it is taken from
+  // IBF_PCG_PMAT_RATIO (default 0.2) terms per row on.
+  {
+    const char* e = getenv("IBF_PCG_PMAT_RATIO");
+    const double ratio = e ? atof(e) : 0.2;
+    a.pmat = (IBF_PCG_PMAT && lanes == 1 && op.contact.n > 0 && (double)op.contact.n >= ratio * (double)n) ? 1 : 0;
+  }
   if (a.zmode) {
     const size_t nc4 = 4 * (size_t)op.contact.n;
     IBF_TRY(w.zdot.reserve(nc4));

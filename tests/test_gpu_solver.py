@@ -602,8 +602,8 @@ def _squishy_press_state(fric, min_constraints, max_frames=120):
     return system, params, aset, x, v, ft, k
 
 
-@pytest.mark.parametrize("fric", [0.0, 0.3])
-def test_production_pcg_path_subproblem_parity(pkg, fric):
+@pytest.mark.parametrize("fric,pmat", [(0.0, False), (0.3, False), (0.0, True)])
+def test_production_pcg_path_subproblem_parity(pkg, fric, pmat, monkeypatch):
     """The PCG configuration of the C4 bench — one thread per row, several
     row sweeps per thread with the last sweep dealt out by slices, residual
     carried on chip, split phase-B barrier, contact (and friction) dots behind
@@ -613,8 +613,11 @@ def test_production_pcg_path_subproblem_parity(pkg, fric):
     at 12 CTAs so each thread sweeps >= 4 rows.  Bars: equal Newton counts,
     CG counts within 2x the oracle's own spread under a 1e-15 input
     perturbation (or 2 %), positions within 4x that spread (or 1e-9 of the
-    step), identical gamma, multipliers within the propagated bound."""
+    step), identical gamma, multipliers within the propagated bound.  With
+    pmat the direction is materialised behind a third barrier (the C4 bench's
+    configuration at >= 0.2 contact terms per row)."""
     from oracle import friction as ofriction
+    monkeypatch.setenv("IBF_PCG_PMAT_RATIO", "0" if pmat else "1e9")
     from paper_2512_12151_b200 import _lib
     from paper_2512_12151_b200.device import to_dev, to_host
     system, params, aset, x, v, ft, frames = _squishy_press_state(fric, 5000)

@@ -1,4 +1,7 @@
-O=gpurun_out/r2ak; mkdir -p $O
-timeout 900 python bench.py --no-cpu-baseline > $O/bench_base.json 2> $O/bench_base.err
-IBF_LIB=tools/variants/libibf_pmat.so timeout 900 python bench.py --no-cpu-baseline > $O/bench_pmat.json 2> $O/bench_pmat.err
-timeout 900 python bench.py --no-cpu-baseline > $O/bench_base2.json 2> $O/bench_base2.err
+O=gpurun_out/r2al; mkdir -p $O
+timeout 1200 python -m pytest tests -m gpu -x -q -s -rA > $O/tests.log 2>&1
+timeout 500 python tools/squishy_run.py --frames 52 --plate-speed 2.0 --every 4 --dump /tmp/sq52.npz > $O/press.log 2>&1
+for v in base base2; do
+  timeout 300 python tools/pcg_contact_bench.py --load /tmp/sq52.npz --frames 0 --iters 200 > $O/pcg_$v.log 2>&1
+done
+timeout 900 python bench.py > $O/bench.json 2> $O/bench.err
