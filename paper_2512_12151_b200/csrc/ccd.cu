@@ -1259,10 +1259,13 @@ static int broad_pass(ibf_ccd* c, int kind, const double* x0, const double* x1, 
   IBF_TRY(c->pairs_sorted.reserve(std::max<int64_t>(cnt, 1)));
   if (cnt) {
     size_t need = 0;
-    cub::DeviceRadixSort::SortKeys(nullptr, need, unsorted, c->pairs_sorted.p, (int)cnt, 0, 64, s);
+    // keys are (query << 32) | primitive, query < nq: only the bits that can be set
+    int end_bit = 32;
+    while (end_bit < 64 && (1LL << (end_bit - 32)) < nq) ++end_bit;
+    cub::DeviceRadixSort::SortKeys(nullptr, need, unsorted, c->pairs_sorted.p, (int)cnt, 0, end_bit, s);
     IBF_TRY(c->cub_tmp.reserve(need + 16));
     size_t have = c->cub_tmp.cap;
-    IBF_CUDA(cub::DeviceRadixSort::SortKeys(c->cub_tmp.p, have, unsorted, c->pairs_sorted.p, (int)cnt, 0, 64, s));
+    IBF_CUDA(cub::DeviceRadixSort::SortKeys(c->cub_tmp.p, have, unsorted, c->pairs_sorted.p, (int)cnt, 0, end_bit, s));
   }
   tr.mark("sort", s, cnt);
   tr.mark("exit", s);
