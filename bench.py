@@ -379,6 +379,34 @@ def _kernel_rooflines(clocks, peak_hbm, peak_fp64):
     return out
 
 
+def _partition_probe(dev, system, state, params, part):
+    """One PCG solve of the scene's rest-state system through the NCCL
+    partition against the single-GPU kernel, before anything is timed: the
+    two must agree to 1e-10 (tests/test_gpu_solver.py holds the same bar for
+    local partitions); raises otherwise, and the caller falls back to
+    replicas."""
+    import torch
+    from paper_2512_12151_b200.device import empty
+    n, h = system.n_vertices, params.h
+    x = torch.from_numpy(state.x).cuda()
+    v = torch.from_numpy(state.v).cuda()
+    x_tilde = x + h * v
+    g = empty((n, 3))
+    dev.assemble(None, x, x_tilde, 1.0, params.offset, h, True, g)
+    rhs = -g
+    a, b = empty((n, 3)), empty((n, 3))
+    dev.set_dist(None)
+    it1, _, _ = dev.pcg(rhs, a, params.cg_tol)
+    dev.set_dist(part)
+    it2, _, _ = dev.pcg(rhs, b, params.cg_tol)
+    dev.set_dist(None)
+    torch.cuda.synchronize()
+    scale = float(a.abs().max()) or 1.0
+    err = float((a - b).abs().max()) / scale
+    if abs(it1 - it2) > 1 or not err <= 1e-10:
+        raise RuntimeError(f"partition probe: CG {it2} vs {it1}, max rel diff {err:.2e}")
+
+
 def run_ours(args):
     import torch
     ws, rank, local = _dist()
@@ -408,8 +436,10 @@ def run_ours(args):
             from paper_2512_12151_b200 import dist as pdist
             try:
                 part = pdist.Partition.from_torch()
+                _partition_probe(dev, system, state, params, part)
                 dev.set_dist(part)
-            except Exception as exc:      # no NCCL communicator: say so and run replicas
+            except Exception as exc:      # no working NCCL partition: say so and run replicas
+                dev.set_dist(None)
                 part, mode = None, f"replicas (partition unavailable: {exc})"[:200]
     aset = ActiveSet()
     aset.ensure(system.n_vertices)
