@@ -49,6 +49,10 @@ namespace ibf {
 #ifndef IBF_PCG_MINB
 #define IBF_PCG_MINB 4
 #endif
+// rows stop at their first padded slot / lower entry (1) or walk the slice's full width (0)
+#ifndef IBF_SELL_STOP
+#define IBF_SELL_STOP 0
+#endif
 #ifndef IBF_SPMV_UNROLL
 #define IBF_SPMV_UNROLL 2
 #endif
@@ -351,27 +355,33 @@ __device__ __forceinline__ void row_product(const Operator& op, const Gather& gp
   // storage by position (row_at maps positions to rows: internal.cuh); row i
   // for the contact incidences.  Padding slots are zero blocks whose column
   // is the position's own row, so they add exact zeros.
-  const int s = pos >> 5, lane = pos & 31;
+  const int s = pos >> SELL_SHIFT, lane = pos & (SELL_C - 1);
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
   {
-    const int q0 = __ldg(op.slice_ptr + s), w = (__ldg(op.slice_ptr + s + 1) - q0) >> 5;
+    const int q0 = __ldg(op.slice_ptr + s), w = (__ldg(op.slice_ptr + s + 1) - q0) >> SELL_SHIFT;
     const double* V = op.val + 9 * (size_t)q0 + QEL_LS * lane;
     const int* C = op.col + q0 + lane;
     int k = 0;
     if (IBF_SPMV_UNROLL >= 2) {
       // column indices are loaded one slot pair ahead, so the p gathers of a
       // pair never wait on an index load (the chain per pair is one level)
-      int n0 = w > 0 ? __ldg(C) : 0, n1 = w > 1 ? __ldg(C + 32) : 0;
+      int n0 = w > 0 ? __ldg(C) : 0, n1 = w > 1 ? __ldg(C + SELL_C) : 0;
       for (; k + 2 <= w; k += 2) {
         const int j0 = n0, j1 = n1;
-        if (k + 2 < w) n0 = __ldg(C + 32 * (k + 2));
-        if (k + 3 < w) n1 = __ldg(C + 32 * (k + 3));
-        const double* B = V + 288 * (size_t)k;
+        // IBF_SELL_STOP: a padded slot (col == own row past the diagonal
+        // slot) ends the row: its lane issues no more loads for the slice
+        if (IBF_SELL_STOP && k > 0 && j0 == i) {
+          k = w;
+          break;
+        }
+        if (k + 2 < w) n0 = __ldg(C + SELL_C * (k + 2));
+        if (k + 3 < w) n1 = __ldg(C + SELL_C * (k + 3));
+        const double* B = V + 9 * SELL_C * (size_t)k;
         double b[9], c[9];
 #pragma unroll
         for (int e = 0; e < 9; ++e) {
           b[e] = __ldg(B + QEL_ES * e);
-          c[e] = __ldg(B + 288 + QEL_ES * e);
+          c[e] = __ldg(B + 9 * SELL_C + QEL_ES * e);
         }
         double x0, x1, x2, y0, y1, y2;
         gp.get(j0, x0, x1, x2);
@@ -381,8 +391,9 @@ __device__ __forceinline__ void row_product(const Operator& op, const Gather& gp
       }
     }
     for (; k < w; ++k) {
-      const int j = __ldg(C + 32 * k);
-      const double* B = V + 288 * (size_t)k;
+      const int j = __ldg(C + SELL_C * k);
+      if (IBF_SELL_STOP && k > 0 && j == i) break;
+      const double* B = V + 9 * SELL_C * (size_t)k;
       double b[9];
 #pragma unroll
       for (int e = 0; e < 9; ++e) b[e] = __ldg(B + QEL_ES * e);
@@ -392,15 +403,19 @@ __device__ __forceinline__ void row_product(const Operator& op, const Gather& gp
     }
   }
   if (!IBF_DIAG_NO_LOWER) {
-    const int l0 = __ldg(op.low_ptr + s), w = (__ldg(op.low_ptr + s + 1) - l0) >> 5;
+    const int l0 = __ldg(op.low_ptr + s), w = (__ldg(op.low_ptr + s + 1) - l0) >> SELL_SHIFT;
     const int2* L = op.low + l0 + lane;
     int t = 0;
     if (IBF_SPMV_UNROLL >= 2) {
-      int2 n0 = w > 0 ? __ldg(L) : make_int2(0, 0), n1 = w > 1 ? __ldg(L + 32) : make_int2(0, 0);
+      int2 n0 = w > 0 ? __ldg(L) : make_int2(0, 0), n1 = w > 1 ? __ldg(L + SELL_C) : make_int2(0, 0);
       for (; t + 2 <= w; t += 2) {
         const int2 e0 = n0, e1 = n1;
-        if (t + 2 < w) n0 = __ldg(L + 32 * (t + 2));
-        if (t + 3 < w) n1 = __ldg(L + 32 * (t + 3));
+        if (IBF_SELL_STOP && e0.x == op.zero_q) {
+          t = w;
+          break;
+        }
+        if (t + 2 < w) n0 = __ldg(L + SELL_C * (t + 2));
+        if (t + 3 < w) n1 = __ldg(L + SELL_C * (t + 3));
         const double* B0 = op.val + qel(e0.x, 0);
         const double* B1 = op.val + qel(e1.x, 0);
         double b[9], c[9];
@@ -417,7 +432,8 @@ __device__ __forceinline__ void row_product(const Operator& op, const Gather& gp
       }
     }
     for (; t < w; ++t) {
-      const int2 le = __ldg(L + 32 * t);
+      const int2 le = __ldg(L + SELL_C * t);
+      if (IBF_SELL_STOP && le.x == op.zero_q) break;
       const double* B = op.val + qel(le.x, 0);
       double b[9];
 #pragma unroll
@@ -577,32 +593,32 @@ __device__ __forceinline__ void warp_terms_z(const ContactView& cv, int r0, int 
 template <class Gather, class Terms = StoredTerms>
 __device__ __forceinline__ void row_product_lanes(const Operator& op, const Gather& gp, int pos, int i, double y[3],
                                                   int sub, int L, const Terms& terms = Terms()) {
-  const int s = pos >> 5, lane = pos & 31;
+  const int s = pos >> SELL_SHIFT, lane = pos & (SELL_C - 1);
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
   {
-    const int q0 = __ldg(op.slice_ptr + s), w = (__ldg(op.slice_ptr + s + 1) - q0) >> 5;
-    const double* V = op.val + 9 * (size_t)q0 + lane;
+    const int q0 = __ldg(op.slice_ptr + s), w = (__ldg(op.slice_ptr + s + 1) - q0) >> SELL_SHIFT;
+    const double* V = op.val + 9 * (size_t)q0 + QEL_LS * lane;
     const int* C = op.col + q0 + lane;
     for (int k = sub; k < w; k += L) {
-      const int j = __ldg(C + 32 * k);
-      const double* B = V + 288 * (size_t)k;
+      const int j = __ldg(C + SELL_C * k);
+      const double* B = V + 9 * SELL_C * (size_t)k;
       double b[9];
 #pragma unroll
-      for (int e = 0; e < 9; ++e) b[e] = __ldg(B + 32 * e);
+      for (int e = 0; e < 9; ++e) b[e] = __ldg(B + QEL_ES * e);
       double x0, x1, x2;
       gp.get(j, x0, x1, x2);
       acc_upper(b, x0, x1, x2, a0, a1, a2);
     }
   }
   {
-    const int l0 = __ldg(op.low_ptr + s), w = (__ldg(op.low_ptr + s + 1) - l0) >> 5;
+    const int l0 = __ldg(op.low_ptr + s), w = (__ldg(op.low_ptr + s + 1) - l0) >> SELL_SHIFT;
     const int2* Lw = op.low + l0 + lane;
     for (int t = sub; t < w; t += L) {
-      const int2 le = __ldg(Lw + 32 * t);
+      const int2 le = __ldg(Lw + SELL_C * t);
       const double* B = op.val + qel(le.x, 0);
       double b[9];
 #pragma unroll
-      for (int e = 0; e < 9; ++e) b[e] = __ldg(B + 32 * e);
+      for (int e = 0; e < 9; ++e) b[e] = __ldg(B + QEL_ES * e);
       double x0, x1, x2;
       gp.get(le.y, x0, x1, x2);
       acc_lower(b, x0, x1, x2, a0, a1, a2);
@@ -776,7 +792,7 @@ int spmv(const Operator& op, const double* x, double* y, cudaStream_t s) {
   if (op.n == 0) return IBF_OK;
   static int tma = -1;
   if (tma < 0) tma = getenv("IBF_SPMV_TMA") ? atoi(getenv("IBF_SPMV_TMA")) : 0;
-  if (tma && !op.contact.n && !op.friction.n) {
+  if (tma && SELL_C == 32 && !op.contact.n && !op.friction.n) {
     // experimental (measured): TMA-staged upper stream
     const int grid = (int)std::min<int64_t>(div_up(op.n, 32 * TMA_WARPS), (int64_t)tma * sm_count());
     k_spmv_tma<<<grid, 32 * TMA_WARPS, 0, s>>>(op, x, y);
@@ -1741,7 +1757,7 @@ int SellPattern::build(int64_t n_, const std::vector<int64_t>& rows_, const std:
   rows = rows_;
   cols = cols_;
   nb = (int64_t)rows.size();
-  n_slices = (int)div_up(n, 32);
+  n_slices = (int)div_up(n, SELL_C);
   const int S = n_slices;
   // per-row upper counts and the transpose lists (source rows ascending)
   std::vector<int> up(n + 1, 0), lo(n + 1, 0);
@@ -1774,12 +1790,12 @@ int SellPattern::build(int64_t n_, const std::vector<int64_t>& rows_, const std:
   std::vector<int> sp(S + 1, 0), lp(S + 1, 0);
   for (int s = 0; s < S; ++s) {
     int w = 0, lw = 0;
-    for (int64_t p = 32LL * s; p < std::min<int64_t>(n, 32LL * s + 32); ++p) {
+    for (int64_t p = (int64_t)SELL_C * s; p < std::min<int64_t>(n, (int64_t)SELL_C * s + SELL_C); ++p) {
       w = std::max(w, ucount(perm_h[p]));
       lw = std::max(lw, lcount(perm_h[p]));
     }
-    sp[s + 1] = sp[s] + 32 * w;
-    lp[s + 1] = lp[s] + 32 * lw;
+    sp[s + 1] = sp[s] + SELL_C * w;
+    lp[s + 1] = lp[s] + SELL_C * lw;
   }
   nq = sp[S];
   nlq = lp[S];
@@ -1794,21 +1810,21 @@ int SellPattern::build(int64_t n_, const std::vector<int64_t>& rows_, const std:
   // padding: the position's own row (positions past n in the last slice keep
   // row/col 0, zero values)
   for (int s = 0; s < S; ++s) {
-    const int w = (sp[s + 1] - sp[s]) / 32;
+    const int w = (sp[s + 1] - sp[s]) / SELL_C;
     for (int k = 0; k < w; ++k)
-      for (int l = 0; l < 32; ++l) {
-        const int64_t p = 32LL * s + l;
-        const int64_t q = sp[s] + 32LL * k + l;
+      for (int l = 0; l < SELL_C; ++l) {
+        const int64_t p = (int64_t)SELL_C * s + l;
+        const int64_t q = sp[s] + (int64_t)SELL_C * k + l;
         qc[q] = qr[q] = (p < n) ? perm_h[p] : 0;
       }
   }
   q_of_b.assign(nb, 0);
   for (int64_t i = 0; i < n; ++i) {
     const int p = pos_of[i];
-    const int s = p >> 5, l = p & 31;
+    const int s = p >> SELL_SHIFT, l = p & (SELL_C - 1);
     for (int k = 0; k < ucount(i); ++k) {
       const int64_t b = up[i] + k;
-      const int q = sp[s] + 32 * k + l;
+      const int q = sp[s] + SELL_C * k + l;
       q_of_b[b] = q;
       qc[q] = (int)cols[b];
       qr[q] = (int)rows[b];
@@ -1820,11 +1836,11 @@ int SellPattern::build(int64_t n_, const std::vector<int64_t>& rows_, const std:
   // (=> source rows ascending); padding (zero block, own row)
   std::vector<int2> le(std::max<int64_t>(nlq, 1));
   for (int s = 0; s < S; ++s) {
-    const int w = (lp[s + 1] - lp[s]) / 32;
+    const int w = (lp[s + 1] - lp[s]) / SELL_C;
     for (int t = 0; t < w; ++t)
-      for (int l = 0; l < 32; ++l) {
-        const int64_t p = 32LL * s + l;
-        le[lp[s] + 32LL * t + l] = make_int2(zero_q, (p < n) ? perm_h[p] : 0);
+      for (int l = 0; l < SELL_C; ++l) {
+        const int64_t p = (int64_t)SELL_C * s + l;
+        le[lp[s] + (int64_t)SELL_C * t + l] = make_int2(zero_q, (p < n) ? perm_h[p] : 0);
       }
   }
   std::vector<int> fill(n, 0);
@@ -1832,9 +1848,9 @@ int SellPattern::build(int64_t n_, const std::vector<int64_t>& rows_, const std:
     if (rows[b] == cols[b]) continue;
     const int64_t j = cols[b];
     const int p = pos_of[j];
-    const int s = p >> 5, l = p & 31;
+    const int s = p >> SELL_SHIFT, l = p & (SELL_C - 1);
     const int t = fill[j]++;
-    le[lp[s] + 32LL * t + l] = make_int2(q_of_b[b], (int)rows[b]);
+    le[lp[s] + (int64_t)SELL_C * t + l] = make_int2(q_of_b[b], (int)rows[b]);
   }
   if (n > 0) IBF_TRY(perm.upload(perm_h.data(), perm_h.size()));
   IBF_TRY(slice_ptr.upload(sp.data(), sp.size()));
