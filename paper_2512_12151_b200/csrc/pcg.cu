@@ -51,7 +51,7 @@ namespace ibf {
 #endif
 // rows stop at their first padded slot / lower entry (1) or walk the slice's full width (0)
 #ifndef IBF_SELL_STOP
-#define IBF_SELL_STOP 0
+#define IBF_SELL_STOP 1
 #endif
 #ifndef IBF_SPMV_UNROLL
 #define IBF_SPMV_UNROLL 2
