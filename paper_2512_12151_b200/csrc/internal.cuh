@@ -52,7 +52,8 @@ struct ContactView {
 // is the maximum over: on the squishy balls the upper padding falls from 26 %
 // to 21 % and the lower from 29 % to 23 %, and k_pcg from 187 to 179 us per
 // CG iteration without contacts (C = 8: 184 us, the 64-byte segments cost L1
-// wavefronts).  The lower triangle is applied via a
+// wavefronts).  Once rows stop at their first padded slot (pcg.cu,
+// IBF_SELL_STOP) 16 and 32 measure the same; 16 builds without spills.  The lower triangle is applied via a
 // per-row list of (storage block, source row) entries stored the same way.
 // Padding blocks are zero with col = own row; padding lower entries point at
 // a zero block past the last slice.

@@ -1,4 +1,6 @@
-O=gpurun_out/r2at; mkdir -p $O
-timeout 1200 python -m pytest tests -m gpu -x -q -rA > $O/tests.log 2>&1
-timeout 900 python bench.py > $O/bench.json 2> $O/bench.err
-IBF_LIB=tools/variants/libibf_nostop.so timeout 900 python bench.py --no-cpu-baseline > $O/bench_nostop.json 2> $O/bench_nostop.err
+O=gpurun_out/r2au; mkdir -p $O
+timeout 500 python tools/squishy_run.py --frames 52 --plate-speed 2.0 --every 4 --dump /tmp/sq52.npz > $O/press.log 2>&1
+for v in base stopc32 stopc8 base2 stopc322; do
+  L=""; case $v in stopc32|stopc322) L=tools/variants/libibf_stopc32.so;; stopc8) L=tools/variants/libibf_stopc8.so;; esac
+  IBF_LIB=$L timeout 300 python tools/pcg_contact_bench.py --load /tmp/sq52.npz --frames 0 --iters 200 > $O/pcg_$v.log 2>&1
+done
