@@ -1640,14 +1640,17 @@ int pcg_solve(const Operator& op, const double* rhs, double* x_out, double rel_t
                 : 0;
   a.zdot = a.pdot = nullptr;
   // The materialised direction pays a third grid barrier and saves the
-  // dot phase's second gather and the direction's on-the-fly registers:
-  // measured 220.0 vs 224.4 us per CG iteration at 0.35 contact terms per
-  // row and 192.5 vs 184.8 us without contacts, so it is taken from
-  // IBF_PCG_PMAT_RATIO (default 0.2) terms per row on.
+  // dot phase's second gather and the direction's on-the-fly registers.
+  // Before rows stopped at their padding it paid off only under heavy
+  // contact (192.5 vs 184.8 us per CG iteration without contacts); with the
+  // row stop it wins at every contact load measured (167 vs 187 us at 0.05
+  // terms per row, 177 vs 196 at 0.15, 204 vs 227 at 0.37), so it is taken
+  // whenever there is one thread per row.  IBF_PCG_PMAT_RATIO (terms per
+  // row, default 0) keeps the on-the-fly direction below a given load.
   {
     const char* e = getenv("IBF_PCG_PMAT_RATIO");
-    const double ratio = e ? atof(e) : 0.2;
-    a.pmat = (IBF_PCG_PMAT && lanes == 1 && op.contact.n > 0 && (double)op.contact.n >= ratio * (double)n) ? 1 : 0;
+    const double ratio = e ? atof(e) : 0.0;
+    a.pmat = (IBF_PCG_PMAT && lanes == 1 && (double)op.contact.n >= ratio * (double)n) ? 1 : 0;
   }
   if (a.zmode) {
     const size_t nc4 = 4 * (size_t)op.contact.n;

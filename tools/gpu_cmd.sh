@@ -1,9 +1,8 @@
-O=gpurun_out/r2aw; mkdir -p $O
-timeout 500 python tools/squishy_run.py --frames 36 --plate-speed 2.0 --every 4 --dump /tmp/sq36.npz > $O/press36.log 2>&1
-timeout 500 python tools/squishy_run.py --load /tmp/sq36.npz --frames 6 --plate-speed 2.0 --every 1 --dump /tmp/sq42.npz > $O/press42.log 2>&1
-for st in sq36 sq42; do
-for v in on off on2 off2; do
-  R=1e9; case $v in on|on2) R=0;; esac
-  IBF_PCG_PMAT_RATIO=$R timeout 300 python tools/pcg_contact_bench.py --load /tmp/$st.npz --frames 0 --iters 200 > $O/pcg_${st}_$v.log 2>&1
+O=gpurun_out/r2ax; mkdir -p $O
+timeout 500 python tools/squishy_run.py --frames 52 --plate-speed 2.0 --every 4 --dump /tmp/sq52.npz > $O/press.log 2>&1
+for v in always ratio02 always2 ratio022; do
+  R=0; case $v in ratio02|ratio022) R=0.2;; esac
+  IBF_PCG_PMAT_RATIO=$R timeout 300 python tools/pcg_contact_bench.py --load /tmp/sq52.npz --frames 0 --iters 200 > $O/pcg_$v.log 2>&1
 done
-done
+timeout 1200 python -m pytest tests -m gpu -x -q -rA > $O/tests.log 2>&1
+timeout 900 python bench.py > $O/bench.json 2> $O/bench.err
