@@ -91,6 +91,11 @@ constexpr int PCG_SMEM_BYTES = IBF_PCG_SMEM_KB * 1024;
 #ifndef IBF_PCG_ZDOT
 #define IBF_PCG_ZDOT 0
 #endif
+// with the materialised direction, the term dots run in phase P before its barrier (1) or after it,
+// behind the ready counter (0): measured equal (203.7 vs 202.6 us per CG iteration at 331k contacts)
+#ifndef IBF_PCG_PMAT_DOTS
+#define IBF_PCG_PMAT_DOTS 0
+#endif
 // materialise p_k behind a third grid barrier (1) or form it on the fly where gathered (0)
 #ifndef IBF_PCG_PMAT
 #define IBF_PCG_PMAT 1
@@ -1007,6 +1012,10 @@ __global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
           double* pki = pk + 3 * (size_t)i;
           pki[0] = pv[0]; pki[1] = pv[1]; pki[2] = pv[2];
         }
+        // the term dots in the same phase, on the direction formed on the fly
+        // (they overlap the p_k stream); barrier P then makes them visible
+        // too, so phase A reads them without the ready counter
+        if (IBF_PCG_PMAT_DOTS && (op.contact.n || op.friction.n)) term_dots(op, gd, true, a.tprev);
         grid.sync();
       }
       const PlainGather gpk{pk};
@@ -1014,7 +1023,7 @@ __global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
       // counter, the CTAs holding term dots compute them first and count
       // themselves in; rows touching terms wait for the count just before
       // their term loop, instead of every CTA waiting at a grid barrier.
-      const bool counted = a.ready != nullptr;
+      const bool counted = a.ready != nullptr && !(pmat && IBF_PCG_PMAT_DOTS);
       const CountedTerms sterms{a.ready, (unsigned)it * a.n_home};
       auto product = [&](int pos, int i, double v[3]) {
         if (counted)
@@ -1022,7 +1031,7 @@ __global__ void __launch_bounds__(PCG_THREADS, IBF_PCG_MINB) k_pcg(PcgArgs a) {
         else
           row_product(op, gd, pos, i, v);
       };
-      if ((op.contact.n && !zmode) || op.friction.n) {
+      if (((op.contact.n && !zmode) || op.friction.n) && !(pmat && IBF_PCG_PMAT_DOTS)) {
         if (counted) {
           if (blockIdx.x < a.n_home) {
             if (pmat)

@@ -602,7 +602,7 @@ def _squishy_press_state(fric, min_constraints, max_frames=120):
     return system, params, aset, x, v, ft, k
 
 
-@pytest.mark.parametrize("fric,pmat", [(0.0, False), (0.3, False), (0.0, True)])
+@pytest.mark.parametrize("fric,pmat", [(0.0, False), (0.3, False), (0.0, True), (0.3, True)])
 def test_production_pcg_path_subproblem_parity(pkg, fric, pmat, monkeypatch):
     """The PCG configuration of the C4 bench — one thread per row, several
     row sweeps per thread with the last sweep dealt out by slices, residual
