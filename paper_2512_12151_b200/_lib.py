@@ -157,7 +157,7 @@ def stream():
 
 
 KERNEL_CLOCKS = ("k_elem", "k_gather_blocks", "k_vertex_rows", "k_energy", "k_traverse", "k_pair_toi", "k_pcg",
-                 "k_prefilter")
+                 "k_prefilter", "k_refit")
 
 
 def kernel_clocks(on=-1, reset=False):

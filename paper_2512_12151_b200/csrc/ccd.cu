@@ -152,7 +152,8 @@ __device__ __forceinline__ int delta(const unsigned long long* k, int n, int i, 
 
 // internal nodes 0..n-2, leaves n-1..2n-2 (leaf n-1+i holds sorted slot i)
 __global__ void k_build(int n, const unsigned long long* __restrict__ k, int* __restrict__ left,
-                        int* __restrict__ right, int* __restrict__ parent, int* __restrict__ last) {
+                        int* __restrict__ right, int* __restrict__ parent, int* __restrict__ last,
+                        int* __restrict__ first) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n - 1; i += gridDim.x * blockDim.x) {
     const int d = (delta(k, n, i, i + 1) - delta(k, n, i, i - 1)) >= 0 ? 1 : -1;
     const int dmin = delta(k, n, i, i - d);
@@ -179,6 +180,7 @@ __global__ void k_build(int n, const unsigned long long* __restrict__ k, int* __
     parent[lc] = i;
     parent[rc] = i;
     last[i] = max(i, j);   // the node covers sorted slots [min(i, j), max(i, j)]
+    if (first) first[i] = min(i, j);
   }
 }
 
@@ -304,6 +306,210 @@ __global__ void k_refit_packed(int n, const unsigned long long* __restrict__ k, 
     while (true) {
       const int old = atomicAdd(flag + node, 1);
       if (old == 0) break;  // first arrival: the sibling finishes this node
+      const int a = left[node], b = right[node];
+      const float* f = reinterpret_cast<const float*>(packed + node);
+      float lo[3], hi[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        lo[c] = fminf(__ldcg(f + c), __ldcg(f + 6 + c));
+        hi[c] = fmaxf(__ldcg(f + 3 + c), __ldcg(f + 9 + c));
+      }
+      packed[node].d = make_int4(a, b, slot_last(a, nl, last), slot_last(b, nl, last));
+      if (node == 0) break;
+      const int par = parent[node];
+      float* g = reinterpret_cast<float*>(packed + par) + (left[par] == node ? 0 : 6);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        g[c] = lo[c];
+        g[3 + c] = hi[c];
+      }
+      __threadfence();
+      node = par;
+    }
+  }
+}
+
+// Chunked treelet refit (IBF_CCD_REFIT_CAP = CAP > 0 threads per CTA).  A
+// Karras subtree covering the sorted slots [f, l] has its internal nodes
+// among the indices [f, l].  Once per topology, k_treelet_lists marks the
+// treelet roots (subtrees of <= S = CAP/4 leaves whose parent covers more)
+// and the single leaves hanging directly off a larger node; treelets and
+// such leaves tile [0, n) into contiguous units.  k_chunk_starts cuts the
+// slots into chunks at unit starts, one chunk every T = CAP - S slots
+// (snapped forward to the next unit start, so a chunk holds < CAP slots and
+// only whole treelets).  Per refit, k_refit_chunks does one chunk per CTA:
+// the topology of its slot range staged in shared memory, the same
+// bottom-up climb as k_refit_packed with the arrival counters and the
+// children's float boxes in shared memory (CTA-scope fences), every finished
+// record written to global memory once, and a treelet root's box written
+// into its parent's record.  k_refit_top then climbs the top part from the
+// treelet roots and single leaves with the device-scope protocol.  Every
+// record is a union of the same float boxes (fminf / fmaxf are exact), so
+// the records are bit-identical to k_refit_packed's.
+#ifndef IBF_CCD_REFIT_CAP
+#define IBF_CCD_REFIT_CAP 256
+#endif
+__global__ void k_treelet_lists(int n, const int* __restrict__ first, const int* __restrict__ last,
+                                const int* __restrict__ parent, int S, uint8_t* __restrict__ ucode,
+                                uint8_t* __restrict__ is_root, int* __restrict__ items, int* __restrict__ counts) {
+  const int nl = n - 1;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nl + n; i += gridDim.x * blockDim.x) {
+    const int sz = i < nl ? last[i] - first[i] + 1 : 1;
+    if (sz > S) continue;
+    if (i == 0) {  // the whole tree is one treelet
+      is_root[0] = 1;
+      ucode[0] = 1;
+      continue;
+    }
+    const int p = parent[i];
+    if (last[p] - first[p] + 1 <= S) continue;
+    if (i < nl) {
+      is_root[i] = 1;
+      ucode[first[i]] = 1;
+    } else {
+      ucode[i - nl] = 2;
+    }
+    items[atomicAdd(counts, 1)] = i;
+  }
+}
+
+__global__ void k_chunk_starts(int n, int T, int nchunks, const uint8_t* __restrict__ ucode,
+                               int* __restrict__ chunk) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c <= nchunks; c += gridDim.x * blockDim.x) {
+    int s = c == nchunks ? n : c * T;
+    while (s < n && ucode[s] == 0) ++s;
+    chunk[c] = s;
+  }
+}
+
+__device__ __forceinline__ void leaf_box(int slot, const unsigned long long* __restrict__ k,
+                                         const double* __restrict__ plo, const double* __restrict__ phi,
+                                         double4* __restrict__ lbox, double lo[3], double hi[3]) {
+  const int prim = (int)(k[slot] & 0xffffffffull);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    lo[c] = plo[3 * prim + c];
+    hi[c] = phi[3 * prim + c];
+  }
+  if (lbox) {
+    lbox[2 * (size_t)slot] = make_double4(lo[0], lo[1], lo[2], hi[0]);
+    reinterpret_cast<double2*>(lbox)[4 * (size_t)slot + 2] = make_double2(hi[1], hi[2]);
+  }
+}
+
+constexpr size_t refit_chunk_smem(int cap) { return (size_t)cap * (12 * sizeof(float) + 6 * sizeof(int) + 1); }
+
+template <int CAP>
+__global__ void __launch_bounds__(CAP) k_refit_chunks(int n, const unsigned long long* __restrict__ k,
+                                                      const double* __restrict__ plo, const double* __restrict__ phi,
+                                                      const int* __restrict__ left, const int* __restrict__ right,
+                                                      const int* __restrict__ parent, const int* __restrict__ last,
+                                                      const int* __restrict__ chunk,
+                                                      const uint8_t* __restrict__ ucode,
+                                                      const uint8_t* __restrict__ is_root,
+                                                      PackedNode* __restrict__ packed, double4* __restrict__ lbox) {
+  extern __shared__ float smem[];
+  float(*sb)[12] = reinterpret_cast<float(*)[12]>(smem);  // children's float boxes of internal node f + j
+  int* sflag = reinterpret_cast<int*>(smem + 12 * CAP);
+  int* sl = sflag + CAP;     // internal node f + j: children,
+  int* sr = sl + CAP;
+  int* sp = sr + CAP;        // parent,
+  int* slast = sp + CAP;     // last slot
+  int* slp = slast + CAP;    // parent of leaf slot f + j
+  uint8_t* sroot = reinterpret_cast<uint8_t*>(slp + CAP);
+  const int nl = n - 1;
+  const int f = chunk[blockIdx.x], m = chunk[blockIdx.x + 1] - f;
+  const int j = threadIdx.x;
+  uint8_t code = 0;
+  if (j < m) {
+    sflag[j] = 0;
+    if (f + j < nl) {
+      sl[j] = left[f + j];
+      sr[j] = right[f + j];
+      sp[j] = parent[f + j];
+      slast[j] = last[f + j];
+      sroot[j] = is_root[f + j];
+    }
+    slp[j] = parent[nl + f + j];
+    code = ucode[f + j];
+  }
+  __syncthreads();
+  if (j >= m) return;
+  const int slot = f + j;
+  double dlo[3], dhi[3];
+  leaf_box(slot, k, plo, phi, lbox, dlo, dhi);
+  int node = nl + slot;
+  int par = slp[j];
+  if (code == 2) {  // a single leaf under a top node
+    pack_child(packed, par, left[par] == node, dlo, dhi);
+    return;
+  }
+  {
+    volatile float* g = sb[par - f] + (sl[par - f] == node ? 0 : 6);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      g[c] = __double2float_rd(dlo[c]);
+      g[3 + c] = __double2float_ru(dhi[c]);
+    }
+  }
+  node = par;
+  while (true) {
+    const int q = node - f;
+    __threadfence_block();
+    if (atomicAdd(&sflag[q], 1) == 0) return;  // the sibling's thread finishes this node
+    __threadfence_block();
+    const volatile float* b = sb[q];
+    float v[12];
+#pragma unroll
+    for (int c = 0; c < 12; ++c) v[c] = b[c];
+    const int a = sl[q], bb = sr[q];
+    const int la = a >= nl ? a - nl : slast[a - f], lb = bb >= nl ? bb - nl : slast[bb - f];
+    packed[node].a = make_float4(v[0], v[1], v[2], v[3]);
+    packed[node].b = make_float4(v[4], v[5], v[6], v[7]);
+    packed[node].c = make_float4(v[8], v[9], v[10], v[11]);
+    packed[node].d = make_int4(a, bb, la, lb);
+    float lo[3], hi[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      lo[c] = fminf(v[c], v[6 + c]);
+      hi[c] = fmaxf(v[3 + c], v[9 + c]);
+    }
+    if (sroot[q]) {
+      if (node != 0) {
+        par = sp[q];
+        float* g = reinterpret_cast<float*>(packed + par) + (left[par] == node ? 0 : 6);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          g[c] = lo[c];
+          g[3 + c] = hi[c];
+        }
+      }
+      return;
+    }
+    par = sp[q];
+    volatile float* g = sb[par - f] + (sl[par - f] == node ? 0 : 6);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      g[c] = lo[c];
+      g[3 + c] = hi[c];
+    }
+    node = par;
+  }
+}
+
+// the top part: climbs from the treelet roots and single leaves, whose
+// boxes k_refit_chunks wrote into their parents' records
+__global__ void k_refit_top(int n, const int* __restrict__ left, const int* __restrict__ right,
+                            const int* __restrict__ parent, const int* __restrict__ last,
+                            const int* __restrict__ items, const int* __restrict__ counts, int* __restrict__ flag,
+                            PackedNode* __restrict__ packed) {
+  const int nl = n - 1;
+  const int nitems = counts[0];
+  for (int it = blockIdx.x * blockDim.x + threadIdx.x; it < nitems; it += gridDim.x * blockDim.x) {
+    int node = parent[items[it]];
+    while (true) {
+      const int old = atomicAdd(flag + node, 1);
+      if (old == 0) break;
       const int a = left[node], b = right[node];
       const float* f = reinterpret_cast<const float*>(packed + node);
       float lo[3], hi[3];
@@ -986,7 +1192,22 @@ static int build_tree(ibf_ccd* c, int64_t n, cudaStream_t s, Tree& t, ibf_ccd::T
   uint8_t* odd = nullptr;
   double4* lbox = nullptr;
   bool refit_only = false;
+  // chunked treelet refit (per-topology lists)
+  int *tfirst = nullptr, *titems = nullptr, *tcounts = nullptr, *tchunk = nullptr;
+  uint8_t *tucode = nullptr, *troot = nullptr;
+  constexpr int kCap = IBF_CCD_REFIT_CAP > 0 ? IBF_CCD_REFIT_CAP : 32, kS = kCap / 4, kT = kCap - kS;
+  const int nchunks = (int)((n + kT - 1) / kT);
   if (cache) {
+    if (IBF_CCD_REFIT_CAP > 0 && IBF_CCD_PACKED) {
+      IBF_TRY(cache->first.reserve(nn));
+      IBF_TRY(cache->titems.reserve(nn));
+      IBF_TRY(cache->tcounts.reserve(2));
+      IBF_TRY(cache->tchunk.reserve(nchunks + 1));
+      IBF_TRY(cache->tucode.reserve(n));
+      IBF_TRY(cache->troot.reserve(nn));
+      tfirst = cache->first.p, titems = cache->titems.p, tcounts = cache->tcounts.p, tchunk = cache->tchunk.p;
+      tucode = cache->tucode.p, troot = cache->troot.p;
+    }
     IBF_TRY(cache->keys_sorted.reserve(n));
     IBF_TRY(cache->left.reserve(nn));
     IBF_TRY(cache->right.reserve(nn));
@@ -1055,8 +1276,18 @@ static int build_tree(ibf_ccd* c, int64_t n, cudaStream_t s, Tree& t, ibf_ccd::T
     size_t have = c->cub_tmp.cap;
     IBF_CUDA(cub::DeviceRadixSort::SortKeys(c->cub_tmp.p, have, c->keys.p, keys_sorted, (int)n, 0, 64, s));
     if (n > 1) {
-      k_build<<<grid_for(n - 1), 256, 0, s>>>((int)n, keys_sorted, left, right, parent, last);
+      k_build<<<grid_for(n - 1), 256, 0, s>>>((int)n, keys_sorted, left, right, parent, last, tfirst);
       IBF_LAUNCH_CHECK();
+      if (tfirst) {
+        IBF_CUDA(cudaMemsetAsync(tcounts, 0, 2 * sizeof(int), s));
+        IBF_CUDA(cudaMemsetAsync(tucode, 0, n, s));
+        IBF_CUDA(cudaMemsetAsync(troot, 0, n - 1, s));
+        k_treelet_lists<<<grid_for(2 * n - 1), 256, 0, s>>>((int)n, tfirst, last, parent, kS, tucode, troot,
+                                                             titems, tcounts);
+        IBF_LAUNCH_CHECK();
+        k_chunk_starts<<<grid_for(nchunks + 1), 256, 0, s>>>((int)n, kT, nchunks, tucode, tchunk);
+        IBF_LAUNCH_CHECK();
+      }
       if (odd) {
         k_depth_parity<<<grid_for(n - 1), 256, 0, s>>>((int)n, parent, odd);
         IBF_LAUNCH_CHECK();
@@ -1073,7 +1304,19 @@ static int build_tree(ibf_ccd* c, int64_t n, cudaStream_t s, Tree& t, ibf_ccd::T
   }
   if (cache) ++cache->uses;
   IBF_CUDA(cudaMemsetAsync(flag, 0, nn * sizeof(int), s));
-  if (packed && n > 1) {
+  // algorithmic: per leaf the FP64 box and key in, the exact leaf record
+  // out; per internal node one 64-byte record out
+  {
+  KernelClock kcr(KC_REFIT, s, (packed && n > 1) ? 96.0 * n + 64.0 * (n - 1) : 0.0, 0.0, (double)n);
+  if (packed && n > 1 && tfirst) {
+    IBF_CUDA(cudaFuncSetAttribute(k_refit_chunks<kCap>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)refit_chunk_smem(kCap)));
+    k_refit_chunks<kCap><<<nchunks, kCap, refit_chunk_smem(kCap), s>>>(
+        (int)n, keys_sorted, c->box_lo.p, c->box_hi.p, left, right, parent, last, tchunk, tucode, troot, packed,
+        prims ? lbox : nullptr);
+    IBF_LAUNCH_CHECK();
+    k_refit_top<<<148 * 2, 256, 0, s>>>((int)n, left, right, parent, last, titems, tcounts, flag, packed);
+  } else if (packed && n > 1) {
     k_refit_packed<<<grid_for(n), 256, 0, s>>>((int)n, keys_sorted, c->box_lo.p, c->box_hi.p, left, right, parent,
                                                 last, flag, packed, prims ? lbox : nullptr);
   } else {
@@ -1086,6 +1329,7 @@ static int build_tree(ibf_ccd* c, int64_t n, cudaStream_t s, Tree& t, ibf_ccd::T
                                          lo, hi, nullptr);
   }
   IBF_LAUNCH_CHECK();
+  }
   if (wide && packed && n > 1) {
     k_widen<<<grid_for(n - 1), 256, 0, s>>>((int)n, odd, packed, wide);
     IBF_LAUNCH_CHECK();

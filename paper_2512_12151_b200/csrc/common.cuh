@@ -90,6 +90,7 @@ enum KernelClockId {
   KC_TOI,           // k_pair_toi: ACCD narrow phase on the survivors
   KC_PCG,           // k_pcg: one persistent PCG solve
   KC_PREFILTER,     // k_prefilter: ACCD prefilter over the broad-phase candidates
+  KC_REFIT,         // LBVH refit: k_refit_treelets + k_refit_top (or k_refit_packed)
   KC_COUNT
 };
 extern std::atomic<bool> g_kclock_on;

@@ -303,6 +303,8 @@ struct ibf_ccd {
     ibf::DevBuf<float4> wide;                            // 4-wide records (8 float4 per internal node)
     ibf::DevBuf<uint8_t> odd;                            // internal-node depth parity
     ibf::DevBuf<double4> lbox;                           // exact leaf records by sorted slot
+    ibf::DevBuf<int> first, titems, tcounts, tchunk;     // chunked treelet refit (per topology)
+    ibf::DevBuf<uint8_t> tucode, troot;
     int64_t n = -1;
     int uses = 0;
   } tc[2];

@@ -55,8 +55,35 @@ __device__ __forceinline__ int region_of(int t, const RegionDev* regs, int nreg)
 __device__ __forceinline__ size_t grad_tile_index(int64_t t, int l) {
   return (size_t)(t >> 5) * 384 + (size_t)(t & 31) * 12 + 3 * l;
 }
+// Staged element blocks: one 288-double tile per (32 tets, local pair q).
+// IBF_STAGE_SPLIT=1: the tile holds each lane's entries 0..7 as a 64-byte
+// run (lane*8), then entry 8 of all lanes (256 + lane), so a block is read
+// with two 256-bit loads and one 64-bit load; =0: 9 consecutive doubles
+// per lane (nine 64-bit loads).
+#ifndef IBF_STAGE_SPLIT
+#define IBF_STAGE_SPLIT 1
+#endif
 __device__ __forceinline__ size_t blk_tile_index(int64_t t, int q) {
-  return ((size_t)(t >> 5) * 10 + q) * 288 + (size_t)(t & 31) * 9;
+  return ((size_t)(t >> 5) * 10 + q) * 288 + (size_t)(t & 31) * (IBF_STAGE_SPLIT ? 8 : 9);
+}
+__device__ __forceinline__ double4 ld_nc_256(const double* p) {
+  double4 r;
+  asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w) : "l"(p));
+  return r;
+}
+// the 9 entries of the staged block of tet t, pair q
+__device__ __forceinline__ void load_staged_block(const double* __restrict__ elem_blk, int64_t t, int q,
+                                                  double v[9]) {
+  const double* K = elem_blk + blk_tile_index(t, q);
+  if (IBF_STAGE_SPLIT) {
+    const double4 a = ld_nc_256(K), b = ld_nc_256(K + 4);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+    v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    v[8] = __ldg(elem_blk + ((size_t)(t >> 5) * 10 + q) * 288 + 256 + (t & 31));
+  } else {
+#pragma unroll
+    for (int k = 0; k < 9; ++k) v[k] = __ldg(K + k);
+  }
 }
 
 // warp-cooperative coalesced store of `per` doubles per lane into a
@@ -71,6 +98,18 @@ __device__ __forceinline__ void warp_store_tile(double* sm, const double v[PER],
   for (int k = 0; k < PER; ++k) gtile[lane + 32 * k] = sm[lane + 32 * k];
   __syncwarp();
 }
+
+#ifndef IBF_GATHER_ILP
+#define IBF_GATHER_ILP 2
+#endif
+// timing-only diagnostics (wrong results): IBF_DIAG_ELEM_NOSTORE drops the
+// staging stores, IBF_DIAG_GATHER_L2 folds the staging reads onto 8,192 tets
+#ifndef IBF_DIAG_ELEM_NOSTORE
+#define IBF_DIAG_ELEM_NOSTORE 0
+#endif
+#ifndef IBF_DIAG_GATHER_L2
+#define IBF_DIAG_GATHER_L2 0
+#endif
 
 struct ElemArgs {
   int64_t m;
@@ -195,7 +234,30 @@ __global__ void __launch_bounds__(ELEM_THREADS, IBF_ELEM_MINB) k_elem(ElemArgs a
     } else {
       el::vertex_block(y[i], y[j], W, tw, fl, U, sc, K);
     }
-    warp_store_tile<9>(sm, K, a.elem_blk + ((size_t)(tile_t >> 5) * 10 + q) * 288);
+    if (IBF_DIAG_ELEM_NOSTORE) {
+      // timing-only bound: blocks computed but not staged
+      double sum = 0.0;
+#pragma unroll
+      for (int k = 0; k < 9; ++k) sum += K[k];
+      if (sum == 1.2345e300) a.elem_blk[t] = sum;
+    } else {
+      double* gt = a.elem_blk + ((size_t)(tile_t >> 5) * 10 + q) * 288;
+      if (IBF_STAGE_SPLIT) {
+        const int lane = threadIdx.x & 31;
+#pragma unroll
+        for (int k = 0; k < 9; ++k) sm[lane * 9 + k] = K[k];
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int j = lane + 32 * k;  // lane j>>3, entry j&7
+          gt[j] = sm[(j >> 3) * 9 + (j & 7)];
+        }
+        gt[256 + lane] = sm[lane * 9 + 8];
+        __syncwarp();
+      } else {
+        warp_store_tile<9>(sm, K, gt);
+      }
+    }
   }
 }
 
@@ -214,12 +276,33 @@ __global__ void k_gather_blocks(int64_t nq, const int* __restrict__ qrow, const 
     for (int k = 0; k < 9; ++k) acc[k] = (k == 0 || k == 4 || k == 8) ? m0 : 0.0;
     if (!(mask && (mask[r] || mask[c]))) {
       const int e0 = blk_ptr[q], e1 = blk_ptr[q + 1];
-      for (int e = e0; e < e1; ++e) {
-        const int src = blk_src[e];
-        const int t = src / 10, qq = src - 10 * (src / 10);
-        const double* K = elem_blk + blk_tile_index(t, qq);
+      int e = e0;
+      // IBF_GATHER_ILP contributions' loads in flight before their adds,
+      // which stay in tet order
+      for (; e + IBF_GATHER_ILP <= e1; e += IBF_GATHER_ILP) {
+        double v[IBF_GATHER_ILP][9];
 #pragma unroll
-        for (int k = 0; k < 9; ++k) acc[k] += K[k];
+        for (int u = 0; u < IBF_GATHER_ILP; ++u) {
+          const int src = blk_src[e + u];
+          int t = src / 10;
+          const int qq = src - 10 * t;
+          if (IBF_DIAG_GATHER_L2) t &= 8191;  // timing-only bound: staging L2-resident
+          load_staged_block(elem_blk, t, qq, v[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < IBF_GATHER_ILP; ++u)
+#pragma unroll
+          for (int k = 0; k < 9; ++k) acc[k] += v[u][k];
+      }
+      for (; e < e1; ++e) {
+        const int src = blk_src[e];
+        int t = src / 10;
+        const int qq = src - 10 * t;
+        if (IBF_DIAG_GATHER_L2) t &= 8191;
+        double v[9];
+        load_staged_block(elem_blk, t, qq, v);
+#pragma unroll
+        for (int k = 0; k < 9; ++k) acc[k] += v[k];
       }
     }
 #pragma unroll
@@ -656,11 +739,13 @@ int system_assemble(ibf_system* s, ibf_contacts* c, const double* x_hat, const d
   const uint8_t* mask = (apply_dbc && s->any_dbc) ? s->dbc.p : nullptr;
   // algorithmic: one 72 B write per stored block (N + E_u) — the staging
   // round trip k_elem -> k_gather_blocks is not algorithmic traffic
-  KernelClock kcg(KC_GATHER, st, 72.0 * s->pat.nb, 0.0, (double)s->pat.nb);
-  k_gather_blocks<<<(int)std::min<int64_t>(div_up(s->pat.nq, 256), 148LL * 32), 256, 0, st>>>(
-      s->pat.nq, s->pat.qrow.p, s->pat.col.p, s->pat.qreal.p, s->blk_ptr.p, s->blk_src.p, s->elem_blk.p,
-      s->masses.p, mask, s->pat.val.p);
-  IBF_LAUNCH_CHECK();
+  {
+    KernelClock kcg(KC_GATHER, st, 72.0 * s->pat.nb, 0.0, (double)s->pat.nb);
+    k_gather_blocks<<<(int)std::min<int64_t>(div_up(s->pat.nq, 256), 148LL * 32), 256, 0, st>>>(
+        s->pat.nq, s->pat.qrow.p, s->pat.col.p, s->pat.qreal.p, s->blk_ptr.p, s->blk_src.p, s->elem_blk.p,
+        s->masses.p, mask, s->pat.val.p);
+    IBF_LAUNCH_CHECK();
+  }
   ContactView cv;
   const double* coef_g = nullptr;
   if (c && c->n) {

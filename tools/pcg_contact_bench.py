@@ -110,6 +110,20 @@ for label, a in (("no_contacts", None), ("contacts", aset)):
         torch.cuda.profiler.stop()
     out[f"{label}_pcg_us_per_iter"] = 1e3 * e0.elapsed_time(e1) / max(it, 1)
     out[f"{label}_pcg_iters"] = it
+# assembly with the active set: whole call and per kernel (ibf_kernel_clocks)
+aset.refresh_anchors(x)
+for _ in range(2):
+    dev.assemble(aset, x, x_tilde, mu, params.offset, params.h, True, g)
+torch.cuda.synchronize()
+_lib.kernel_clocks(on=1, reset=True)
+e0.record()
+for _ in range(10):
+    dev.assemble(aset, x, x_tilde, mu, params.offset, params.h, True, g)
+e1.record()
+torch.cuda.synchronize()
+kc = _lib.kernel_clocks(on=0)
+out["assembly_ms"] = e0.elapsed_time(e1) / 10
+out["assembly_kernels_us"] = {k: round(1e3 * v["ms"] / max(v["launches"], 1), 1) for k, v in kc.items() if v["launches"]}
 out["spmv_bytes"] = dev.spmv_bytes()
 out["bytes_per_cg_iter"] = out["spmv_bytes"] + 288.0 * N
 out["contacts_GBps"] = out["bytes_per_cg_iter"] / out["contacts_pcg_us_per_iter"] / 1e3
