@@ -1,4 +1,3 @@
-O=gpurun_out/r2bi; mkdir -p $O
-timeout 900 python bench.py > $O/bench.json 2> $O/bench.err
-timeout 900 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.log 2>&1
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1
+O=gpurun_out/r2bj; mkdir -p $O
+timeout 500 python tools/squishy_run.py --frames 45 --plate-speed 2.0 --every 8 --dump /tmp/sq45.npz > $O/press.log 2>&1
+timeout 900 python tools/ccd_cache_sim.py --load /tmp/sq45.npz --frames 3 > $O/sim.log 2>&1
