@@ -1,3 +1,5 @@
-O=gpurun_out/r2bj; mkdir -p $O
-timeout 500 python tools/squishy_run.py --frames 45 --plate-speed 2.0 --every 8 --dump /tmp/sq45.npz > $O/press.log 2>&1
-timeout 900 python tools/ccd_cache_sim.py --load /tmp/sq45.npz --frames 3 > $O/sim.log 2>&1
+O=gpurun_out/r2bk; mkdir -p $O
+timeout 500 python tools/squishy_run.py --frames 48 --plate-speed 2.0 --every 8 --dump /tmp/sq48.npz > $O/press.log 2>&1
+for v in lb1 lb2 lb4 lb1 lb2 lb4; do
+  IBF_LIB=tools/variants/libibf_$v.so timeout 300 python tools/ccd_bench.py --load /tmp/sq48.npz --frames 0 --reps 10 >> $O/ccd_$v.log 2>&1
+done
