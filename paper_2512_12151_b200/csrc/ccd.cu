@@ -346,9 +346,6 @@ __global__ void k_refit_packed(int n, const unsigned long long* __restrict__ k, 
 // treelet roots and single leaves with the device-scope protocol.  Every
 // record is a union of the same float boxes (fminf / fmaxf are exact), so
 // the records are bit-identical to k_refit_packed's.
-#ifndef IBF_CCD_LEAF_BATCH
-#define IBF_CCD_LEAF_BATCH 2
-#endif
 #ifndef IBF_CCD_REFIT_CAP
 #define IBF_CCD_REFIT_CAP 256
 #endif
@@ -964,42 +961,19 @@ __global__ void __launch_bounds__(128) k_traverse_wide(TraverseArgs a) {
     const float Lx[4] = {lx.x, lx.y, lx.z, lx.w}, Ly[4] = {ly.x, ly.y, ly.z, ly.w}, Lz[4] = {lz.x, lz.y, lz.z, lz.w};
     const float Hx[4] = {hx.x, hx.y, hx.z, hx.w}, Hy[4] = {hy.x, hy.y, hy.z, hy.w}, Hz[4] = {hz.x, hz.y, hz.z, hz.w};
     int next = -1;
-    bool hk[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      hk[k] = overlap_f(qlf, qhf, Lx[k], Ly[k], Lz[k], Hx[k], Hy[k], Hz[k]);
-      if (SELF) hk[k] = hk[k] && cl[k] > t;
-    }
-    // IBF_CCD_LEAF_BATCH > 1: the leaf records of a group of overlapping
-    // leaf children are loaded together (independent loads in flight)
-    // before their tests, instead of one dependent round trip per leaf
-    constexpr int LB = (IBF_CCD_LEAF_BATCH > 1 && !FILTER) ? IBF_CCD_LEAF_BATCH : 1;
-    double2 lrec[LB][4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      if (LB > 1 && k % LB == 0 && a.tree.lbox) {
-#pragma unroll
-        for (int g = 0; g < LB; ++g)
-          if (hk[k + g] && cid[k + g] >= nl) {
-            const double2* L = reinterpret_cast<const double2*>(a.tree.lbox + 2 * (size_t)(cid[k + g] - nl));
-#pragma unroll
-            for (int u = 0; u < 4; ++u) lrec[g][u] = __ldg(L + u);
-          }
-      }
-      if (!hk[k]) continue;
+      bool h = overlap_f(qlf, qhf, Lx[k], Ly[k], Lz[k], Hx[k], Hy[k], Hz[k]);
+      if (SELF) h = h && cl[k] > t;
+      if (!h) continue;
       const int c = cid[k];
       if (c >= nl) {
         int pi;
         bool hit;
         if (a.tree.lbox) {
           // one 64-byte record per leaf, sibling leaves in adjacent slots
-          double2 l0, l1, l2, l3;
-          if (LB > 1) {
-            l0 = lrec[k % LB][0], l1 = lrec[k % LB][1], l2 = lrec[k % LB][2], l3 = lrec[k % LB][3];
-          } else {
-            const double2* L = reinterpret_cast<const double2*>(a.tree.lbox + 2 * (size_t)(c - nl));
-            l0 = __ldg(L), l1 = __ldg(L + 1), l2 = __ldg(L + 2), l3 = __ldg(L + 3);
-          }
+          const double2* L = reinterpret_cast<const double2*>(a.tree.lbox + 2 * (size_t)(c - nl));
+          const double2 l0 = __ldg(L), l1 = __ldg(L + 1), l2 = __ldg(L + 2), l3 = __ldg(L + 3);
           const double4 b0 = make_double4(l0.x, l0.y, l1.x, l1.y), b1 = make_double4(l2.x, l2.y, l3.x, l3.y);
           const long long w0 = __double_as_longlong(b1.z), w1 = __double_as_longlong(b1.w);
           pi = (int)(w0 & 0xffffffffll);
