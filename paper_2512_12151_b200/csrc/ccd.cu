@@ -346,6 +346,9 @@ __global__ void k_refit_packed(int n, const unsigned long long* __restrict__ k, 
 // treelet roots and single leaves with the device-scope protocol.  Every
 // record is a union of the same float boxes (fminf / fmaxf are exact), so
 // the records are bit-identical to k_refit_packed's.
+#ifndef IBF_CCD_TREELET_DIV
+#define IBF_CCD_TREELET_DIV 4  // treelets of at most CAP / DIV leaves
+#endif
 #ifndef IBF_CCD_REFIT_CAP
 #define IBF_CCD_REFIT_CAP 256
 #endif
@@ -1195,7 +1198,7 @@ static int build_tree(ibf_ccd* c, int64_t n, cudaStream_t s, Tree& t, ibf_ccd::T
   // chunked treelet refit (per-topology lists)
   int *tfirst = nullptr, *titems = nullptr, *tcounts = nullptr, *tchunk = nullptr;
   uint8_t *tucode = nullptr, *troot = nullptr;
-  constexpr int kCap = IBF_CCD_REFIT_CAP > 0 ? IBF_CCD_REFIT_CAP : 32, kS = kCap / 4, kT = kCap - kS;
+  constexpr int kCap = IBF_CCD_REFIT_CAP > 0 ? IBF_CCD_REFIT_CAP : 32, kS = kCap / IBF_CCD_TREELET_DIV, kT = kCap - kS;
   const int nchunks = (int)((n + kT - 1) / kT);
   if (cache) {
     if (IBF_CCD_REFIT_CAP > 0 && IBF_CCD_PACKED) {
