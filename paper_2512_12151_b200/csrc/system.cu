@@ -449,7 +449,15 @@ __device__ __forceinline__ double trial_coord(const EnergyArgs& a, double r, int
   return a.p ? __dadd_rn(a.xh[k], __dmul_rn(r, a.p[k])) : a.xh[k];
 }
 
-__global__ void __launch_bounds__(256) k_energy(EnergyArgs a) {
+#ifndef IBF_ENERGY_MINB
+#define IBF_ENERGY_MINB 3  // 0: the compiler's register choice for 256 threads (128)
+#endif
+#if IBF_ENERGY_MINB > 0
+#define IBF_ENERGY_BOUNDS __launch_bounds__(256, IBF_ENERGY_MINB)
+#else
+#define IBF_ENERGY_BOUNDS __launch_bounds__(256)
+#endif
+__global__ void IBF_ENERGY_BOUNDS k_energy(EnergyArgs a) {
   __shared__ double red[8];
   double acc[MAXT];
 #pragma unroll
