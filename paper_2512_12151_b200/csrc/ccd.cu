@@ -346,6 +346,14 @@ __global__ void k_refit_packed(int n, const unsigned long long* __restrict__ k, 
 // treelet roots and single leaves with the device-scope protocol.  Every
 // record is a union of the same float boxes (fminf / fmaxf are exact), so
 // the records are bit-identical to k_refit_packed's.
+#ifndef IBF_TRAV_MINB
+#define IBF_TRAV_MINB 0  // 0: the compiler's register choice for 128 threads
+#endif
+#if IBF_TRAV_MINB > 0
+#define IBF_TRAV_BOUNDS __launch_bounds__(128, IBF_TRAV_MINB)
+#else
+#define IBF_TRAV_BOUNDS __launch_bounds__(128)
+#endif
 #ifndef IBF_CCD_TREELET_DIV
 #define IBF_CCD_TREELET_DIV 4  // treelets of at most CAP / DIV leaves
 #endif
@@ -903,7 +911,7 @@ __global__ void __launch_bounds__(128) k_traverse_dyn(TraverseArgs a) {
 // k_traverse_dyn over the 4-wide records: same query fetching, slot pruning
 // and leaf handling; up to three internal children are pushed per step.
 template <bool FILTER, bool SELF>
-__global__ void __launch_bounds__(128) k_traverse_wide(TraverseArgs a) {
+__global__ void IBF_TRAV_BOUNDS k_traverse_wide(TraverseArgs a) {
   const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
   const int nl = a.tree.n - 1;
@@ -1450,11 +1458,9 @@ static int broad_pass(ibf_ccd* c, int kind, const double* x0, const double* x1, 
         if (tree.wide)
           kern = a.filter ? (self ? k_traverse_wide<true, true> : k_traverse_wide<true, false>)
                           : (self ? k_traverse_wide<false, true> : k_traverse_wide<false, false>);
-        static int blocks_per_sm = 0;
-        if (!blocks_per_sm) {
-          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_traverse_dyn<false, true>, 128, 0);
-          blocks_per_sm = std::max(blocks_per_sm, 1);
-        }
+        int blocks_per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, 128, 0);
+        blocks_per_sm = std::max(blocks_per_sm, 1);
         const int64_t want = div_up(nq, 128);
         kern<<<(int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)blocks_per_sm * sm_count())), 128, 0, s>>>(a);
       } else {
