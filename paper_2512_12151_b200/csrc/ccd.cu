@@ -354,6 +354,22 @@ __global__ void k_refit_packed(int n, const unsigned long long* __restrict__ k, 
 #else
 #define IBF_TRAV_BOUNDS __launch_bounds__(128)
 #endif
+#ifndef IBF_PREFILTER_MINB
+#define IBF_PREFILTER_MINB 3
+#endif
+#if IBF_PREFILTER_MINB > 0
+#define IBF_PREFILTER_BOUNDS __launch_bounds__(256, IBF_PREFILTER_MINB)
+#else
+#define IBF_PREFILTER_BOUNDS __launch_bounds__(256)
+#endif
+#ifndef IBF_TOI_MINB
+#define IBF_TOI_MINB 3
+#endif
+#if IBF_TOI_MINB > 0
+#define IBF_TOI_BOUNDS __launch_bounds__(256, IBF_TOI_MINB)
+#else
+#define IBF_TOI_BOUNDS
+#endif
 #ifndef IBF_CCD_TREELET_DIV
 #define IBF_CCD_TREELET_DIV 4  // treelets of at most CAP / DIV leaves
 #endif
@@ -1056,7 +1072,7 @@ __device__ __forceinline__ void quad_box(const V3* X0, const V3* X1, int k0, int
   }
 }
 
-__global__ void __launch_bounds__(256) k_prefilter(TraverseArgs a, int64_t n, const unsigned long long* __restrict__ cand) {
+__global__ void IBF_PREFILTER_BOUNDS k_prefilter(TraverseArgs a, int64_t n, const unsigned long long* __restrict__ cand) {
   unsigned long long n_exact = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const unsigned long long e = cand[i];
@@ -1096,7 +1112,7 @@ __global__ void __launch_bounds__(256) k_prefilter(TraverseArgs a, int64_t n, co
   if (n_exact) atomicAdd(a.counters + 1, n_exact);
 }
 
-__global__ void k_pair_toi(int64_t n, int kind, const unsigned long long* __restrict__ pairs,
+__global__ void IBF_TOI_BOUNDS k_pair_toi(int64_t n, int kind, const unsigned long long* __restrict__ pairs,
                            const int* __restrict__ qprim, const int* __restrict__ tprim,
                            const double* __restrict__ x0, const double* __restrict__ x1, double min_gap,
                            double* __restrict__ toi, int* __restrict__ quad_out) {
