@@ -1,7 +1,7 @@
-O=gpurun_out/r2br; mkdir -p $O
+O=gpurun_out/r2bs; mkdir -p $O
+timeout 500 python tools/squishy_run.py --frames 48 --plate-speed 2.0 --every 8 --dump /tmp/sq48.npz > $O/press.log 2>&1
+for v in r1 main r4 r1 main r4; do
+  if [ $v = main ]; then L=""; else L=tools/variants/libibf_$v.so; fi
+  IBF_LIB=$L timeout 300 python tools/pcg_contact_bench.py --load /tmp/sq48.npz --frames 0 --iters 50 >> $O/asm_$v.log 2>&1
+done
 timeout 900 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.log 2>&1
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1
-timeout 900 python bench.py > $O/bench.json 2> $O/bench.err
-timeout 900 python bench.py > $O/bench2.json 2> $O/bench2.err
-IBF_BENCH_PROFILE_RANGE=1 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv --log-file $O/launches_bench.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-certify > $O/bench_under_ncu.log 2>&1
-gzip -f $O/launches_bench.csv
