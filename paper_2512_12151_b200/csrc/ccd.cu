@@ -22,6 +22,7 @@
 // (intact/ccd.py:64-68).  The traversal evaluates that test in place and
 // appends only the survivors (usually a tiny fraction), which are then sorted
 // (deterministic order) and advanced by one thread each.
+#include <mutex>
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -1336,8 +1337,13 @@ static int build_tree(ibf_ccd* c, int64_t n, cudaStream_t s, Tree& t, ibf_ccd::T
   {
   KernelClock kcr(KC_REFIT, s, (packed && n > 1) ? 96.0 * n + 64.0 * (n - 1) : 0.0, 0.0, (double)n);
   if (packed && n > 1 && tfirst) {
-    IBF_CUDA(cudaFuncSetAttribute(k_refit_chunks<kCap>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)refit_chunk_smem(kCap)));
+    if (refit_chunk_smem(kCap) > 48 * 1024) {
+      static std::once_flag smem_once;
+      std::call_once(smem_once, [] {
+        cudaFuncSetAttribute(k_refit_chunks<kCap>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)refit_chunk_smem(kCap));
+      });
+    }
     k_refit_chunks<kCap><<<nchunks, kCap, refit_chunk_smem(kCap), s>>>(
         (int)n, keys_sorted, c->box_lo.p, c->box_hi.p, left, right, parent, last, tchunk, tucode, troot, packed,
         prims ? lbox : nullptr);
