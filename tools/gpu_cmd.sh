@@ -1,3 +1,4 @@
-O=gpurun_out/r2bu; mkdir -p $O
-timeout 600 python bench.py --workload c5 --steps 10 --warmup 2 --no-cpu-baseline --concurrency 8 > $O/c5_k8.json 2> $O/c5_k8.err
-timeout 600 python bench.py --workload c5 --steps 10 --warmup 2 --no-cpu-baseline --concurrency 1 > $O/c5_k1.json 2> $O/c5_k1.err
+O=gpurun_out/r2bv; mkdir -p $O
+timeout 900 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.log 2>&1
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1
+timeout 900 python bench.py > $O/bench.json 2> $O/bench.err
