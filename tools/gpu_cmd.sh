@@ -1,4 +1,2 @@
-O=gpurun_out/r2bv; mkdir -p $O
-timeout 900 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.log 2>&1
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1
-timeout 900 python bench.py > $O/bench.json 2> $O/bench.err
+O=gpurun_out/r2bw; mkdir -p $O
+timeout 1500 python tools/squishy_run.py --frames 120 --plate-speed 2.0 --certify --every 5 --out $O/press120.json > $O/press.log 2>&1
