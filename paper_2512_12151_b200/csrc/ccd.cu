@@ -1400,8 +1400,6 @@ static int broad_pass(ibf_ccd* c, int kind, const double* x0, const double* x1, 
     // static triangle boxes (intact/intersect.py:129-131), queried against themselves
     k_swept_boxes<3><<<grid_for(nt), 256, 0, s>>>(nt, c->tris.p, x0, x1, 0.0, c->box_lo.p, c->box_hi.p);
     IBF_LAUNCH_CHECK();
-    IBF_CUDA(cudaMemcpyAsync(c->qlo.p, c->box_lo.p, 3 * nt * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    IBF_CUDA(cudaMemcpyAsync(c->qhi.p, c->box_hi.p, 3 * nt * sizeof(double), cudaMemcpyDeviceToDevice, s));
   } else if (kind == 0) {
     k_swept_boxes<3><<<grid_for(nt), 256, 0, s>>>(nt, c->tris.p, x0, x1, min_gap, c->box_lo.p, c->box_hi.p);
     IBF_LAUNCH_CHECK();
@@ -1410,8 +1408,6 @@ static int broad_pass(ibf_ccd* c, int kind, const double* x0, const double* x1, 
   } else {
     k_swept_boxes<2><<<grid_for(nt), 256, 0, s>>>(nt, c->edges.p, x0, x1, 0.5 * min_gap, c->box_lo.p, c->box_hi.p);
     IBF_LAUNCH_CHECK();
-    IBF_CUDA(cudaMemcpyAsync(c->qlo.p, c->box_lo.p, 3 * nt * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    IBF_CUDA(cudaMemcpyAsync(c->qhi.p, c->box_hi.p, 3 * nt * sizeof(double), cudaMemcpyDeviceToDevice, s));
   }
   tr.mark("boxes", s, nt);
   Tree tree;
@@ -1453,8 +1449,9 @@ static int broad_pass(ibf_ccd* c, int kind, const double* x0, const double* x1, 
     a.tree = tree;
     a.qorder = qorder;
     a.nq = nq;
-    a.qlo = c->qlo.p;
-    a.qhi = c->qhi.p;
+    // self-queries (EE, TT) read the tree's own primitive boxes
+    a.qlo = kind == 0 ? c->qlo.p : c->box_lo.p;
+    a.qhi = kind == 0 ? c->qhi.p : c->box_hi.p;
     a.kind = kind;
     a.qprim = (kind == 0) ? c->verts.p : ((kind == 1) ? c->edges.p : c->tris.p);
     a.tprim = (kind == 1) ? c->edges.p : c->tris.p;
